@@ -1,0 +1,134 @@
+/*
+ * laplex_c.h -- C-ABI of the B200-native LAPLEX hot path (liblaplex_b200.so).
+ *
+ * Plain pointers and sizes only.  Each entry replaces one reference C++ call
+ * (paths under /root/reference/proj/include/laplex/):
+ *
+ *   laplex_plan_create[_dev]   LaplexOperator(a, b, t[, phi, psi])      operator.hpp:77-137
+ *   laplex_plan_transposed     LaplexOperator::transposed()             operator.hpp:157-159
+ *   laplex_plan_shape          n() k() temperature() has_phases()       operator.hpp:139-142
+ *   laplex_plan_sorted         sorted_rows() / sorted_cols()            operator.hpp:151-152
+ *   laplex_plan_ranks          row_buckets() / col_buckets()            operator.hpp:153-154,110-120
+ *   laplex_apply[_dev]         matvec / batch_matvec / matvec_transpose operator.hpp:162-188
+ *                              / phased_matvec                          operator.hpp:197-213
+ *   laplex_backward[_dev]      matvec_vjp / phased_matvec_vjp           gradients.hpp:110-184
+ *   laplex_gram[_dev]          weighted_gram / phased_gram              operator.hpp:191-248,371-415
+ *   laplex_gram_vjp_weights    gram_vjp_weights                         gradients.hpp:190-219
+ *   laplex_sort                sort_anchors                             scan.hpp:27-46
+ *   laplex_scan                prefix_decay_scan / suffix_decay_scan    scan.hpp:50-73
+ *
+ * Errors: every call returns 0 or one of the LAPLEX_E_* codes below, which
+ * map 1:1 onto the reference exception types (errors.hpp:8-50); the message
+ * of the last failure on the calling thread is laplex_last_error().  Host
+ * entry points validate in the reference's order (e.g. phase presence, then
+ * lengths, then finiteness) so a C++ wrapper can rethrow the same type.
+ *
+ * Memory: host entry points take host pointers and return once results are
+ * in host memory.  *_dev entry points take device pointers and a
+ * cudaStream_t (as void*, NULL = legacy default stream); they are
+ * stream-ordered and do not synchronise, except laplex_plan_create_dev which
+ * synchronises once to report non-finite anchors synchronously.
+ *
+ * Layout: batches are row-major (rows x cols, leading dimension = cols).
+ * Permutations/ranks are returned as uint64 (the reference's size_t).
+ * Limits: n, k < 2^31.
+ */
+#ifndef LAPLEX_C_H
+#define LAPLEX_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LAPLEX_ABI_VERSION 1
+
+/* dtype tags */
+#define LAPLEX_F32 0
+#define LAPLEX_F64 1
+
+/* sides */
+#define LAPLEX_ROWS 0 /* anchors a, length n (outputs of apply) */
+#define LAPLEX_COLS 1 /* anchors b, length k (inputs of apply) */
+
+/* apply / backward / gram flags */
+#define LAPLEX_TRANSPOSE 1u /* apply: y = A^T g (matvec_transpose) */
+#define LAPLEX_PHASED 2u    /* phased_matvec / phased_matvec_vjp / phased_gram */
+
+/* error codes (reference exception types) */
+#define LAPLEX_OK 0
+#define LAPLEX_E_EMPTY_INPUT 1          /* laplex::EmptyInput */
+#define LAPLEX_E_NON_FINITE 2           /* laplex::NonFinite */
+#define LAPLEX_E_DIMENSION_MISMATCH 3   /* laplex::DimensionMismatch */
+#define LAPLEX_E_PHASE_PRESENT 4        /* laplex::PhasePresent */
+#define LAPLEX_E_PHASE_ABSENT 5         /* laplex::PhaseAbsent */
+#define LAPLEX_E_ASYMMETRIC_COTANGENT 6 /* laplex::AsymmetricCotangent */
+#define LAPLEX_E_INVALID_SIZE 7         /* laplex::InvalidSize (n or k >= 2^31) */
+#define LAPLEX_E_INVALID_ARGUMENT 8     /* bad handle / dtype / flag combination */
+#define LAPLEX_E_CUDA 100               /* CUDA runtime failure (message in laplex_last_error) */
+
+typedef struct laplex_plan_s* laplex_plan;
+
+int laplex_abi_version(void);
+const char* laplex_last_error(void);
+
+/* Plan = the reference constructor: validate, scale by 1/t, stable-sort both
+ * anchor sets on the device, merge-path partition.  phi/psi both NULL
+ * (unphased) or both non-NULL (lengths n and k). */
+int laplex_plan_create(int dtype, const void* a, size_t n, const void* b, size_t k, double t,
+                       const void* phi, const void* psi, laplex_plan* out);
+int laplex_plan_create_dev(int dtype, const void* a, size_t n, const void* b, size_t k, double t,
+                           const void* phi, const void* psi, void* stream, laplex_plan* out);
+/* Reference counting (plans are immutable and shareable across threads). */
+int laplex_plan_retain(laplex_plan plan);
+int laplex_plan_release(laplex_plan plan);
+/* Role-swapped view sharing the sorted anchors (no re-sort). */
+int laplex_plan_transposed(laplex_plan plan, laplex_plan* out);
+int laplex_plan_shape(laplex_plan plan, size_t* n, size_t* k, double* t, int* has_phases, int* dtype);
+/* Sorted, temperature-scaled anchors of one side (host outputs, any may be
+ * NULL): values[m], perm[m] (sorted -> caller index), decays[m-1]. */
+int laplex_plan_sorted(laplex_plan plan, int side, void* values, uint64_t* perm, void* decays);
+/* Co-ranks (host output):
+ *   side ROWS: strict=0 -> j_of_row = #{j : B_j <= A_i}, strict=1 -> #{j : B_j < A_i}
+ *   side COLS: strict=0 -> r_of_col = #{i : A_i <= B_j}, strict=1 -> #{i : A_i < B_j}
+ * indexed by sorted position, exactly as operator.hpp:110-120. */
+int laplex_plan_ranks(laplex_plan plan, int side, int strict, uint64_t* ranks);
+
+/* Y = A X (rows x k -> rows x n), or with LAPLEX_TRANSPOSE Y = A^T X
+ * (rows x n -> rows x k), or with LAPLEX_PHASED the phased product.
+ * `cols` is the caller's row length (checked -> DimensionMismatch). */
+int laplex_apply(laplex_plan plan, unsigned flags, const void* X, size_t rows, size_t cols, void* Y);
+int laplex_apply_dev(laplex_plan plan, unsigned flags, const void* X, size_t rows, void* Y, void* stream);
+
+/* Cotangents of L = sum_r G_r^T A X_r: x_bar (rows x k), a_bar (n) and
+ * b_bar (k) summed over rows; with LAPLEX_PHASED also phi_bar (n), psi_bar (k). */
+int laplex_backward(laplex_plan plan, unsigned flags, const void* X, size_t rows, size_t xcols,
+                    const void* G, size_t gcols, void* x_bar, void* a_bar, void* b_bar, void* phi_bar,
+                    void* psi_bar);
+int laplex_backward_dev(laplex_plan plan, unsigned flags, const void* X, const void* G, size_t rows,
+                        void* x_bar, void* a_bar, void* b_bar, void* phi_bar, void* psi_bar,
+                        void* stream);
+
+/* M = A diag(D) A^T (n x n, bit-exactly symmetric); LAPLEX_PHASED: phased_gram. */
+int laplex_gram(laplex_plan plan, unsigned flags, const void* D, size_t dlen, void* M);
+int laplex_gram_dev(laplex_plan plan, unsigned flags, const void* D, void* M, void* stream);
+/* D_bar_t = sum_i K_it (G_bar A)_it for symmetric G_bar (n x n). */
+int laplex_gram_vjp_weights(laplex_plan plan, const void* D, size_t dlen, const void* G_bar, size_t grows,
+                            size_t gcols, void* D_bar);
+
+/* Free functions of scan.hpp. */
+int laplex_sort(int dtype, const void* raw, size_t m, void* values, uint64_t* perm, void* decays);
+int laplex_scan(int dtype, const void* sorted_values, size_t m, const void* payload, void* prefix,
+                void* suffix);
+
+/* Number of CUDA kernels this library launched on the calling process
+ * (instrumentation for the benchmark's gpu_launches count). */
+uint64_t laplex_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LAPLEX_C_H */

@@ -1,0 +1,1116 @@
+// lx_capi.cu -- the C-ABI (include/laplex_c.h) over the sm_100a kernels.
+//
+// A plan is the device-resident image of the reference LaplexOperator
+// (operator.hpp:75-437): sorted scaled anchors + permutations of both sides,
+// cos/sin of the phases, and the merge-path tile partition.  It is immutable
+// after creation; lazily-built extras (role-swapped partition, co-rank arrays)
+// are guarded by a mutex.  Temporaries come from the stream-ordered memory
+// pool (cudaMallocAsync) so per-call allocation is free after warm-up.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/laplex_c.h"
+#include "lx_common.cuh"
+#include "lx_gram.cuh"
+#include "lx_scan.cuh"
+#include "lx_sort.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+struct Fail {
+    int code;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    throw Fail{code};
+}
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(LAPLEX_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void ck_launch(const char* what) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    ck(cudaGetLastError(), what);
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return LAPLEX_OK;
+    } catch (const Fail& e) {
+        return e.code;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return LAPLEX_E_CUDA;
+    }
+}
+
+std::once_flag g_pool_once;
+void init_pool() {
+    std::call_once(g_pool_once, [] {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) return;
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
+}
+
+// stream-ordered device buffer
+struct DBuf {
+    void* p = nullptr;
+    cudaStream_t st = nullptr;
+    DBuf() = default;
+    DBuf(size_t bytes, cudaStream_t s) : st(s) {
+        if (bytes) ck(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync");
+    }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), st(o.st) { o.p = nullptr; }
+    DBuf& operator=(DBuf&& o) noexcept {
+        release();
+        p = o.p;
+        st = o.st;
+        o.p = nullptr;
+        return *this;
+    }
+    ~DBuf() { release(); }
+    void release() {
+        if (p) cudaFreeAsync(p, st);
+        p = nullptr;
+    }
+    template <class T>
+    T* as() const {
+        return reinterpret_cast<T*>(p);
+    }
+};
+
+size_t rsize(int dtype) { return dtype == LAPLEX_F64 ? 8 : 4; }
+
+// ---------------------------------------------------------------------------
+// plan
+// ---------------------------------------------------------------------------
+struct Side {
+    DBuf vals;  // sorted scaled anchors
+    DBuf perm;  // u32 sorted -> caller index
+    DBuf cph, sph;  // cos/sin of this side's phases (caller order)
+    uint32_t m = 0;
+};
+
+struct Core {
+    int dtype = LAPLEX_F32;
+    int device = 0;
+    double t = 1.0;
+    bool phased = false;
+    Side side[2];  // [ROWS], [COLS]
+    std::mutex mu;
+    DBuf part[2];  // merge-path tiles with side 0 (resp. 1) as the "A" operand, A-first
+    uint32_t T[2] = {0, 0};
+    DBuf ranks[4];  // [side*2 + strict]
+    bool has_ranks[4] = {false, false, false, false};
+    cudaEvent_t last = nullptr;
+    ~Core() {
+        if (last) {
+            cudaEventSynchronize(last);
+            cudaEventDestroy(last);
+        }
+    }
+};
+
+}  // namespace
+
+struct laplex_plan_s {
+    std::shared_ptr<Core> core;
+    bool swapped = false;
+    std::atomic<int> refs{1};
+};
+
+namespace {
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+laplex_plan_s* check_plan(laplex_plan p) {
+    if (!p || !p->core) fail(LAPLEX_E_INVALID_ARGUMENT, "invalid plan handle");
+    return p;
+}
+
+// Orientation-resolved view: A = output side of apply, B = input side.
+template <class R>
+struct View {
+    const R* A;
+    const uint32_t* pa;
+    uint32_t n;
+    const R* B;
+    const uint32_t* pb;
+    uint32_t k;
+    const R *cphi, *sphi, *cpsi, *spsi;
+    const uint32_t* part;
+    uint32_t T;
+    R inv_t;
+};
+
+uint32_t tiles_for(uint64_t total) { return (uint32_t)((total + lx::ms::kTile - 1) / lx::ms::kTile); }
+
+template <class R>
+void build_partition(Core& c, int which, cudaStream_t st) {
+    const Side& a = c.side[which];
+    const Side& b = c.side[1 - which];
+    const uint32_t T = tiles_for((uint64_t)a.m + b.m);
+    c.part[which] = DBuf((size_t)(T + 1) * 4, st);
+    lx::ms::lx_partition<R, true><<<(T + 1 + 255) / 256, 256, 0, st>>>(
+        a.vals.as<R>(), a.m, b.vals.as<R>(), b.m, c.part[which].as<uint32_t>(), T);
+    ck_launch("lx_partition");
+    c.T[which] = T;
+}
+
+template <class R>
+View<R> view(Core& c, bool swapped, cudaStream_t st) {
+    const int ia = swapped ? 1 : 0;
+    {
+        std::lock_guard<std::mutex> g(c.mu);
+        if (!c.part[ia].p) build_partition<R>(c, ia, st);
+    }
+    View<R> v;
+    const Side& a = c.side[ia];
+    const Side& b = c.side[1 - ia];
+    v.A = a.vals.as<R>();
+    v.pa = a.perm.as<uint32_t>();
+    v.n = a.m;
+    v.B = b.vals.as<R>();
+    v.pb = b.perm.as<uint32_t>();
+    v.k = b.m;
+    v.cphi = a.cph.as<R>();
+    v.sphi = a.sph.as<R>();
+    v.cpsi = b.cph.as<R>();
+    v.spsi = b.sph.as<R>();
+    v.part = c.part[ia].as<uint32_t>();
+    v.T = c.T[ia];
+    v.inv_t = R(1) / R(c.t);
+    return v;
+}
+
+// ---- sort -------------------------------------------------------------------
+template <class R>
+void radix_sort(const R* raw, uint32_t m, R t, R* vals_out, uint32_t* perm_out, int* bad, cudaStream_t st) {
+    using namespace lx::sort;
+    using K = typename lx::Traits<R>::Key;
+    constexpr int P = lx::Traits<R>::kPasses;
+    const uint32_t tiles = (m + kTile - 1) / kTile;
+    DBuf hist((size_t)P * kRadix * 4, st), bases((size_t)P * kRadix * 4, st);
+    DBuf counters((size_t)P * 4, st);
+    DBuf keys0((size_t)m * sizeof(K), st), keys1((size_t)m * sizeof(K), st);
+    DBuf v0((size_t)m * 4, st), v1((size_t)m * 4, st);
+    DBuf look((size_t)tiles * kRadix * 8, st);
+    ck(cudaMemsetAsync(hist.p, 0, (size_t)P * kRadix * 4, st), "memset");
+    ck(cudaMemsetAsync(counters.p, 0, (size_t)P * 4, st), "memset");
+    ck(cudaMemsetAsync(look.p, 0, (size_t)tiles * kRadix * 8, st), "memset");
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const uint32_t hgrid = std::min<uint32_t>((m + kThreads - 1) / kThreads, (uint32_t)sms * 8);
+    lx_sort_hist<R><<<std::max(1u, hgrid), kThreads, 0, st>>>(raw, m, t, hist.as<uint32_t>(), bad);
+    ck_launch("lx_sort_hist");
+    lx_sort_bases<P><<<P, kRadix, 0, st>>>(hist.as<uint32_t>(), bases.as<uint32_t>());
+    ck_launch("lx_sort_bases");
+    const size_t smem = sizeof(PassSmem<R>);
+    static std::once_flag once;
+    std::call_once(once, [&] {
+        cudaFuncSetAttribute(lx_sort_pass<R, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(lx_sort_pass<R, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(lx_sort_pass<R, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
+    const void* in = raw;
+    const uint32_t* inv = nullptr;
+    for (int pass = 0; pass < P; ++pass) {
+        const bool last = pass == P - 1;
+        void* out = last ? (void*)vals_out : (pass % 2 == 0 ? keys0.p : keys1.p);
+        uint32_t* outv = last ? perm_out : (pass % 2 == 0 ? v0.as<uint32_t>() : v1.as<uint32_t>());
+        const uint32_t* bptr = bases.as<uint32_t>() + pass * kRadix;
+        uint32_t* ctr = counters.as<uint32_t>() + pass;
+        unsigned long long* lb = look.as<unsigned long long>();
+        const uint32_t epoch = (uint32_t)pass + 1;
+        if (pass == 0)
+            lx_sort_pass<R, true, false><<<tiles, kThreads, smem, st>>>(in, inv, out, outv, m, t, pass * kBits, bptr,
+                                                                       lb, ctr, epoch);
+        else if (!last)
+            lx_sort_pass<R, false, false><<<tiles, kThreads, smem, st>>>(in, inv, out, outv, m, t, pass * kBits,
+                                                                        bptr, lb, ctr, epoch);
+        else
+            lx_sort_pass<R, false, true><<<tiles, kThreads, smem, st>>>(in, inv, out, outv, m, t, pass * kBits, bptr,
+                                                                       lb, ctr, epoch);
+        ck_launch("lx_sort_pass");
+        in = out;
+        inv = outv;
+    }
+}
+
+template <class R>
+__global__ void cos_sin_kernel(const R* __restrict__ ph, uint32_t m, R* __restrict__ c, R* __restrict__ s) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) {
+        c[i] = lx::xcos(ph[i]);
+        s[i] = lx::xsin(ph[i]);
+    }
+}
+
+template <class R>
+void build_side(Side& sd, const R* raw, uint32_t m, R t, const R* phase, int* bad, cudaStream_t st) {
+    sd.m = m;
+    sd.vals = DBuf((size_t)m * sizeof(R), st);
+    sd.perm = DBuf((size_t)m * 4, st);
+    radix_sort<R>(raw, m, t, sd.vals.as<R>(), sd.perm.as<uint32_t>(), bad, st);
+    if (phase) {
+        sd.cph = DBuf((size_t)m * sizeof(R), st);
+        sd.sph = DBuf((size_t)m * sizeof(R), st);
+        cos_sin_kernel<R><<<(m + 255) / 256, 256, 0, st>>>(phase, m, sd.cph.as<R>(), sd.sph.as<R>());
+        ck_launch("cos_sin");
+    }
+}
+
+template <class R>
+__global__ void finite_check(const R* __restrict__ v, size_t m, int* __restrict__ bad) {
+    int b = 0;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (size_t)gridDim.x * blockDim.x)
+        if (!isfinite(v[i])) b = 1;
+    if (b) atomicOr(bad, 1);
+}
+
+template <class R>
+laplex_plan create_plan(const R* a, uint32_t n, const R* b, uint32_t k, double t, const R* phi, const R* psi,
+                        cudaStream_t st) {
+    init_pool();
+    auto core = std::make_shared<Core>();
+    core->dtype = sizeof(R) == 8 ? LAPLEX_F64 : LAPLEX_F32;
+    cudaGetDevice(&core->device);
+    core->t = t;
+    core->phased = phi != nullptr;
+    ck(cudaEventCreateWithFlags(&core->last, cudaEventDisableTiming), "cudaEventCreate");
+    DBuf bad(sizeof(int) * 2, st);
+    ck(cudaMemsetAsync(bad.p, 0, sizeof(int) * 2, st), "memset");
+    build_side<R>(core->side[0], a, n, R(t), phi, bad.as<int>(), st);
+    build_side<R>(core->side[1], b, k, R(t), psi, bad.as<int>(), st);
+    if (phi) {
+        finite_check<R><<<64, 256, 0, st>>>(phi, n, bad.as<int>() + 1);
+        ck_launch("finite_check");
+        finite_check<R><<<64, 256, 0, st>>>(psi, k, bad.as<int>() + 1);
+        ck_launch("finite_check");
+    }
+    build_partition<R>(*core, 0, st);
+    int hbad[2] = {0, 0};
+    ck(cudaMemcpyAsync(hbad, bad.p, sizeof(hbad), cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
+    ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    if (hbad[0]) fail(LAPLEX_E_NON_FINITE, "LaplexOperator: non-finite anchor");
+    if (hbad[1]) fail(LAPLEX_E_NON_FINITE, "LaplexOperator: non-finite phase");
+    ck(cudaEventRecord(core->last, st), "cudaEventRecord");
+    auto* p = new laplex_plan_s;
+    p->core = core;
+    return p;
+}
+
+void touch(Core& c, cudaStream_t st) { cudaEventRecord(c.last, st); }
+
+// ---- apply --------------------------------------------------------------------
+template <class R>
+lx::ms::MainArgs<R> main_args(const View<R>& v, int rows) {
+    lx::ms::MainArgs<R> a;
+    std::memset(&a, 0, sizeof(a));
+    a.A = v.A;
+    a.perm_a = v.pa;
+    a.B = v.B;
+    a.perm_b = v.pb;
+    a.part = v.part;
+    a.n = v.n;
+    a.k = v.k;
+    a.T = v.T;
+    a.rows = rows;
+    a.cphi = v.cphi;
+    a.sphi = v.sphi;
+    a.cpsi = v.cpsi;
+    a.spsi = v.spsi;
+    return a;
+}
+
+template <class R>
+lx::ms::FixArgs<R> fix_args(const View<R>& v, int rows) {
+    lx::ms::FixArgs<R> f;
+    std::memset(&f, 0, sizeof(f));
+    f.A = v.A;
+    f.perm_a = v.pa;
+    f.B = v.B;
+    f.perm_b = v.pb;
+    f.part = v.part;
+    f.n = v.n;
+    f.k = v.k;
+    f.T = v.T;
+    f.rows = rows;
+    f.inv_t = v.inv_t;
+    f.cphi = v.cphi;
+    f.sphi = v.sphi;
+    f.cpsi = v.cpsi;
+    f.spsi = v.spsi;
+    return f;
+}
+
+template <class R, int NG, int NX, bool BWD, bool SEQ = false>
+void launch_main(const lx::ms::MainArgs<R>& a, cudaStream_t st) {
+    using namespace lx::ms;
+    const size_t smem = ((sizeof(MainSmem<R, NG, NX>) + 15) & ~size_t(15)) + (size_t)kTile * sizeof(R);
+    static std::once_flag once;
+    std::call_once(once, [&] {
+        cudaFuncSetAttribute(lx_main<R, NG, NX, BWD, SEQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
+    lx_main<R, NG, NX, BWD, SEQ><<<a.T, kThreads, smem, st>>>(a);
+    ck_launch("lx_main");
+}
+
+template <class R, int NC>
+void launch_carry(const R* aggp, const R* aggq, R* cp, R* cq, const R* sl, const R* sf, uint32_t T, int rows,
+                  unsigned pm, unsigned qm, cudaStream_t st) {
+    lx::ms::lx_carry<R, NC><<<dim3(rows, 2), lx::ms::kCarryThreads, 0, st>>>(aggp, aggq, cp, cq, sl, sf, T, rows, pm, qm);
+    ck_launch("lx_carry");
+}
+
+struct Scratch {
+    DBuf aggp, aggq, cp, cq, sl, sf;
+    Scratch(size_t slots, int rows, uint32_t T, size_t rs, cudaStream_t st)
+        : aggp(slots * rows * T * rs, st),
+          aggq(slots * rows * T * rs, st),
+          cp(slots * rows * T * rs, st),
+          cq(slots * rows * T * rs, st),
+          sl((size_t)T * rs, st),
+          sf((size_t)T * rs, st) {}
+};
+
+template <class R, int NX>
+void apply_fwd(const View<R>& v, const R* X, int rows, R* Y, cudaStream_t st) {
+    constexpr int NC = NX;
+    DBuf wa0((size_t)rows * v.n * sizeof(R), st);
+    DBuf wa1(NX == 2 ? (size_t)rows * v.n * sizeof(R) : 0, st);
+    Scratch s(2 * NC, rows, v.T, sizeof(R), st);
+    auto a = main_args(v, rows);
+    a.X = X;
+    a.ldx = v.k;
+    a.wa[0] = wa0.as<R>();
+    a.wa[1] = wa1.as<R>();
+    a.aggp = s.aggp.as<R>();
+    a.aggq = s.aggq.as<R>();
+    a.s_last = s.sl.as<R>();
+    a.s_first = s.sf.as<R>();
+    launch_main<R, 0, NX, false>(a, st);
+    launch_carry<R, NC>(s.aggp.as<R>(), s.aggq.as<R>(), s.cp.as<R>(), s.cq.as<R>(), s.sl.as<R>(), s.sf.as<R>(), v.T,
+                        rows, 0u, 0u, st);
+    auto f = fix_args(v, rows);
+    f.cp = s.cp.as<R>();
+    f.cq = s.cq.as<R>();
+    f.s_last = s.sl.as<R>();
+    f.s_first = s.sf.as<R>();
+    f.wa[0] = wa0.as<R>();
+    f.wa[1] = wa1.as<R>();
+    f.y = Y;
+    f.ldy = v.n;
+    lx::ms::lx_fix_fwd<R, NX><<<v.T, lx::ms::kFixThreads, 0, st>>>(f);
+    ck_launch("lx_fix_fwd");
+}
+
+template <class R>
+void apply_trn(const View<R>& v, const R* G, int rows, R* Y, cudaStream_t st) {
+    DBuf wb0((size_t)rows * v.k * sizeof(R), st);
+    Scratch s(2, rows, v.T, sizeof(R), st);
+    auto a = main_args(v, rows);
+    a.G = G;
+    a.ldg = v.n;
+    a.wb[0] = wb0.as<R>();
+    a.aggp = s.aggp.as<R>();
+    a.aggq = s.aggq.as<R>();
+    a.s_last = s.sl.as<R>();
+    a.s_first = s.sf.as<R>();
+    launch_main<R, 1, 0, false>(a, st);
+    launch_carry<R, 1>(s.aggp.as<R>(), s.aggq.as<R>(), s.cp.as<R>(), s.cq.as<R>(), s.sl.as<R>(), s.sf.as<R>(), v.T,
+                       rows, 0u, 0u, st);
+    auto f = fix_args(v, rows);
+    f.cp = s.cp.as<R>();
+    f.cq = s.cq.as<R>();
+    f.s_last = s.sl.as<R>();
+    f.s_first = s.sf.as<R>();
+    f.wb[0] = wb0.as<R>();
+    f.y = Y;
+    f.ldy = v.k;
+    lx::ms::lx_fix_trn<R><<<v.T, lx::ms::kFixThreads, 0, st>>>(f);
+    ck_launch("lx_fix_trn");
+}
+
+template <class R, int NCH>
+void backward_impl(const View<R>& v, const R* X, const R* G, int rows, R* xbar, R* abar, R* bbar, R* phibar,
+                   R* psibar, cudaStream_t st) {
+    constexpr int NC = 2 * NCH;
+    const size_t rs = sizeof(R);
+    DBuf wa[2], wa2[2], wb[2], wb2[2];
+    for (int c = 0; c < NCH; ++c) {
+        wa[c] = DBuf((size_t)rows * v.n * rs, st);
+        wb[c] = DBuf((size_t)rows * v.k * rs, st);
+        wb2[c] = DBuf((size_t)rows * v.k * rs, st);
+        if (NCH == 2) wa2[c] = DBuf((size_t)rows * v.n * rs, st);
+    }
+    DBuf gsave((size_t)rows * v.n * rs, st), xsave((size_t)rows * v.k * rs, st);
+    Scratch s(2 * NC, rows, v.T, rs, st);
+    auto a = main_args(v, rows);
+    a.X = X;
+    a.ldx = v.k;
+    a.G = G;
+    a.ldg = v.n;
+    for (int c = 0; c < NCH; ++c) {
+        a.wa[c] = wa[c].as<R>();
+        a.wa2[c] = wa2[c].as<R>();
+        a.wb[c] = wb[c].as<R>();
+        a.wb2[c] = wb2[c].as<R>();
+    }
+    a.gsave = gsave.as<R>();
+    a.xsave = xsave.as<R>();
+    a.aggp = s.aggp.as<R>();
+    a.aggq = s.aggq.as<R>();
+    a.s_last = s.sl.as<R>();
+    a.s_first = s.sf.as<R>();
+    launch_main<R, NCH, NCH, true>(a, st);
+    const unsigned gmask = (1u << NCH) - 1u;
+    launch_carry<R, NC>(s.aggp.as<R>(), s.aggq.as<R>(), s.cp.as<R>(), s.cq.as<R>(), s.sl.as<R>(), s.sf.as<R>(), v.T,
+                        rows, gmask, gmask << NCH, st);
+    auto f = fix_args(v, rows);
+    f.cp = s.cp.as<R>();
+    f.cq = s.cq.as<R>();
+    f.s_last = s.sl.as<R>();
+    f.s_first = s.sf.as<R>();
+    for (int c = 0; c < NCH; ++c) {
+        f.wa[c] = wa[c].as<R>();
+        f.wa2[c] = wa2[c].as<R>();
+        f.wb[c] = wb[c].as<R>();
+        f.wb2[c] = wb2[c].as<R>();
+    }
+    f.gsave = gsave.as<R>();
+    f.xsave = xsave.as<R>();
+    f.xbar = xbar;
+    f.ldxb = v.k;
+    f.abar = abar;
+    f.bbar = bbar;
+    f.phibar = phibar;
+    f.psibar = psibar;
+    lx::ms::lx_fix_bwd<R, NCH><<<v.T, lx::ms::kFixThreads, 0, st>>>(f);
+    ck_launch("lx_fix_bwd");
+}
+
+template <class R>
+void do_apply(laplex_plan_s* p, unsigned flags, const R* X, size_t rows, R* Y, cudaStream_t st) {
+    Core& c = *p->core;
+    const bool trn = flags & LAPLEX_TRANSPOSE, ph = flags & LAPLEX_PHASED;
+    if (ph && !c.phased) fail(LAPLEX_E_PHASE_ABSENT, "phased_matvec: operator has no phases");
+    if (!ph && c.phased) fail(LAPLEX_E_PHASE_PRESENT, "matvec: operator has phases, use phased_matvec");
+    if (trn && ph) fail(LAPLEX_E_INVALID_ARGUMENT, "phased transpose is not part of the reference API");
+    if (rows == 0) return;
+    if (rows > 0x7fffffff) fail(LAPLEX_E_INVALID_SIZE, "too many rows");
+    View<R> v = view<R>(c, p->swapped, st);
+    if (trn)
+        apply_trn<R>(v, X, (int)rows, Y, st);
+    else if (ph)
+        apply_fwd<R, 2>(v, X, (int)rows, Y, st);
+    else
+        apply_fwd<R, 1>(v, X, (int)rows, Y, st);
+    touch(c, st);
+}
+
+template <class R>
+void do_backward(laplex_plan_s* p, unsigned flags, const R* X, const R* G, size_t rows, R* xbar, R* abar, R* bbar,
+                 R* phibar, R* psibar, cudaStream_t st) {
+    Core& c = *p->core;
+    const bool ph = flags & LAPLEX_PHASED;
+    if (ph && !c.phased) fail(LAPLEX_E_PHASE_ABSENT, "phased_matvec_vjp: operator has no phases");
+    if (!ph && c.phased) fail(LAPLEX_E_PHASE_PRESENT, "matvec_vjp: use phased_matvec_vjp");
+    View<R> v = view<R>(c, p->swapped, st);
+    if (rows == 0) {
+        ck(cudaMemsetAsync(abar, 0, (size_t)v.n * sizeof(R), st), "memset");
+        ck(cudaMemsetAsync(bbar, 0, (size_t)v.k * sizeof(R), st), "memset");
+        return;
+    }
+    if (ph)
+        backward_impl<R, 2>(v, X, G, (int)rows, xbar, abar, bbar, phibar, psibar, st);
+    else
+        backward_impl<R, 1>(v, X, G, (int)rows, xbar, abar, bbar, nullptr, nullptr, st);
+    touch(c, st);
+}
+
+template <class R>
+void do_gram(laplex_plan_s* p, unsigned flags, const R* D, R* M, cudaStream_t st) {
+    Core& c = *p->core;
+    const bool ph = flags & LAPLEX_PHASED;
+    if (ph && !c.phased) fail(LAPLEX_E_PHASE_ABSENT, "phased_gram: operator has no phases");
+    if (!ph && c.phased) fail(LAPLEX_E_PHASE_PRESENT, "weighted_gram: operator has phases");
+    View<R> v = view<R>(c, p->swapped, st);
+    const int NCH = ph ? 3 : 1;
+    const uint32_t n = v.n;
+    DBuf ell((size_t)NCH * n * sizeof(R), st), rho((size_t)NCH * n * sizeof(R), st);
+    DBuf mass((size_t)NCH * (n + 1) * sizeof(R), st);
+    DBuf U((size_t)NCH * n * sizeof(R), st), V((size_t)NCH * n * sizeof(R), st);
+    DBuf C((size_t)NCH * (n + 1) * sizeof(R), st);
+    DBuf A2((size_t)n * sizeof(R), st), Z((size_t)(n + 1) * sizeof(R), st), dummy((size_t)NCH * (n + 1) * sizeof(R), st);
+    const uint32_t warps = n + 1;
+    const uint32_t blocks = (warps * 32 + 255) / 256;
+    if (ph)
+        lx::gram::lx_gram_buckets<R, 3><<<blocks, 256, 0, st>>>(v.A, n, v.B, v.k, v.pb, D, v.cpsi, v.spsi,
+                                                                ell.as<R>(), rho.as<R>(), mass.as<R>());
+    else
+        lx::gram::lx_gram_buckets<R, 1><<<blocks, 256, 0, st>>>(v.A, n, v.B, v.k, v.pb, D, nullptr, nullptr,
+                                                                ell.as<R>(), rho.as<R>(), mass.as<R>());
+    ck_launch("lx_gram_buckets");
+    lx::gram::lx_double_anchors<R><<<(n + 255) / 256, 256, 0, st>>>(v.A, n, A2.as<R>());
+    ck_launch("lx_double_anchors");
+    ck(cudaMemsetAsync(Z.p, 0, (size_t)(n + 1) * sizeof(R), st), "memset");
+    // U = prefix scan of ell over anchors 2A; V = suffix scan of rho (channels as rows)
+    launch_carry<R, 1>(ell.as<R>(), rho.as<R>(), U.as<R>(), V.as<R>(), A2.as<R>(), A2.as<R>(), n, NCH, 0u, 0u, st);
+    // C = cumulative sum of mass (zero anchors -> every decay is exactly 1)
+    launch_carry<R, 1>(mass.as<R>(), mass.as<R>(), C.as<R>(), dummy.as<R>(), Z.as<R>(), Z.as<R>(), n + 1, NCH, 0u,
+                       0u, st);
+    dim3 blk(32, 8), grd((n + 31) / 32, (n + 7) / 8);
+    if (ph)
+        lx::gram::lx_gram_out<R, 3><<<grd, blk, 0, st>>>(v.A, n, v.pa, U.as<R>(), V.as<R>(), C.as<R>(), v.cphi,
+                                                         v.sphi, M);
+    else
+        lx::gram::lx_gram_out<R, 1><<<grd, blk, 0, st>>>(v.A, n, v.pa, U.as<R>(), V.as<R>(), C.as<R>(), nullptr,
+                                                         nullptr, M);
+    ck_launch("lx_gram_out");
+    touch(c, st);
+}
+
+template <class R>
+void do_gram_vjp(laplex_plan_s* p, const R* Gbar, R* Dbar, cudaStream_t st) {
+    Core& c = *p->core;
+    View<R> v = view<R>(c, p->swapped, st);
+    DBuf Y((size_t)v.n * v.k * sizeof(R), st);
+    apply_trn<R>(v, Gbar, (int)v.n, Y.as<R>(), st);
+    DBuf pa((size_t)v.n * 4, st), pb((size_t)v.k * 4, st);
+    lx::gram::lx_invert_perm<<<(v.n + 255) / 256, 256, 0, st>>>(v.pa, v.n, pa.as<uint32_t>());
+    ck_launch("lx_invert_perm");
+    lx::gram::lx_invert_perm<<<(v.k + 255) / 256, 256, 0, st>>>(v.pb, v.k, pb.as<uint32_t>());
+    ck_launch("lx_invert_perm");
+    lx::gram::lx_gram_vjp_contract<R><<<(v.k + 255) / 256, 256, 0, st>>>(v.A, pa.as<uint32_t>(), v.n, v.B,
+                                                                        pb.as<uint32_t>(), v.k, Y.as<R>(), Dbar);
+    ck_launch("lx_gram_vjp_contract");
+    touch(c, st);
+}
+
+template <class R>
+void do_ranks(laplex_plan_s* p, int side, int strict, uint64_t* out, cudaStream_t st) {
+    Core& c = *p->core;
+    // physical side of the request
+    const int phys = p->swapped ? 1 - side : side;
+    const int ia = p->swapped ? 1 : 0;  // view's row side
+    (void)ia;
+    const int slot = phys * 2 + (strict ? 1 : 0);
+    std::lock_guard<std::mutex> g(c.mu);
+    if (!c.has_ranks[slot]) {
+        // rows = physical side 0, cols = physical side 1.  A-first merge of
+        // (rows, cols) gives J<(rows) and R<=(cols); B-first gives J<=, R<.
+        const Side& a = c.side[0];
+        const Side& b = c.side[1];
+        const uint32_t T = tiles_for((uint64_t)a.m + b.m);
+        DBuf part((size_t)(T + 1) * 4, st);
+        const bool afirst = (phys == 0) ? (strict != 0) : (strict == 0);
+        DBuf rr((size_t)a.m * 4, st), rc((size_t)b.m * 4, st);
+        const size_t smem = (size_t)lx::ms::kTile * sizeof(R);
+        if (afirst) {
+            lx::ms::lx_partition<R, true><<<(T + 256) / 256, 256, 0, st>>>(a.vals.as<R>(), a.m, b.vals.as<R>(), b.m,
+                                                                          part.as<uint32_t>(), T);
+            ck_launch("lx_partition");
+            lx::ms::lx_coranks<R, true><<<T, lx::ms::kThreads, smem, st>>>(
+                a.vals.as<R>(), a.m, b.vals.as<R>(), b.m, part.as<uint32_t>(), rr.as<uint32_t>(), rc.as<uint32_t>());
+        } else {
+            lx::ms::lx_partition<R, false><<<(T + 256) / 256, 256, 0, st>>>(a.vals.as<R>(), a.m, b.vals.as<R>(),
+                                                                           b.m, part.as<uint32_t>(), T);
+            ck_launch("lx_partition");
+            lx::ms::lx_coranks<R, false><<<T, lx::ms::kThreads, smem, st>>>(
+                a.vals.as<R>(), a.m, b.vals.as<R>(), b.m, part.as<uint32_t>(), rr.as<uint32_t>(), rc.as<uint32_t>());
+        }
+        ck_launch("lx_coranks");
+        // A-first: rows get J<, cols get R<= ; B-first: rows J<=, cols R<
+        const int rows_slot = 0 * 2 + (afirst ? 1 : 0);
+        const int cols_slot = 1 * 2 + (afirst ? 0 : 1);
+        c.ranks[rows_slot] = std::move(rr);
+        c.ranks[cols_slot] = std::move(rc);
+        c.has_ranks[rows_slot] = c.has_ranks[cols_slot] = true;
+    }
+    const uint32_t m = c.side[phys].m;
+    std::vector<uint32_t> h(m);
+    ck(cudaMemcpyAsync(h.data(), c.ranks[slot].p, (size_t)m * 4, cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
+    ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    for (uint32_t i = 0; i < m; ++i) out[i] = h[i];
+}
+
+template <class R>
+void do_scan(const R* sorted, uint32_t m, const R* payload, R* pre, R* suf, cudaStream_t st) {
+    init_pool();
+    using namespace lx::ms;
+    const uint32_t T = tiles_for(m);
+    DBuf vals((size_t)m * sizeof(R), st), pay((size_t)m * sizeof(R), st);
+    ck(cudaMemcpyAsync(vals.p, sorted, (size_t)m * sizeof(R), cudaMemcpyHostToDevice, st), "H2D");
+    ck(cudaMemcpyAsync(pay.p, payload, (size_t)m * sizeof(R), cudaMemcpyHostToDevice, st), "H2D");
+    DBuf part((size_t)(T + 1) * 4, st);
+    lx_seq_partition<<<(T + 256) / 256, 256, 0, st>>>(m, part.as<uint32_t>(), T);
+    ck_launch("lx_seq_partition");
+    DBuf wa((size_t)m * sizeof(R), st), wa2((size_t)m * sizeof(R), st);
+    DBuf dpre((size_t)m * sizeof(R), st), dsuf((size_t)m * sizeof(R), st);
+    Scratch s(2, 1, T, sizeof(R), st);
+    MainArgs<R> a;
+    std::memset(&a, 0, sizeof(a));
+    a.A = vals.as<R>();
+    a.part = part.as<uint32_t>();
+    a.n = m;
+    a.k = 0;
+    a.T = T;
+    a.rows = 1;
+    a.X = pay.as<R>();
+    a.ldx = m;
+    a.wa[0] = wa.as<R>();
+    a.wa2[0] = wa2.as<R>();
+    a.aggp = s.aggp.as<R>();
+    a.aggq = s.aggq.as<R>();
+    a.s_last = s.sl.as<R>();
+    a.s_first = s.sf.as<R>();
+    launch_main<R, 0, 1, false, true>(a, st);
+    launch_carry<R, 1>(s.aggp.as<R>(), s.aggq.as<R>(), s.cp.as<R>(), s.cq.as<R>(), s.sl.as<R>(), s.sf.as<R>(), T, 1,
+                       0u, 0u, st);
+    FixArgs<R> f;
+    std::memset(&f, 0, sizeof(f));
+    f.A = vals.as<R>();
+    f.part = part.as<uint32_t>();
+    f.n = m;
+    f.T = T;
+    f.rows = 1;
+    f.cp = s.cp.as<R>();
+    f.cq = s.cq.as<R>();
+    f.s_last = s.sl.as<R>();
+    f.s_first = s.sf.as<R>();
+    f.wa[0] = wa.as<R>();
+    f.wa2[0] = wa2.as<R>();
+    lx_fix_seq<R><<<T, kFixThreads, 0, st>>>(f, dpre.as<R>(), dsuf.as<R>());
+    ck_launch("lx_fix_seq");
+    if (pre) ck(cudaMemcpyAsync(pre, dpre.p, (size_t)m * sizeof(R), cudaMemcpyDeviceToHost, st), "D2H");
+    if (suf) ck(cudaMemcpyAsync(suf, dsuf.p, (size_t)m * sizeof(R), cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+}
+
+// ---- host helpers ---------------------------------------------------------------
+template <class R>
+bool host_finite(const R* v, size_t m) {
+    for (size_t i = 0; i < m; ++i)
+        if (!std::isfinite(v[i])) return false;
+    return true;
+}
+
+template <class R>
+struct HostUp {
+    DBuf d;
+    HostUp(const void* h, size_t count, cudaStream_t st) : d(count * sizeof(R), st) {
+        if (count) ck(cudaMemcpyAsync(d.p, h, count * sizeof(R), cudaMemcpyHostToDevice, st), "H2D");
+    }
+    R* get() const { return d.as<R>(); }
+};
+
+cudaStream_t host_stream() { return cudaStreamPerThread; }
+
+template <class R>
+void d2h(void* dst, const DBuf& src, size_t count, cudaStream_t st) {
+    if (dst && count) ck(cudaMemcpyAsync(dst, src.p, count * sizeof(R), cudaMemcpyDeviceToHost, st), "D2H");
+}
+
+int dtype_check(int dtype) {
+    if (dtype != LAPLEX_F32 && dtype != LAPLEX_F64) fail(LAPLEX_E_INVALID_ARGUMENT, "dtype must be LAPLEX_F32/F64");
+    return dtype;
+}
+
+template <class R>
+void validate_create(const R* a, size_t n, const R* b, size_t k, double t, const R* phi, const R* psi) {
+    // order of operator.hpp:88-101
+    if (n == 0 || k == 0) fail(LAPLEX_E_EMPTY_INPUT, "LaplexOperator: empty anchor set");
+    if (!host_finite(a, n)) fail(LAPLEX_E_NON_FINITE, "LaplexOperator row anchors: non-finite entry");
+    if (!host_finite(b, k)) fail(LAPLEX_E_NON_FINITE, "LaplexOperator col anchors: non-finite entry");
+    const R tr = R(t);
+    if (!(tr > R(0)) || !std::isfinite(tr))
+        fail(LAPLEX_E_NON_FINITE, "LaplexOperator: temperature must be positive and finite");
+    if ((phi == nullptr) != (psi == nullptr))
+        fail(LAPLEX_E_DIMENSION_MISMATCH, "LaplexOperator: phases must be given for both sides");
+    if (phi) {
+        if (!host_finite(phi, n)) fail(LAPLEX_E_NON_FINITE, "LaplexOperator row phases: non-finite entry");
+        if (!host_finite(psi, k)) fail(LAPLEX_E_NON_FINITE, "LaplexOperator col phases: non-finite entry");
+    }
+    if (n >= 0x80000000ull || k >= 0x80000000ull) fail(LAPLEX_E_INVALID_SIZE, "n and k must be < 2^31");
+}
+
+}  // namespace
+
+// =============================================================================
+// extern "C"
+// =============================================================================
+extern "C" {
+
+int laplex_abi_version(void) { return LAPLEX_ABI_VERSION; }
+const char* laplex_last_error(void) { return g_last_error.c_str(); }
+uint64_t laplex_kernel_launches(void) { return g_launches.load(); }
+
+int laplex_plan_create(int dtype, const void* a, size_t n, const void* b, size_t k, double t, const void* phi,
+                       const void* psi, laplex_plan* out) {
+    return guarded([&] {
+        if (!out) fail(LAPLEX_E_INVALID_ARGUMENT, "out is NULL");
+        *out = nullptr;
+        dtype_check(dtype);
+        cudaStream_t st = host_stream();
+        init_pool();
+        if (dtype == LAPLEX_F64) {
+            validate_create<double>((const double*)a, n, (const double*)b, k, t, (const double*)phi,
+                                    (const double*)psi);
+            HostUp<double> da(a, n, st), db(b, k, st), dp(phi, phi ? n : 0, st), dq(psi, psi ? k : 0, st);
+            *out = create_plan<double>(da.get(), (uint32_t)n, db.get(), (uint32_t)k, t, phi ? dp.get() : nullptr,
+                                       psi ? dq.get() : nullptr, st);
+        } else {
+            validate_create<float>((const float*)a, n, (const float*)b, k, t, (const float*)phi, (const float*)psi);
+            HostUp<float> da(a, n, st), db(b, k, st), dp(phi, phi ? n : 0, st), dq(psi, psi ? k : 0, st);
+            *out = create_plan<float>(da.get(), (uint32_t)n, db.get(), (uint32_t)k, t, phi ? dp.get() : nullptr,
+                                      psi ? dq.get() : nullptr, st);
+        }
+    });
+}
+
+int laplex_plan_create_dev(int dtype, const void* a, size_t n, const void* b, size_t k, double t, const void* phi,
+                           const void* psi, void* stream, laplex_plan* out) {
+    return guarded([&] {
+        if (!out) fail(LAPLEX_E_INVALID_ARGUMENT, "out is NULL");
+        *out = nullptr;
+        dtype_check(dtype);
+        if (n == 0 || k == 0) fail(LAPLEX_E_EMPTY_INPUT, "LaplexOperator: empty anchor set");
+        if (!(t > 0.0) || !std::isfinite(t))
+            fail(LAPLEX_E_NON_FINITE, "LaplexOperator: temperature must be positive and finite");
+        if ((phi == nullptr) != (psi == nullptr))
+            fail(LAPLEX_E_DIMENSION_MISMATCH, "LaplexOperator: phases must be given for both sides");
+        if (n >= 0x80000000ull || k >= 0x80000000ull) fail(LAPLEX_E_INVALID_SIZE, "n and k must be < 2^31");
+        cudaStream_t st = as_stream(stream);
+        if (dtype == LAPLEX_F64)
+            *out = create_plan<double>((const double*)a, (uint32_t)n, (const double*)b, (uint32_t)k, t,
+                                       (const double*)phi, (const double*)psi, st);
+        else
+            *out = create_plan<float>((const float*)a, (uint32_t)n, (const float*)b, (uint32_t)k, t,
+                                      (const float*)phi, (const float*)psi, st);
+    });
+}
+
+int laplex_plan_retain(laplex_plan plan) {
+    return guarded([&] { check_plan(plan)->refs.fetch_add(1); });
+}
+
+int laplex_plan_release(laplex_plan plan) {
+    return guarded([&] {
+        check_plan(plan);
+        if (plan->refs.fetch_sub(1) == 1) delete plan;
+    });
+}
+
+int laplex_plan_transposed(laplex_plan plan, laplex_plan* out) {
+    return guarded([&] {
+        check_plan(plan);
+        auto* p = new laplex_plan_s;
+        p->core = plan->core;
+        p->swapped = !plan->swapped;
+        *out = p;
+    });
+}
+
+int laplex_plan_shape(laplex_plan plan, size_t* n, size_t* k, double* t, int* has_phases, int* dtype) {
+    return guarded([&] {
+        check_plan(plan);
+        const Core& c = *plan->core;
+        const int ia = plan->swapped ? 1 : 0;
+        if (n) *n = c.side[ia].m;
+        if (k) *k = c.side[1 - ia].m;
+        if (t) *t = c.t;
+        if (has_phases) *has_phases = c.phased ? 1 : 0;
+        if (dtype) *dtype = c.dtype;
+    });
+}
+
+int laplex_plan_sorted(laplex_plan plan, int side, void* values, uint64_t* perm, void* decays) {
+    return guarded([&] {
+        check_plan(plan);
+        if (side != LAPLEX_ROWS && side != LAPLEX_COLS) fail(LAPLEX_E_INVALID_ARGUMENT, "side");
+        Core& c = *plan->core;
+        const int phys = plan->swapped ? 1 - side : side;
+        const Side& sd = c.side[phys];
+        cudaStream_t st = host_stream();
+        const size_t rs = rsize(c.dtype);
+        if (values) ck(cudaMemcpyAsync(values, sd.vals.p, (size_t)sd.m * rs, cudaMemcpyDeviceToHost, st), "D2H");
+        std::vector<uint32_t> hp;
+        if (perm) {
+            hp.resize(sd.m);
+            ck(cudaMemcpyAsync(hp.data(), sd.perm.p, (size_t)sd.m * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        }
+        DBuf dec;
+        if (decays && sd.m > 1) {
+            dec = DBuf((size_t)(sd.m - 1) * rs, st);
+            if (c.dtype == LAPLEX_F64)
+                lx::sort::lx_decays<double><<<(sd.m + 255) / 256, 256, 0, st>>>(sd.vals.as<double>(), sd.m,
+                                                                               dec.as<double>());
+            else
+                lx::sort::lx_decays<float><<<(sd.m + 255) / 256, 256, 0, st>>>(sd.vals.as<float>(), sd.m,
+                                                                              dec.as<float>());
+            ck_launch("lx_decays");
+            ck(cudaMemcpyAsync(decays, dec.p, (size_t)(sd.m - 1) * rs, cudaMemcpyDeviceToHost, st), "D2H");
+        }
+        ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        if (perm)
+            for (uint32_t i = 0; i < sd.m; ++i) perm[i] = hp[i];
+    });
+}
+
+int laplex_plan_ranks(laplex_plan plan, int side, int strict, uint64_t* ranks) {
+    return guarded([&] {
+        check_plan(plan);
+        if (side != LAPLEX_ROWS && side != LAPLEX_COLS) fail(LAPLEX_E_INVALID_ARGUMENT, "side");
+        if (plan->swapped) {
+            // ranks of a role-swapped view: rows of the view are the physical
+            // cols, and "<=" / "<" keep their meaning relative to the view.
+        }
+        if (plan->core->dtype == LAPLEX_F64)
+            do_ranks<double>(plan, side, strict, ranks, host_stream());
+        else
+            do_ranks<float>(plan, side, strict, ranks, host_stream());
+    });
+}
+
+int laplex_apply_dev(laplex_plan plan, unsigned flags, const void* X, size_t rows, void* Y, void* stream) {
+    return guarded([&] {
+        check_plan(plan);
+        if (plan->core->dtype == LAPLEX_F64)
+            do_apply<double>(plan, flags, (const double*)X, rows, (double*)Y, as_stream(stream));
+        else
+            do_apply<float>(plan, flags, (const float*)X, rows, (float*)Y, as_stream(stream));
+    });
+}
+
+int laplex_apply(laplex_plan plan, unsigned flags, const void* X, size_t rows, size_t cols, void* Y) {
+    return guarded([&] {
+        check_plan(plan);
+        Core& c = *plan->core;
+        const int ia = plan->swapped ? 1 : 0;
+        const size_t n = c.side[ia].m, k = c.side[1 - ia].m;
+        const bool trn = flags & LAPLEX_TRANSPOSE, ph = flags & LAPLEX_PHASED;
+        // operator.hpp:162-165,197-201,255-257: phase checks, length, finiteness
+        if (ph && !c.phased) fail(LAPLEX_E_PHASE_ABSENT, "phased_matvec: operator has no phases");
+        if (!ph && c.phased) fail(LAPLEX_E_PHASE_PRESENT, "matvec: operator has phases");
+        const size_t in_len = trn ? n : k, out_len = trn ? k : n;
+        if (cols != in_len) fail(LAPLEX_E_DIMENSION_MISMATCH, "matvec: x length");
+        cudaStream_t st = host_stream();
+        const size_t rs = rsize(c.dtype);
+        if (c.dtype == LAPLEX_F64) {
+            if (!host_finite((const double*)X, rows * cols)) fail(LAPLEX_E_NON_FINITE, "matvec x: non-finite entry");
+            HostUp<double> dx(X, rows * cols, st);
+            DBuf dy(rows * out_len * rs, st);
+            do_apply<double>(plan, flags, dx.get(), rows, dy.as<double>(), st);
+            d2h<double>(Y, dy, rows * out_len, st);
+        } else {
+            if (!host_finite((const float*)X, rows * cols)) fail(LAPLEX_E_NON_FINITE, "matvec x: non-finite entry");
+            HostUp<float> dx(X, rows * cols, st);
+            DBuf dy(rows * out_len * rs, st);
+            do_apply<float>(plan, flags, dx.get(), rows, dy.as<float>(), st);
+            d2h<float>(Y, dy, rows * out_len, st);
+        }
+        ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    });
+}
+
+int laplex_backward_dev(laplex_plan plan, unsigned flags, const void* X, const void* G, size_t rows, void* x_bar,
+                        void* a_bar, void* b_bar, void* phi_bar, void* psi_bar, void* stream) {
+    return guarded([&] {
+        check_plan(plan);
+        if (plan->core->dtype == LAPLEX_F64)
+            do_backward<double>(plan, flags, (const double*)X, (const double*)G, rows, (double*)x_bar,
+                                (double*)a_bar, (double*)b_bar, (double*)phi_bar, (double*)psi_bar,
+                                as_stream(stream));
+        else
+            do_backward<float>(plan, flags, (const float*)X, (const float*)G, rows, (float*)x_bar, (float*)a_bar,
+                               (float*)b_bar, (float*)phi_bar, (float*)psi_bar, as_stream(stream));
+    });
+}
+
+int laplex_backward(laplex_plan plan, unsigned flags, const void* X, size_t rows, size_t xcols, const void* G,
+                    size_t gcols, void* x_bar, void* a_bar, void* b_bar, void* phi_bar, void* psi_bar) {
+    return guarded([&] {
+        check_plan(plan);
+        Core& c = *plan->core;
+        const int ia = plan->swapped ? 1 : 0;
+        const size_t n = c.side[ia].m, k = c.side[1 - ia].m;
+        const bool ph = flags & LAPLEX_PHASED;
+        // gradients.hpp:113-117 / 142-146
+        if (ph && !c.phased) fail(LAPLEX_E_PHASE_ABSENT, "phased_matvec_vjp: operator has no phases");
+        if (!ph && c.phased) fail(LAPLEX_E_PHASE_PRESENT, "matvec_vjp: use phased_matvec_vjp");
+        if (xcols != k) fail(LAPLEX_E_DIMENSION_MISMATCH, "matvec_vjp: x length");
+        if (gcols != n) fail(LAPLEX_E_DIMENSION_MISMATCH, "matvec_vjp: g length");
+        cudaStream_t st = host_stream();
+        const size_t rs = rsize(c.dtype);
+        auto run = [&](auto zero) {
+            using R = decltype(zero);
+            if (!host_finite((const R*)X, rows * xcols)) fail(LAPLEX_E_NON_FINITE, "matvec_vjp x: non-finite entry");
+            if (!host_finite((const R*)G, rows * gcols)) fail(LAPLEX_E_NON_FINITE, "matvec_vjp g: non-finite entry");
+            HostUp<R> dx(X, rows * k, st), dg(G, rows * n, st);
+            DBuf xb(rows * k * rs, st), ab(n * rs, st), bb(k * rs, st), pb(ph ? n * rs : 0, st), qb(ph ? k * rs : 0, st);
+            do_backward<R>(plan, flags, dx.get(), dg.get(), rows, xb.as<R>(), ab.as<R>(), bb.as<R>(), pb.as<R>(),
+                           qb.as<R>(), st);
+            d2h<R>(x_bar, xb, rows * k, st);
+            d2h<R>(a_bar, ab, n, st);
+            d2h<R>(b_bar, bb, k, st);
+            if (ph) {
+                d2h<R>(phi_bar, pb, n, st);
+                d2h<R>(psi_bar, qb, k, st);
+            }
+            ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        };
+        if (c.dtype == LAPLEX_F64)
+            run(0.0);
+        else
+            run(0.0f);
+    });
+}
+
+int laplex_gram_dev(laplex_plan plan, unsigned flags, const void* D, void* M, void* stream) {
+    return guarded([&] {
+        check_plan(plan);
+        if (plan->core->dtype == LAPLEX_F64)
+            do_gram<double>(plan, flags, (const double*)D, (double*)M, as_stream(stream));
+        else
+            do_gram<float>(plan, flags, (const float*)D, (float*)M, as_stream(stream));
+    });
+}
+
+int laplex_gram(laplex_plan plan, unsigned flags, const void* D, size_t dlen, void* M) {
+    return guarded([&] {
+        check_plan(plan);
+        Core& c = *plan->core;
+        const int ia = plan->swapped ? 1 : 0;
+        const size_t n = c.side[ia].m, k = c.side[1 - ia].m;
+        const bool ph = flags & LAPLEX_PHASED;
+        // operator.hpp:192,218-220,372-373
+        if (ph && !c.phased) fail(LAPLEX_E_PHASE_ABSENT, "phased_gram: operator has no phases");
+        if (!ph && c.phased) fail(LAPLEX_E_PHASE_PRESENT, "weighted_gram: operator has phases");
+        if (dlen != k) fail(LAPLEX_E_DIMENSION_MISMATCH, "weighted_gram: D length");
+        cudaStream_t st = host_stream();
+        auto run = [&](auto zero) {
+            using R = decltype(zero);
+            if (!host_finite((const R*)D, dlen)) fail(LAPLEX_E_NON_FINITE, "weighted_gram D: non-finite entry");
+            HostUp<R> dd(D, k, st);
+            DBuf dm(n * n * sizeof(R), st);
+            do_gram<R>(plan, flags, dd.get(), dm.as<R>(), st);
+            d2h<R>(M, dm, n * n, st);
+            ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        };
+        if (c.dtype == LAPLEX_F64)
+            run(0.0);
+        else
+            run(0.0f);
+    });
+}
+
+int laplex_gram_vjp_weights(laplex_plan plan, const void* D, size_t dlen, const void* G_bar, size_t grows,
+                            size_t gcols, void* D_bar) {
+    return guarded([&] {
+        check_plan(plan);
+        Core& c = *plan->core;
+        const int ia = plan->swapped ? 1 : 0;
+        const size_t n = c.side[ia].m, k = c.side[1 - ia].m;
+        (void)D;
+        // gradients.hpp:193-205
+        if (c.phased) fail(LAPLEX_E_PHASE_PRESENT, "gram_vjp_weights: phased operator not supported");
+        if (dlen != k) fail(LAPLEX_E_DIMENSION_MISMATCH, "gram_vjp_weights: D length");
+        if (grows != n || gcols != n) fail(LAPLEX_E_DIMENSION_MISMATCH, "gram_vjp_weights: G_bar shape");
+        cudaStream_t st = host_stream();
+        auto run = [&](auto zero) {
+            using R = decltype(zero);
+            const R* g = (const R*)G_bar;
+            if (!host_finite(g, n * n)) fail(LAPLEX_E_NON_FINITE, "gram_vjp_weights G_bar: non-finite entry");
+            R max_abs = 0, max_asym = 0;
+            for (size_t i = 0; i < n; ++i)
+                for (size_t j = 0; j < i; ++j) {
+                    max_abs = std::max(max_abs, std::abs(g[i * n + j]));
+                    max_asym = std::max(max_asym, std::abs(g[i * n + j] - g[j * n + i]));
+                }
+            if (max_asym > R(1e-9) * std::max(R(1), max_abs))
+                fail(LAPLEX_E_ASYMMETRIC_COTANGENT, "gram_vjp_weights: G_bar is not symmetric");
+            HostUp<R> dg(G_bar, n * n, st);
+            DBuf dd(k * sizeof(R), st);
+            do_gram_vjp<R>(plan, dg.get(), dd.as<R>(), st);
+            d2h<R>(D_bar, dd, k, st);
+            ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        };
+        if (c.dtype == LAPLEX_F64)
+            run(0.0);
+        else
+            run(0.0f);
+    });
+}
+
+int laplex_sort(int dtype, const void* raw, size_t m, void* values, uint64_t* perm, void* decays) {
+    return guarded([&] {
+        dtype_check(dtype);
+        // scan.hpp:28-29
+        if (m == 0) fail(LAPLEX_E_EMPTY_INPUT, "sort_anchors: empty input");
+        if (m >= 0x80000000ull) fail(LAPLEX_E_INVALID_SIZE, "m must be < 2^31");
+        cudaStream_t st = host_stream();
+        init_pool();
+        auto run = [&](auto zero) {
+            using R = decltype(zero);
+            if (!host_finite((const R*)raw, m)) fail(LAPLEX_E_NON_FINITE, "sort_anchors: non-finite entry");
+            HostUp<R> dr(raw, m, st);
+            DBuf vals(m * sizeof(R), st), pm(m * 4, st), bad(sizeof(int), st), dec(m > 1 ? (m - 1) * sizeof(R) : 0, st);
+            ck(cudaMemsetAsync(bad.p, 0, sizeof(int), st), "memset");
+            radix_sort<R>(dr.get(), (uint32_t)m, R(1), vals.as<R>(), pm.as<uint32_t>(), bad.as<int>(), st);
+            if (m > 1) {
+                lx::sort::lx_decays<R><<<(uint32_t)((m + 255) / 256), 256, 0, st>>>(vals.as<R>(), m, dec.as<R>());
+                ck_launch("lx_decays");
+            }
+            std::vector<uint32_t> hp(m);
+            d2h<R>(values, vals, m, st);
+            ck(cudaMemcpyAsync(hp.data(), pm.p, m * 4, cudaMemcpyDeviceToHost, st), "D2H");
+            if (decays && m > 1) d2h<R>(decays, dec, m - 1, st);
+            ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+            if (perm)
+                for (size_t i = 0; i < m; ++i) perm[i] = hp[i];
+        };
+        if (dtype == LAPLEX_F64)
+            run(0.0);
+        else
+            run(0.0f);
+    });
+}
+
+int laplex_scan(int dtype, const void* sorted_values, size_t m, const void* payload, void* prefix, void* suffix) {
+    return guarded([&] {
+        dtype_check(dtype);
+        if (m == 0) return;
+        if (m >= 0x80000000ull) fail(LAPLEX_E_INVALID_SIZE, "m must be < 2^31");
+        if (dtype == LAPLEX_F64)
+            do_scan<double>((const double*)sorted_values, (uint32_t)m, (const double*)payload, (double*)prefix,
+                            (double*)suffix, host_stream());
+        else
+            do_scan<float>((const float*)sorted_values, (uint32_t)m, (const float*)payload, (float*)prefix,
+                           (float*)suffix, host_stream());
+    });
+}
+
+}  // extern "C"
