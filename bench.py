@@ -1,0 +1,381 @@
+#!/usr/bin/env python
+"""LAPLEX fwd+bwd benchmark (BASELINE.json metric, config C5: n = k = 2^30, B = 1).
+
+One step = plan build (scale by 1/t, device radix sort of both anchor sets,
+merge-path partition) + forward y = A x + backward (x_bar, a_bar, b_bar) for a
+synthetic cotangent g, all through the library's C-ABI device entry points,
+inputs resident in HBM.  `value` is elements/s = n / step time (whole job:
+sum over ranks).  `e2e` is the same step through the host-buffer C-ABI entry
+points (host -> device copies and result read-back inside the timed region).
+
+--impl reference times the reference's own CPU implementation (the UNMODIFIED
+reference headers compiled by oracle/Makefile into oracle/_ref) on a bounded
+sample of the same workload, on all host threads.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "elements/sec and % HBM roofline, LAPLEX fwd+bwd n=2^30, 1/2/4/8 B200 vs CPU ref"
+UNIT = "elements/s"
+
+# Algorithmic bytes per element of the step: fwd+bwd incl.
+# plan = 100n + 96k + B(8n + 12k) with fp32 values, u32 indices, 4-pass LSD.
+def step_model_bytes(n, k, B=1):
+    return 100 * n + 96 * k + B * (8 * n + 12 * k)
+
+
+# Algorithmic bytes per kernel (per whole step), DESIGN.md "Kernels".
+def kernel_model_bytes(name, n, k, rows=1):
+    m2 = n + k
+    return {
+        "lx_sort_hist": 4 * m2,                       # read raw keys once
+        "lx_sort_pass": (12 + 16 + 16 + 16) * m2,     # pass1 r4 w8; passes 2-4 r8 w8
+        # A, Bh, perm_b once; per row: x (gathered) in, row partials out
+        "lx_main_fwd": 4 * n + 8 * k + rows * (4 * k + 4 * n),
+        # A, perm_a once; per row: partials in, y out (scattered)
+        "lx_fix_fwd": 8 * n + rows * 8 * n,
+        # A, Bh, perm_a, perm_b once; per row: g, x in; wa, wb, wb2, gsave, xsave out
+        "lx_main_bwd": 8 * n + 8 * k + rows * (12 * n + 16 * k),
+        # Bh, perm_b, A, perm_a once + a_bar, b_bar out; per row: wb, wb2, xsave, x_bar; wa, gsave
+        "lx_fix_bwd": 12 * n + 12 * k + rows * (8 * n + 16 * k),
+    }.get(name)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and s[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# reference CPU arm
+# ---------------------------------------------------------------------------
+def reference_sample(log2n: int, seed: int):
+    """One fwd+bwd of the compiled reference (ctor + matvec + matvec_vjp), fp32."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+    import oracle as O
+
+    lib = O._lib("ref")
+    n = 1 << log2n
+    buf = np.empty(4 * n)
+    lib.lxr_mt_uniform(C.c_uint64(seed), C.c_size_t(4 * n), C.c_double(-1.0), C.c_double(1.0),
+                       buf.ctypes.data_as(C.c_void_p))
+    a = (buf[:n] * 100).astype(np.float32)
+    b = (buf[n:2 * n] * 100).astype(np.float32)
+    x = buf[2 * n:3 * n].astype(np.float32)
+    g = buf[3 * n:].astype(np.float32)
+    t0 = time.perf_counter()
+    op = O.OracleOp(a, b, 1.0, dtype=np.float32, backend="ref")
+    op.matvec(x)
+    op.vjp(x, g)
+    return time.perf_counter() - t0
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    log2n = args.ref_log2n
+    threads = max(1, min(os.cpu_count() or 1, args.ref_threads))
+    # warm-up + timed steps: each step = `threads` concurrent fwd+bwd samples
+    def step():
+        res = [0.0] * threads
+        ths = [threading.Thread(target=lambda i=i: res.__setitem__(i, reference_sample(log2n, 42 + i)))
+               for i in range(threads)]
+        t0 = time.perf_counter()
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        return time.perf_counter() - t0
+    for _ in range(args.warmup):
+        step()
+    times = [step() for _ in range(args.steps)]
+    ms = 1000 * statistics.median(times)
+    value = threads * (1 << log2n) / (ms / 1000)
+    sample = (f"reference CPU (oracle/_ref: unmodified proj/include headers, -O3 -DNDEBUG), "
+              f"n=k=2^{log2n} fwd+bwd (ctor+matvec+matvec_vjp) fp32 per thread, {threads} concurrent samples "
+              f"per step; workload C5 is n=2^30")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"C5 fwd+bwd n=k=2^{args.log2n} B=1 (reference sampled at 2^{log2n})",
+                   "n": 1 << args.log2n, "batch": 1, "parallelism": "cpu threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def cpu_baseline(args):
+    """Rank-0, N=1: the compiled reference on one core, bounded sample."""
+    log2n = args.ref_log2n
+    reference_sample(max(10, log2n - 4), 1)  # warm
+    times = [reference_sample(log2n, 42 + i) for i in range(args.ref_trials)]
+    med = statistics.median(times)
+    return {"value": (1 << log2n) / med, "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": f"n=k=2^{log2n} fp32 fwd+bwd (LaplexOperator ctor + matvec + matvec_vjp) of the unmodified "
+                      f"reference compiled -O3 -DNDEBUG (oracle/_ref), median of {args.ref_trials} trials "
+                      f"({med:.2f} s each), single thread as the library is single-threaded"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, rank, world, dist):
+    import numpy as np
+    import torch
+
+    import paper_2605_24584_b200 as L
+    from paper_2605_24584_b200 import _lib
+
+    lib = _lib.lib()
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    n = k = 1 << args.log2n
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(42 + rank)
+    a = torch.empty(n, device=dev).uniform_(-100, 100, generator=gen)
+    b = torch.empty(k, device=dev).uniform_(-100, 100, generator=gen)
+    x = torch.empty(1, k, device=dev).uniform_(-1, 1, generator=gen)
+    g = torch.empty(1, n, device=dev).uniform_(-1, 1, generator=gen)
+    y = torch.empty(1, n, device=dev)
+    xb = torch.empty(1, k, device=dev)
+    ab = torch.empty(n, device=dev)
+    bb = torch.empty(k, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        op = L.DeviceOperator(a, b, 1.0)
+        op.apply(x, out=y)
+        op.backward(x, g, x_bar=xb, a_bar=ab, b_bar=bb)
+        return op
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    launches0 = L.kernel_launches()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        barrier()
+    launches = L.kernel_launches() - launches0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if dist is not None:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # sanity at full size: translation conservation sum(a_bar) + sum(b_bar) ~ 0
+    cons = float((ab.double().sum() + bb.double().sum()).abs() /
+                 (ab.double().abs().sum() + bb.double().abs().sum()))
+
+    # per-kernel CUDA-event timing over extra (untimed) steps
+    lib.laplex_profile_enable(1)
+    prof_steps = 2
+    for _ in range(prof_steps):
+        step()
+    torch.cuda.synchronize()
+    buf = C.create_string_buffer(1 << 16)
+    lib.laplex_profile_dump(buf, len(buf))
+    lib.laplex_profile_enable(0)
+    prof = json.loads(buf.value.decode())
+    for v in prof.values():
+        v["ms"] /= prof_steps
+        v["launches"] //= prof_steps
+    hbm, peak_kind = peaks()
+    roof = None
+    kern_table = {}
+    for name, v in prof.items():
+        mb = kernel_model_bytes(name, n, k)
+        gbs = mb / (v["ms"] / 1000) / 1e9 if mb else None
+        kern_table[name] = {"ms_per_step": round(v["ms"], 4), "launches_per_step": v["launches"],
+                            "model_bytes": mb, "achieved_gbs": round(gbs, 1) if gbs else None,
+                            "frac": round(gbs / hbm, 4) if gbs else None}
+    dom = max(prof.items(), key=lambda kv: kv[1]["ms"])[0] if prof else None
+    if dom:
+        d = kern_table[dom]
+        per_launch_bytes = d["model_bytes"] / max(1, d["launches_per_step"]) if d["model_bytes"] else None
+        roof = {"bound": "hbm", "kernel": dom, "achieved": d["achieved_gbs"], "peak": hbm, "unit": "GB/s",
+                "frac": d["frac"], "traffic": None, "peak_kind": peak_kind,
+                "bytes_per_launch": per_launch_bytes,
+                "avg_launch_ms": d["ms_per_step"] / max(1, d["launches_per_step"])}
+
+    total_units = n * world
+    value = total_units / (ms / 1000)
+    step_bytes = step_model_bytes(n, k)
+    step_gbs = step_bytes / (ms / 1000) / 1e9
+
+    e2e = None
+    if args.e2e and rank == 0:
+        e2e = run_e2e(args, torch, lib, n, k)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic: anchors U(-100,100), x and g U(-1,1), t=1 (torch.Generator seed 42+rank)",
+            "config": {"workload": f"C5 LAPLEX fwd+bwd incl. plan build, n=k=2^{args.log2n}, batch 1",
+                       "n": n, "k": k, "batch": 1, "temperature": 1.0,
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs (4 GiB each) larger than the 126 MB L2; no flush needed"},
+            "gpu_launches": launches,
+            "roofline": roof,
+            "step_roofline": {"model": "SURVEY 8(d) fwd+bwd incl. plan: 100n+96k+8n+12k bytes",
+                              "bytes": step_bytes, "achieved": round(step_gbs, 1), "peak": hbm, "unit": "GB/s",
+                              "frac": round(step_gbs / hbm, 4)},
+            "kernels": kern_table,
+            "check": {"conservation_rel": cons},
+            "clocks": clk.summary(),
+            "e2e": e2e,
+        }
+        if world == 1 and args.cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(args)
+        print(json.dumps(line), flush=True)
+
+
+def run_e2e(args, torch, lib, n, k):
+    """Same step through the host-buffer C-ABI: pinned host in, host out."""
+    import paper_2605_24584_b200 as L  # noqa: F401
+    pin = dict(dtype=torch.float32, pin_memory=True)
+    gen = torch.Generator()
+    gen.manual_seed(7)
+    ha = torch.empty(n, **pin).uniform_(-100, 100, generator=gen)
+    hb = torch.empty(k, **pin).uniform_(-100, 100, generator=gen)
+    hx = torch.empty(k, **pin).uniform_(-1, 1, generator=gen)
+    hg = torch.empty(n, **pin).uniform_(-1, 1, generator=gen)
+    hy = torch.empty(n, **pin)
+    hxb = torch.empty(k, **pin)
+    hab = torch.empty(n, **pin)
+    hbb = torch.empty(k, **pin)
+
+    def step():
+        h = C.c_void_p()
+        rc = lib.laplex_plan_create(0, ha.data_ptr(), n, hb.data_ptr(), k, 1.0, None, None, C.byref(h))
+        assert rc == 0, lib.laplex_last_error()
+        rc = lib.laplex_apply(h, 0, hx.data_ptr(), 1, k, hy.data_ptr())
+        assert rc == 0, lib.laplex_last_error()
+        rc = lib.laplex_backward(h, 0, hx.data_ptr(), 1, k, hg.data_ptr(), n, hxb.data_ptr(), hab.data_ptr(),
+                                 hbb.data_ptr(), None, None)
+        assert rc == 0, lib.laplex_last_error()
+        lib.laplex_plan_release(h)
+
+    step()
+    times = []
+    for _ in range(args.e2e_steps):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    sec = statistics.median(times)
+    return {"value": n / sec, "unit": UNIT, "h2d_bytes_per_step": 4 * (n + k + k + k + n),
+            "d2h_bytes_per_step": 4 * (n + k + n + k), "ms_per_step": 1000 * sec,
+            "path": "laplex_plan_create + laplex_apply + laplex_backward (host pointers, pinned torch buffers; "
+                    "host-side require_finite on every input, as the reference API)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--log2n", type=int, default=30)
+    ap.add_argument("--ref-log2n", type=int, default=21)
+    ap.add_argument("--ref-trials", type=int, default=3)
+    ap.add_argument("--ref-threads", type=int, default=64)
+    ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        tdist.init_process_group("nccl")
+        dist = tdist
+    run_ours(args, rank, world, dist)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

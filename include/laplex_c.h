@@ -127,6 +127,13 @@ int laplex_scan(int dtype, const void* sorted_values, size_t m, const void* payl
  * (instrumentation for the benchmark's gpu_launches count). */
 uint64_t laplex_kernel_launches(void);
 
+/* Optional per-kernel CUDA-event timing: while enabled every kernel launch is
+ * bracketed by two events on its stream; laplex_profile_dump synchronises
+ * them and writes {"kernel": {"launches": L, "ms": T}, ...} (JSON) into buf,
+ * then clears the records. */
+int laplex_profile_enable(int on);
+int laplex_profile_dump(char* buf, size_t cap);
+
 #ifdef __cplusplus
 }
 #endif

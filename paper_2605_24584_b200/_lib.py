@@ -23,6 +23,8 @@ _SIGS = {
     "laplex_abi_version": (C.c_int, []),
     "laplex_last_error": (C.c_char_p, []),
     "laplex_kernel_launches": (C.c_uint64, []),
+    "laplex_profile_enable": (C.c_int, [C.c_int]),
+    "laplex_profile_dump": (C.c_int, [C.c_char_p, sz]),
     "laplex_plan_create": (C.c_int, [C.c_int, vp, sz, vp, sz, C.c_double, vp, vp, C.POINTER(vp)]),
     "laplex_plan_create_dev": (C.c_int, [C.c_int, vp, sz, vp, sz, C.c_double, vp, vp, vp, C.POINTER(vp)]),
     "laplex_plan_retain": (C.c_int, [vp]),

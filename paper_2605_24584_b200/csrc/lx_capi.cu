@@ -15,6 +15,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/laplex_c.h"
@@ -44,6 +45,35 @@ void ck(cudaError_t e, const char* what) {
 void ck_launch(const char* what) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
     ck(cudaGetLastError(), what);
+}
+
+// ---- optional per-kernel CUDA-event timing (laplex_profile_*) ----
+std::atomic<bool> g_prof{false};
+struct ProfRec {
+    const char* name;
+    cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+std::vector<ProfRec> g_prof_recs;
+
+// Launch wrapper: every kernel goes through here, so the launch counter and
+// the optional event bracketing see all of them.
+template <class F>
+void launch(const char* name, cudaStream_t st, F&& f) {
+    const bool prof = g_prof.load(std::memory_order_relaxed);
+    ProfRec r{name, nullptr, nullptr};
+    if (prof) {
+        cudaEventCreate(&r.a);
+        cudaEventCreate(&r.b);
+        cudaEventRecord(r.a, st);
+    }
+    f();
+    ck_launch(name);
+    if (prof) {
+        cudaEventRecord(r.b, st);
+        std::lock_guard<std::mutex> g(g_prof_mu);
+        g_prof_recs.push_back(r);
+    }
 }
 
 template <class F>
@@ -173,9 +203,10 @@ void build_partition(Core& c, int which, cudaStream_t st) {
     const Side& b = c.side[1 - which];
     const uint32_t T = tiles_for((uint64_t)a.m + b.m);
     c.part[which] = DBuf((size_t)(T + 1) * 4, st);
-    lx::ms::lx_partition<R, true><<<(T + 1 + 255) / 256, 256, 0, st>>>(
-        a.vals.as<R>(), a.m, b.vals.as<R>(), b.m, c.part[which].as<uint32_t>(), T);
-    ck_launch("lx_partition");
+    launch("lx_partition", st, [&] {
+        lx::ms::lx_partition<R, true><<<(T + 1 + 255) / 256, 256, 0, st>>>(
+            a.vals.as<R>(), a.m, b.vals.as<R>(), b.m, c.part[which].as<uint32_t>(), T);
+    });
     c.T[which] = T;
 }
 
@@ -223,10 +254,12 @@ void radix_sort(const R* raw, uint32_t m, R t, R* vals_out, uint32_t* perm_out, 
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const uint32_t hgrid = std::min<uint32_t>((m + kThreads - 1) / kThreads, (uint32_t)sms * 8);
-    lx_sort_hist<R><<<std::max(1u, hgrid), kThreads, 0, st>>>(raw, m, t, hist.as<uint32_t>(), bad);
-    ck_launch("lx_sort_hist");
-    lx_sort_bases<P><<<P, kRadix, 0, st>>>(hist.as<uint32_t>(), bases.as<uint32_t>());
-    ck_launch("lx_sort_bases");
+    launch("lx_sort_hist", st, [&] {
+        lx_sort_hist<R><<<std::max(1u, hgrid), kThreads, 0, st>>>(raw, m, t, hist.as<uint32_t>(), bad);
+    });
+    launch("lx_sort_bases", st, [&] {
+        lx_sort_bases<P><<<P, kRadix, 0, st>>>(hist.as<uint32_t>(), bases.as<uint32_t>());
+    });
     const size_t smem = sizeof(PassSmem<R>);
     static std::once_flag once;
     std::call_once(once, [&] {
@@ -244,16 +277,17 @@ void radix_sort(const R* raw, uint32_t m, R t, R* vals_out, uint32_t* perm_out, 
         uint32_t* ctr = counters.as<uint32_t>() + pass;
         unsigned long long* lb = look.as<unsigned long long>();
         const uint32_t epoch = (uint32_t)pass + 1;
-        if (pass == 0)
-            lx_sort_pass<R, true, false><<<tiles, kThreads, smem, st>>>(in, inv, out, outv, m, t, pass * kBits, bptr,
-                                                                       lb, ctr, epoch);
-        else if (!last)
-            lx_sort_pass<R, false, false><<<tiles, kThreads, smem, st>>>(in, inv, out, outv, m, t, pass * kBits,
-                                                                        bptr, lb, ctr, epoch);
-        else
-            lx_sort_pass<R, false, true><<<tiles, kThreads, smem, st>>>(in, inv, out, outv, m, t, pass * kBits, bptr,
-                                                                       lb, ctr, epoch);
-        ck_launch("lx_sort_pass");
+        launch("lx_sort_pass", st, [&] {
+            if (pass == 0)
+                lx_sort_pass<R, true, false><<<tiles, kThreads, smem, st>>>(in, inv, out, outv, m, t, pass * kBits,
+                                                                           bptr, lb, ctr, epoch);
+            else if (!last)
+                lx_sort_pass<R, false, false><<<tiles, kThreads, smem, st>>>(in, inv, out, outv, m, t, pass * kBits,
+                                                                            bptr, lb, ctr, epoch);
+            else
+                lx_sort_pass<R, false, true><<<tiles, kThreads, smem, st>>>(in, inv, out, outv, m, t, pass * kBits,
+                                                                           bptr, lb, ctr, epoch);
+        });
         in = out;
         inv = outv;
     }
@@ -277,8 +311,9 @@ void build_side(Side& sd, const R* raw, uint32_t m, R t, const R* phase, int* ba
     if (phase) {
         sd.cph = DBuf((size_t)m * sizeof(R), st);
         sd.sph = DBuf((size_t)m * sizeof(R), st);
-        cos_sin_kernel<R><<<(m + 255) / 256, 256, 0, st>>>(phase, m, sd.cph.as<R>(), sd.sph.as<R>());
-        ck_launch("cos_sin");
+        launch("cos_sin", st, [&] {
+            cos_sin_kernel<R><<<(m + 255) / 256, 256, 0, st>>>(phase, m, sd.cph.as<R>(), sd.sph.as<R>());
+        });
     }
 }
 
@@ -305,10 +340,12 @@ laplex_plan create_plan(const R* a, uint32_t n, const R* b, uint32_t k, double t
     build_side<R>(core->side[0], a, n, R(t), phi, bad.as<int>(), st);
     build_side<R>(core->side[1], b, k, R(t), psi, bad.as<int>(), st);
     if (phi) {
-        finite_check<R><<<64, 256, 0, st>>>(phi, n, bad.as<int>() + 1);
-        ck_launch("finite_check");
-        finite_check<R><<<64, 256, 0, st>>>(psi, k, bad.as<int>() + 1);
-        ck_launch("finite_check");
+        launch("finite_check", st, [&] {
+            finite_check<R><<<64, 256, 0, st>>>(phi, n, bad.as<int>() + 1);
+        });
+        launch("finite_check", st, [&] {
+            finite_check<R><<<64, 256, 0, st>>>(psi, k, bad.as<int>() + 1);
+        });
     }
     build_partition<R>(*core, 0, st);
     int hbad[2] = {0, 0};
@@ -367,22 +404,24 @@ lx::ms::FixArgs<R> fix_args(const View<R>& v, int rows) {
 }
 
 template <class R, int NG, int NX, bool BWD, bool SEQ = false>
-void launch_main(const lx::ms::MainArgs<R>& a, cudaStream_t st) {
+void launch_main(const char* name, const lx::ms::MainArgs<R>& a, cudaStream_t st) {
     using namespace lx::ms;
     const size_t smem = ((sizeof(MainSmem<R, NG, NX>) + 15) & ~size_t(15)) + (size_t)kTile * sizeof(R);
     static std::once_flag once;
     std::call_once(once, [&] {
         cudaFuncSetAttribute(lx_main<R, NG, NX, BWD, SEQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     });
-    lx_main<R, NG, NX, BWD, SEQ><<<a.T, kThreads, smem, st>>>(a);
-    ck_launch("lx_main");
+    launch(name, st, [&] {
+        lx_main<R, NG, NX, BWD, SEQ><<<a.T, kThreads, smem, st>>>(a);
+    });
 }
 
 template <class R, int NC>
 void launch_carry(const R* aggp, const R* aggq, R* cp, R* cq, const R* sl, const R* sf, uint32_t T, int rows,
                   unsigned pm, unsigned qm, cudaStream_t st) {
-    lx::ms::lx_carry<R, NC><<<dim3(rows, 2), lx::ms::kCarryThreads, 0, st>>>(aggp, aggq, cp, cq, sl, sf, T, rows, pm, qm);
-    ck_launch("lx_carry");
+    launch("lx_carry", st, [&] {
+        lx::ms::lx_carry<R, NC><<<dim3(rows, 2), lx::ms::kCarryThreads, 0, st>>>(aggp, aggq, cp, cq, sl, sf, T, rows, pm, qm);
+    });
 }
 
 struct Scratch {
@@ -411,7 +450,7 @@ void apply_fwd(const View<R>& v, const R* X, int rows, R* Y, cudaStream_t st) {
     a.aggq = s.aggq.as<R>();
     a.s_last = s.sl.as<R>();
     a.s_first = s.sf.as<R>();
-    launch_main<R, 0, NX, false>(a, st);
+    launch_main<R, 0, NX, false>(NX == 2 ? "lx_main_fwd_phased" : "lx_main_fwd", a, st);
     launch_carry<R, NC>(s.aggp.as<R>(), s.aggq.as<R>(), s.cp.as<R>(), s.cq.as<R>(), s.sl.as<R>(), s.sf.as<R>(), v.T,
                         rows, 0u, 0u, st);
     auto f = fix_args(v, rows);
@@ -423,8 +462,9 @@ void apply_fwd(const View<R>& v, const R* X, int rows, R* Y, cudaStream_t st) {
     f.wa[1] = wa1.as<R>();
     f.y = Y;
     f.ldy = v.n;
-    lx::ms::lx_fix_fwd<R, NX><<<v.T, lx::ms::kFixThreads, 0, st>>>(f);
-    ck_launch("lx_fix_fwd");
+    launch("lx_fix_fwd", st, [&] {
+        lx::ms::lx_fix_fwd<R, NX><<<v.T, lx::ms::kFixThreads, 0, st>>>(f);
+    });
 }
 
 template <class R>
@@ -439,7 +479,7 @@ void apply_trn(const View<R>& v, const R* G, int rows, R* Y, cudaStream_t st) {
     a.aggq = s.aggq.as<R>();
     a.s_last = s.sl.as<R>();
     a.s_first = s.sf.as<R>();
-    launch_main<R, 1, 0, false>(a, st);
+    launch_main<R, 1, 0, false>("lx_main_trn", a, st);
     launch_carry<R, 1>(s.aggp.as<R>(), s.aggq.as<R>(), s.cp.as<R>(), s.cq.as<R>(), s.sl.as<R>(), s.sf.as<R>(), v.T,
                        rows, 0u, 0u, st);
     auto f = fix_args(v, rows);
@@ -450,8 +490,9 @@ void apply_trn(const View<R>& v, const R* G, int rows, R* Y, cudaStream_t st) {
     f.wb[0] = wb0.as<R>();
     f.y = Y;
     f.ldy = v.k;
-    lx::ms::lx_fix_trn<R><<<v.T, lx::ms::kFixThreads, 0, st>>>(f);
-    ck_launch("lx_fix_trn");
+    launch("lx_fix_trn", st, [&] {
+        lx::ms::lx_fix_trn<R><<<v.T, lx::ms::kFixThreads, 0, st>>>(f);
+    });
 }
 
 template <class R, int NCH>
@@ -485,7 +526,7 @@ void backward_impl(const View<R>& v, const R* X, const R* G, int rows, R* xbar, 
     a.aggq = s.aggq.as<R>();
     a.s_last = s.sl.as<R>();
     a.s_first = s.sf.as<R>();
-    launch_main<R, NCH, NCH, true>(a, st);
+    launch_main<R, NCH, NCH, true>(NCH == 2 ? "lx_main_bwd_phased" : "lx_main_bwd", a, st);
     const unsigned gmask = (1u << NCH) - 1u;
     launch_carry<R, NC>(s.aggp.as<R>(), s.aggq.as<R>(), s.cp.as<R>(), s.cq.as<R>(), s.sl.as<R>(), s.sf.as<R>(), v.T,
                         rows, gmask, gmask << NCH, st);
@@ -508,8 +549,9 @@ void backward_impl(const View<R>& v, const R* X, const R* G, int rows, R* xbar, 
     f.bbar = bbar;
     f.phibar = phibar;
     f.psibar = psibar;
-    lx::ms::lx_fix_bwd<R, NCH><<<v.T, lx::ms::kFixThreads, 0, st>>>(f);
-    ck_launch("lx_fix_bwd");
+    launch("lx_fix_bwd", st, [&] {
+        lx::ms::lx_fix_bwd<R, NCH><<<v.T, lx::ms::kFixThreads, 0, st>>>(f);
+    });
 }
 
 template <class R>
@@ -567,15 +609,17 @@ void do_gram(laplex_plan_s* p, unsigned flags, const R* D, R* M, cudaStream_t st
     DBuf A2((size_t)n * sizeof(R), st), Z((size_t)(n + 1) * sizeof(R), st), dummy((size_t)NCH * (n + 1) * sizeof(R), st);
     const uint32_t warps = n + 1;
     const uint32_t blocks = (warps * 32 + 255) / 256;
-    if (ph)
-        lx::gram::lx_gram_buckets<R, 3><<<blocks, 256, 0, st>>>(v.A, n, v.B, v.k, v.pb, D, v.cpsi, v.spsi,
-                                                                ell.as<R>(), rho.as<R>(), mass.as<R>());
-    else
-        lx::gram::lx_gram_buckets<R, 1><<<blocks, 256, 0, st>>>(v.A, n, v.B, v.k, v.pb, D, nullptr, nullptr,
-                                                                ell.as<R>(), rho.as<R>(), mass.as<R>());
-    ck_launch("lx_gram_buckets");
-    lx::gram::lx_double_anchors<R><<<(n + 255) / 256, 256, 0, st>>>(v.A, n, A2.as<R>());
-    ck_launch("lx_double_anchors");
+    launch("lx_gram_buckets", st, [&] {
+        if (ph)
+            lx::gram::lx_gram_buckets<R, 3><<<blocks, 256, 0, st>>>(v.A, n, v.B, v.k, v.pb, D, v.cpsi, v.spsi,
+                                                                    ell.as<R>(), rho.as<R>(), mass.as<R>());
+        else
+            lx::gram::lx_gram_buckets<R, 1><<<blocks, 256, 0, st>>>(v.A, n, v.B, v.k, v.pb, D, nullptr, nullptr,
+                                                                    ell.as<R>(), rho.as<R>(), mass.as<R>());
+    });
+    launch("lx_double_anchors", st, [&] {
+        lx::gram::lx_double_anchors<R><<<(n + 255) / 256, 256, 0, st>>>(v.A, n, A2.as<R>());
+    });
     ck(cudaMemsetAsync(Z.p, 0, (size_t)(n + 1) * sizeof(R), st), "memset");
     // U = prefix scan of ell over anchors 2A; V = suffix scan of rho (channels as rows)
     launch_carry<R, 1>(ell.as<R>(), rho.as<R>(), U.as<R>(), V.as<R>(), A2.as<R>(), A2.as<R>(), n, NCH, 0u, 0u, st);
@@ -583,13 +627,14 @@ void do_gram(laplex_plan_s* p, unsigned flags, const R* D, R* M, cudaStream_t st
     launch_carry<R, 1>(mass.as<R>(), mass.as<R>(), C.as<R>(), dummy.as<R>(), Z.as<R>(), Z.as<R>(), n + 1, NCH, 0u,
                        0u, st);
     dim3 blk(32, 8), grd((n + 31) / 32, (n + 7) / 8);
-    if (ph)
-        lx::gram::lx_gram_out<R, 3><<<grd, blk, 0, st>>>(v.A, n, v.pa, U.as<R>(), V.as<R>(), C.as<R>(), v.cphi,
-                                                         v.sphi, M);
-    else
-        lx::gram::lx_gram_out<R, 1><<<grd, blk, 0, st>>>(v.A, n, v.pa, U.as<R>(), V.as<R>(), C.as<R>(), nullptr,
-                                                         nullptr, M);
-    ck_launch("lx_gram_out");
+    launch("lx_gram_out", st, [&] {
+        if (ph)
+            lx::gram::lx_gram_out<R, 3><<<grd, blk, 0, st>>>(v.A, n, v.pa, U.as<R>(), V.as<R>(), C.as<R>(), v.cphi,
+                                                             v.sphi, M);
+        else
+            lx::gram::lx_gram_out<R, 1><<<grd, blk, 0, st>>>(v.A, n, v.pa, U.as<R>(), V.as<R>(), C.as<R>(), nullptr,
+                                                             nullptr, M);
+    });
     touch(c, st);
 }
 
@@ -600,13 +645,16 @@ void do_gram_vjp(laplex_plan_s* p, const R* Gbar, R* Dbar, cudaStream_t st) {
     DBuf Y((size_t)v.n * v.k * sizeof(R), st);
     apply_trn<R>(v, Gbar, (int)v.n, Y.as<R>(), st);
     DBuf pa((size_t)v.n * 4, st), pb((size_t)v.k * 4, st);
-    lx::gram::lx_invert_perm<<<(v.n + 255) / 256, 256, 0, st>>>(v.pa, v.n, pa.as<uint32_t>());
-    ck_launch("lx_invert_perm");
-    lx::gram::lx_invert_perm<<<(v.k + 255) / 256, 256, 0, st>>>(v.pb, v.k, pb.as<uint32_t>());
-    ck_launch("lx_invert_perm");
-    lx::gram::lx_gram_vjp_contract<R><<<(v.k + 255) / 256, 256, 0, st>>>(v.A, pa.as<uint32_t>(), v.n, v.B,
-                                                                        pb.as<uint32_t>(), v.k, Y.as<R>(), Dbar);
-    ck_launch("lx_gram_vjp_contract");
+    launch("lx_invert_perm", st, [&] {
+        lx::gram::lx_invert_perm<<<(v.n + 255) / 256, 256, 0, st>>>(v.pa, v.n, pa.as<uint32_t>());
+    });
+    launch("lx_invert_perm", st, [&] {
+        lx::gram::lx_invert_perm<<<(v.k + 255) / 256, 256, 0, st>>>(v.pb, v.k, pb.as<uint32_t>());
+    });
+    launch("lx_gram_vjp_contract", st, [&] {
+        lx::gram::lx_gram_vjp_contract<R><<<(v.k + 255) / 256, 256, 0, st>>>(v.A, pa.as<uint32_t>(), v.n, v.B,
+                                                                            pb.as<uint32_t>(), v.k, Y.as<R>(), Dbar);
+    });
     touch(c, st);
 }
 
@@ -629,20 +677,22 @@ void do_ranks(laplex_plan_s* p, int side, int strict, uint64_t* out, cudaStream_
         const bool afirst = (phys == 0) ? (strict != 0) : (strict == 0);
         DBuf rr((size_t)a.m * 4, st), rc((size_t)b.m * 4, st);
         const size_t smem = (size_t)lx::ms::kTile * sizeof(R);
-        if (afirst) {
-            lx::ms::lx_partition<R, true><<<(T + 256) / 256, 256, 0, st>>>(a.vals.as<R>(), a.m, b.vals.as<R>(), b.m,
-                                                                          part.as<uint32_t>(), T);
-            ck_launch("lx_partition");
-            lx::ms::lx_coranks<R, true><<<T, lx::ms::kThreads, smem, st>>>(
-                a.vals.as<R>(), a.m, b.vals.as<R>(), b.m, part.as<uint32_t>(), rr.as<uint32_t>(), rc.as<uint32_t>());
-        } else {
-            lx::ms::lx_partition<R, false><<<(T + 256) / 256, 256, 0, st>>>(a.vals.as<R>(), a.m, b.vals.as<R>(),
-                                                                           b.m, part.as<uint32_t>(), T);
-            ck_launch("lx_partition");
-            lx::ms::lx_coranks<R, false><<<T, lx::ms::kThreads, smem, st>>>(
-                a.vals.as<R>(), a.m, b.vals.as<R>(), b.m, part.as<uint32_t>(), rr.as<uint32_t>(), rc.as<uint32_t>());
-        }
-        ck_launch("lx_coranks");
+        launch("lx_partition", st, [&] {
+            if (afirst)
+                lx::ms::lx_partition<R, true><<<(T + 256) / 256, 256, 0, st>>>(a.vals.as<R>(), a.m, b.vals.as<R>(),
+                                                                              b.m, part.as<uint32_t>(), T);
+            else
+                lx::ms::lx_partition<R, false><<<(T + 256) / 256, 256, 0, st>>>(a.vals.as<R>(), a.m, b.vals.as<R>(),
+                                                                               b.m, part.as<uint32_t>(), T);
+        });
+        launch("lx_coranks", st, [&] {
+            if (afirst)
+                lx::ms::lx_coranks<R, true><<<T, lx::ms::kThreads, smem, st>>>(
+                    a.vals.as<R>(), a.m, b.vals.as<R>(), b.m, part.as<uint32_t>(), rr.as<uint32_t>(), rc.as<uint32_t>());
+            else
+                lx::ms::lx_coranks<R, false><<<T, lx::ms::kThreads, smem, st>>>(
+                    a.vals.as<R>(), a.m, b.vals.as<R>(), b.m, part.as<uint32_t>(), rr.as<uint32_t>(), rc.as<uint32_t>());
+        });
         // A-first: rows get J<, cols get R<= ; B-first: rows J<=, cols R<
         const int rows_slot = 0 * 2 + (afirst ? 1 : 0);
         const int cols_slot = 1 * 2 + (afirst ? 0 : 1);
@@ -666,8 +716,9 @@ void do_scan(const R* sorted, uint32_t m, const R* payload, R* pre, R* suf, cuda
     ck(cudaMemcpyAsync(vals.p, sorted, (size_t)m * sizeof(R), cudaMemcpyHostToDevice, st), "H2D");
     ck(cudaMemcpyAsync(pay.p, payload, (size_t)m * sizeof(R), cudaMemcpyHostToDevice, st), "H2D");
     DBuf part((size_t)(T + 1) * 4, st);
-    lx_seq_partition<<<(T + 256) / 256, 256, 0, st>>>(m, part.as<uint32_t>(), T);
-    ck_launch("lx_seq_partition");
+    launch("lx_seq_partition", st, [&] {
+        lx_seq_partition<<<(T + 256) / 256, 256, 0, st>>>(m, part.as<uint32_t>(), T);
+    });
     DBuf wa((size_t)m * sizeof(R), st), wa2((size_t)m * sizeof(R), st);
     DBuf dpre((size_t)m * sizeof(R), st), dsuf((size_t)m * sizeof(R), st);
     Scratch s(2, 1, T, sizeof(R), st);
@@ -687,7 +738,7 @@ void do_scan(const R* sorted, uint32_t m, const R* payload, R* pre, R* suf, cuda
     a.aggq = s.aggq.as<R>();
     a.s_last = s.sl.as<R>();
     a.s_first = s.sf.as<R>();
-    launch_main<R, 0, 1, false, true>(a, st);
+    launch_main<R, 0, 1, false, true>("lx_main_seq", a, st);
     launch_carry<R, 1>(s.aggp.as<R>(), s.aggq.as<R>(), s.cp.as<R>(), s.cq.as<R>(), s.sl.as<R>(), s.sf.as<R>(), T, 1,
                        0u, 0u, st);
     FixArgs<R> f;
@@ -703,18 +754,39 @@ void do_scan(const R* sorted, uint32_t m, const R* payload, R* pre, R* suf, cuda
     f.s_first = s.sf.as<R>();
     f.wa[0] = wa.as<R>();
     f.wa2[0] = wa2.as<R>();
-    lx_fix_seq<R><<<T, kFixThreads, 0, st>>>(f, dpre.as<R>(), dsuf.as<R>());
-    ck_launch("lx_fix_seq");
+    launch("lx_fix_seq", st, [&] {
+        lx_fix_seq<R><<<T, kFixThreads, 0, st>>>(f, dpre.as<R>(), dsuf.as<R>());
+    });
     if (pre) ck(cudaMemcpyAsync(pre, dpre.p, (size_t)m * sizeof(R), cudaMemcpyDeviceToHost, st), "D2H");
     if (suf) ck(cudaMemcpyAsync(suf, dsuf.p, (size_t)m * sizeof(R), cudaMemcpyDeviceToHost, st), "D2H");
     ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
 }
 
 // ---- host helpers ---------------------------------------------------------------
+// Host-side require_finite (common.hpp:34-37), split over hardware threads
+// for large inputs so the host-buffer API is not bound by one core.
 template <class R>
 bool host_finite(const R* v, size_t m) {
-    for (size_t i = 0; i < m; ++i)
-        if (!std::isfinite(v[i])) return false;
+    auto scan = [v](size_t lo, size_t hi) {
+        bool ok = true;
+        for (size_t i = lo; i < hi; ++i) ok &= std::isfinite(v[i]);
+        return ok;
+    };
+    const size_t kPar = size_t(1) << 22;
+    unsigned nt = std::thread::hardware_concurrency();
+    if (m < kPar || nt < 2) return scan(0, m);
+    nt = std::min<unsigned>(nt, 32);
+    std::vector<std::thread> th;
+    std::vector<char> res(nt, 1);
+    const size_t chunk = (m + nt - 1) / nt;
+    for (unsigned t = 0; t < nt; ++t)
+        th.emplace_back([&, t] {
+            const size_t lo = std::min(m, t * chunk), hi = std::min(m, lo + chunk);
+            res[t] = scan(lo, hi);
+        });
+    for (auto& x : th) x.join();
+    for (char r : res)
+        if (!r) return false;
     return true;
 }
 
@@ -767,6 +839,56 @@ extern "C" {
 int laplex_abi_version(void) { return LAPLEX_ABI_VERSION; }
 const char* laplex_last_error(void) { return g_last_error.c_str(); }
 uint64_t laplex_kernel_launches(void) { return g_launches.load(); }
+
+int laplex_profile_enable(int on) {
+    g_prof.store(on != 0);
+    return LAPLEX_OK;
+}
+
+int laplex_profile_dump(char* buf, size_t cap) {
+    return guarded([&] {
+        std::vector<ProfRec> recs;
+        {
+            std::lock_guard<std::mutex> g(g_prof_mu);
+            recs.swap(g_prof_recs);
+        }
+        struct Agg {
+            std::string name;
+            uint64_t count = 0;
+            double ms = 0;
+        };
+        std::vector<Agg> agg;
+        for (auto& r : recs) {
+            ck(cudaEventSynchronize(r.b), "cudaEventSynchronize");
+            float ms = 0;
+            cudaEventElapsedTime(&ms, r.a, r.b);
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+            Agg* a = nullptr;
+            for (auto& x : agg)
+                if (x.name == r.name) a = &x;
+            if (!a) {
+                agg.push_back({r.name, 0, 0});
+                a = &agg.back();
+            }
+            a->count += 1;
+            a->ms += ms;
+        }
+        std::string js = "{";
+        for (size_t i = 0; i < agg.size(); ++i) {
+            char tmp[256];
+            std::snprintf(tmp, sizeof(tmp), "%s\"%s\": {\"launches\": %llu, \"ms\": %.6f}", i ? ", " : "",
+                          agg[i].name.c_str(), (unsigned long long)agg[i].count, agg[i].ms);
+            js += tmp;
+        }
+        js += "}";
+        if (buf && cap) {
+            std::strncpy(buf, js.c_str(), cap - 1);
+            buf[cap - 1] = 0;
+        }
+        if (js.size() + 1 > cap) fail(LAPLEX_E_INVALID_ARGUMENT, "profile buffer too small");
+    });
+}
 
 int laplex_plan_create(int dtype, const void* a, size_t n, const void* b, size_t k, double t, const void* phi,
                        const void* psi, laplex_plan* out) {
@@ -865,13 +987,14 @@ int laplex_plan_sorted(laplex_plan plan, int side, void* values, uint64_t* perm,
         DBuf dec;
         if (decays && sd.m > 1) {
             dec = DBuf((size_t)(sd.m - 1) * rs, st);
-            if (c.dtype == LAPLEX_F64)
-                lx::sort::lx_decays<double><<<(sd.m + 255) / 256, 256, 0, st>>>(sd.vals.as<double>(), sd.m,
-                                                                               dec.as<double>());
-            else
-                lx::sort::lx_decays<float><<<(sd.m + 255) / 256, 256, 0, st>>>(sd.vals.as<float>(), sd.m,
-                                                                              dec.as<float>());
-            ck_launch("lx_decays");
+            launch("lx_decays", st, [&] {
+                if (c.dtype == LAPLEX_F64)
+                    lx::sort::lx_decays<double><<<(sd.m + 255) / 256, 256, 0, st>>>(sd.vals.as<double>(), sd.m,
+                                                                                   dec.as<double>());
+                else
+                    lx::sort::lx_decays<float><<<(sd.m + 255) / 256, 256, 0, st>>>(sd.vals.as<float>(), sd.m,
+                                                                                  dec.as<float>());
+            });
             ck(cudaMemcpyAsync(decays, dec.p, (size_t)(sd.m - 1) * rs, cudaMemcpyDeviceToHost, st), "D2H");
         }
         ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
@@ -1081,8 +1204,9 @@ int laplex_sort(int dtype, const void* raw, size_t m, void* values, uint64_t* pe
             ck(cudaMemsetAsync(bad.p, 0, sizeof(int), st), "memset");
             radix_sort<R>(dr.get(), (uint32_t)m, R(1), vals.as<R>(), pm.as<uint32_t>(), bad.as<int>(), st);
             if (m > 1) {
-                lx::sort::lx_decays<R><<<(uint32_t)((m + 255) / 256), 256, 0, st>>>(vals.as<R>(), m, dec.as<R>());
-                ck_launch("lx_decays");
+                launch("lx_decays", st, [&] {
+                    lx::sort::lx_decays<R><<<(uint32_t)((m + 255) / 256), 256, 0, st>>>(vals.as<R>(), m, dec.as<R>());
+                });
             }
             std::vector<uint32_t> hp(m);
             d2h<R>(values, vals, m, st);
