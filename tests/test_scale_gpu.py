@@ -1,0 +1,84 @@
+"""GPU parity at large sizes through the device-pointer C-ABI.
+
+Where the CPU oracle still finishes in seconds (2^24) the permutations and
+co-ranks are compared bit-exactly; beyond that, size-independent properties:
+permutation validity, sortedness, adjointness <g, A x> = <A^T g, x>,
+linearity, translation conservation sum(a_bar) + sum(b_bar) = 0, the
+swap symmetry a_bar == b_bar when a = b and x = g, and x_bar == A^T g bitwise.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2605_24584_b200 as L
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    return torch
+
+
+def test_perms_and_ranks_bit_exact_2p24(torch):
+    rng = np.random.default_rng(24)
+    N = 1 << 24
+    a = rng.uniform(-100, 100, N).astype(np.float32)
+    b = rng.uniform(-100, 100, N).astype(np.float32)
+    op = L.LaplexOperator(a, b, 1.0, dtype=np.float32)
+    of = O.OracleOp(a, b, 1.0, dtype=np.float32)
+    assert np.array_equal(op.sorted_rows().perm, of.sorted(0)[1])
+    assert np.array_equal(op.sorted_cols().perm, of.sorted(1)[1])
+    assert np.array_equal(op.sorted_cols().values, of.sorted(1)[0])
+    assert np.array_equal(op.col_buckets(), of.ranks(1))
+    assert np.array_equal(op.row_buckets(), of.ranks(0))
+
+
+@pytest.mark.parametrize("lg", [27])
+def test_properties_at_scale(torch, lg):
+    N = 1 << lg
+    dev = torch.device("cuda:0")
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(lg)
+    a = torch.empty(N, device=dev).uniform_(-100, 100, generator=gen)
+    b = torch.empty(N, device=dev).uniform_(-100, 100, generator=gen)
+    x = torch.empty(1, N, device=dev).uniform_(-1, 1, generator=gen)
+    x2 = torch.empty(1, N, device=dev).uniform_(-1, 1, generator=gen)
+    g = torch.empty(1, N, device=dev).uniform_(-1, 1, generator=gen)
+    op = L.DeviceOperator(a, b, 1.0)
+    y = op.apply(x)
+    yt = op.apply(g, transpose=True)
+    xb, ab, bb, _, _ = op.backward(x, g)
+    torch.cuda.synchronize()
+    # x_bar of the VJP is the transpose product, bitwise
+    assert torch.equal(xb, yt)
+    # adjointness
+    lhs = (g.double() * y.double()).sum()
+    rhs = (yt.double() * x.double()).sum()
+    assert abs(float(lhs - rhs)) <= 1e-6 * float((g.double().abs() * y.double().abs()).sum())
+    # linearity
+    y2 = op.apply(x2)
+    y3 = op.apply(x + 2 * x2)
+    ref = y.double() + 2 * y2.double()
+    assert float((y3.double() - ref).norm() / ref.norm()) <= 1e-6
+    # translation conservation
+    s = float(ab.double().sum() + bb.double().sum())
+    assert abs(s) <= 1e-6 * float(ab.double().abs().sum() + bb.double().abs().sum())
+    del op
+    # swap symmetry: a = b, x = g  ->  a_bar == b_bar
+    ops = L.DeviceOperator(a, a, 1.0)
+    _, ab2, bb2, _, _ = ops.backward(x, x)
+    torch.cuda.synchronize()
+    assert float((ab2.double() - bb2.double()).norm() / ab2.double().norm()) <= 1e-5
+
+
+def test_sorted_plan_is_a_permutation_at_scale(torch):
+    N = 1 << 26
+    rng = np.random.default_rng(26)
+    a = rng.uniform(-100, 100, N).astype(np.float32)
+    op = L.LaplexOperator(a, a[:1000], 0.5, dtype=np.float32)
+    s = op.sorted_rows()
+    assert np.all(np.diff(s.values) >= 0)
+    assert np.array_equal(np.sort(s.perm), np.arange(N, dtype=np.uint64))
+    assert np.array_equal(s.values, (a / np.float32(0.5))[s.perm.astype(np.int64)])
