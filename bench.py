@@ -50,6 +50,12 @@ def kernel_model_bytes(name, n, k, rows=1):
         "lx_main_bwd": 8 * n + 8 * k + rows * (12 * n + 16 * k),
         # Bh, perm_b, A, perm_a once + a_bar, b_bar out; per row: wb, wb2, xsave, x_bar; wa, gsave
         "lx_fix_bwd": 12 * n + 12 * k + rows * (8 * n + 16 * k),
+        # permutation plan build: read perm, write pos (sequential) and dst (bucket streams)
+        "lx_splan": 12 * m2,
+        # stage passes: x (fwd), g and x (bwd): read dst + src (L2 window), write stage
+        "lx_perm_gather": 12 * (k + n + k) * rows,
+        # y (fwd); x_bar + b_bar (bwd, one pass), a_bar (bwd): read dst + stage, write out
+        "lx_perm_scatter": 12 * n * rows + (4 * k + 8 * k * rows + 4 * k) + 12 * n,
     }.get(name)
 
 

@@ -139,9 +139,19 @@ size_t rsize(int dtype) { return dtype == LAPLEX_F64 ? 8 : 4; }
 struct Side {
     DBuf vals;  // sorted scaled anchors
     DBuf perm;  // u32 sorted -> caller index
-    DBuf cph, sph;  // cos/sin of this side's phases (caller order)
+    DBuf cph, sph;  // cos/sin of this side's phases, SORTED order
+    // permutation plan (large sides): pos[i] = bucketed position of sorted i,
+    // dst[q] = caller index at bucketed position q (caller-index buckets of
+    // 2^shift elements, so each bucket's caller range is an L2-sized window)
+    DBuf spos, sdst;
+    bool staged = false;
     uint32_t m = 0;
 };
+
+// Sides up to this many elements permute directly (the whole vector is
+// L2-resident, 126 MB); larger ones go through the two-pass plan.
+constexpr uint32_t kDirectMax = 1u << 22;
+constexpr size_t kTmaPad = 64;  // slack after anchor arrays for 16-byte TMA rounding
 
 struct Core {
     int dtype = LAPLEX_F32;
@@ -193,6 +203,7 @@ struct View {
     const uint32_t* part;
     uint32_t T;
     R inv_t;
+    const uint32_t *pos_a, *dst_a, *pos_b, *dst_b;  // null = direct permutation
 };
 
 uint32_t tiles_for(uint64_t total) { return (uint32_t)((total + lx::ms::kTile - 1) / lx::ms::kTile); }
@@ -233,6 +244,10 @@ View<R> view(Core& c, bool swapped, cudaStream_t st) {
     v.part = c.part[ia].as<uint32_t>();
     v.T = c.T[ia];
     v.inv_t = R(1) / R(c.t);
+    v.pos_a = a.staged ? a.spos.as<uint32_t>() : nullptr;
+    v.dst_a = a.staged ? a.sdst.as<uint32_t>() : nullptr;
+    v.pos_b = b.staged ? b.spos.as<uint32_t>() : nullptr;
+    v.dst_b = b.staged ? b.sdst.as<uint32_t>() : nullptr;
     return v;
 }
 
@@ -253,9 +268,11 @@ void radix_sort(const R* raw, uint32_t m, R t, R* vals_out, uint32_t* perm_out, 
     ck(cudaMemsetAsync(look.p, 0, (size_t)tiles * kRadix * 8, st), "memset");
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const uint32_t hgrid = std::min<uint32_t>((m + kThreads - 1) / kThreads, (uint32_t)sms * 8);
+    const uint32_t per_block = kHistThreads * kHistItems;
+    const uint32_t hgrid = std::max(1u, std::min<uint32_t>((m + per_block - 1) / per_block, (uint32_t)sms * 4));
+    const size_t hsmem = (size_t)4 * P * kRadix * sizeof(uint32_t);
     launch("lx_sort_hist", st, [&] {
-        lx_sort_hist<R><<<std::max(1u, hgrid), kThreads, 0, st>>>(raw, m, t, hist.as<uint32_t>(), bad);
+        lx_sort_hist<R><<<hgrid, kHistThreads, hsmem, st>>>(raw, m, t, hist.as<uint32_t>(), bad);
     });
     launch("lx_sort_bases", st, [&] {
         lx_sort_bases<P><<<P, kRadix, 0, st>>>(hist.as<uint32_t>(), bases.as<uint32_t>());
@@ -302,19 +319,81 @@ __global__ void cos_sin_kernel(const R* __restrict__ ph, uint32_t m, R* __restri
     }
 }
 
+void build_splan(Side& sd, cudaStream_t st) {
+    using namespace lx::sort;
+    const uint32_t m = sd.m;
+    int bits = 0;
+    while ((1ull << bits) < m) ++bits;
+    const int shift = bits > 8 ? bits - 8 : 0;
+    const uint32_t tiles = (m + kTile - 1) / kTile;
+    sd.spos = DBuf((size_t)m * 4, st);
+    sd.sdst = DBuf((size_t)m * 4, st);
+    DBuf look((size_t)tiles * kRadix * 8, st), ctr(4, st);
+    ck(cudaMemsetAsync(look.p, 0, (size_t)tiles * kRadix * 8, st), "memset");
+    ck(cudaMemsetAsync(ctr.p, 0, 4, st), "memset");
+    const size_t smem = sizeof(PassSmem<float>);
+    static std::once_flag once;
+    std::call_once(once, [&] {
+        cudaFuncSetAttribute(lx_sort_pass<float, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    });
+    launch("lx_splan", st, [&] {
+        lx_sort_pass<float, false, false, true><<<tiles, kThreads, smem, st>>>(
+            sd.perm.p, nullptr, sd.sdst.p, sd.spos.as<uint32_t>(), m, 1.0f, shift, nullptr,
+            look.as<unsigned long long>(), ctr.as<uint32_t>(), 1u);
+    });
+    sd.staged = true;
+}
+
 template <class R>
 void build_side(Side& sd, const R* raw, uint32_t m, R t, const R* phase, int* bad, cudaStream_t st) {
     sd.m = m;
-    sd.vals = DBuf((size_t)m * sizeof(R), st);
+    sd.vals = DBuf((size_t)m * sizeof(R) + kTmaPad, st);  // TMA reads round up to 16 B
     sd.perm = DBuf((size_t)m * 4, st);
     radix_sort<R>(raw, m, t, sd.vals.as<R>(), sd.perm.as<uint32_t>(), bad, st);
     if (phase) {
+        DBuf ph((size_t)m * sizeof(R), st);
+        launch("lx_gather_sorted", st, [&] {
+            lx::sort::lx_gather_sorted<R><<<(m + 255) / 256, 256, 0, st>>>(phase, sd.perm.as<uint32_t>(), m,
+                                                                           ph.as<R>());
+        });
         sd.cph = DBuf((size_t)m * sizeof(R), st);
         sd.sph = DBuf((size_t)m * sizeof(R), st);
         launch("cos_sin", st, [&] {
-            cos_sin_kernel<R><<<(m + 255) / 256, 256, 0, st>>>(phase, m, sd.cph.as<R>(), sd.sph.as<R>());
+            cos_sin_kernel<R><<<(m + 255) / 256, 256, 0, st>>>(ph.as<R>(), m, sd.cph.as<R>(), sd.sph.as<R>());
         });
     }
+    if (m > kDirectMax) build_splan(sd, st);
+}
+
+// ---- permutation application ------------------------------------------------
+int grid_for(size_t work) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const size_t blocks = (work + 255) / 256;
+    return (int)std::max<size_t>(1, std::min<size_t>(blocks, (size_t)sms * 16));
+}
+
+// caller-order rows x m -> bucket-staged copy (consumer reads stage[pos[i]])
+template <class R>
+DBuf stage_gather(const R* src, size_t ld, const uint32_t* dst, uint32_t m, int rows, cudaStream_t st) {
+    DBuf out((size_t)rows * m * sizeof(R), st);
+    using namespace lx::sort;
+    const uint32_t chunks = (m + kPermChunk - 1) / kPermChunk;
+    launch("lx_perm_gather", st, [&] {
+        lx_perm_stage_gather<R><<<dim3(chunks, rows), kPermThreads, 0, st>>>(src, ld, dst, m, out.as<R>());
+    });
+    return out;
+}
+
+template <class R>
+void stage_scatter(const uint32_t* dst, uint32_t m, const R* s1, R* o1, size_t ld1, int rows1, const R* s2, R* o2,
+                   const R* s3, R* o3, cudaStream_t st) {
+    using namespace lx::sort;
+    const uint32_t chunks = (m + kPermChunk - 1) / kPermChunk;
+    launch("lx_perm_scatter", st, [&] {
+        lx_perm_stage_scatter<R><<<chunks, kPermThreads, 0, st>>>(dst, m, s1, o1, ld1, rows1, s2, o2, s3, o3);
+    });
 }
 
 template <class R>
@@ -406,7 +485,7 @@ lx::ms::FixArgs<R> fix_args(const View<R>& v, int rows) {
 template <class R, int NG, int NX, bool BWD, bool SEQ = false>
 void launch_main(const char* name, const lx::ms::MainArgs<R>& a, cudaStream_t st) {
     using namespace lx::ms;
-    const size_t smem = ((sizeof(MainSmem<R, NG, NX>) + 15) & ~size_t(15)) + (size_t)kTile * sizeof(R);
+    const size_t smem = sizeof(MainSmem<R, NG, NX>);
     static std::once_flag once;
     std::call_once(once, [&] {
         cudaFuncSetAttribute(lx_main<R, NG, NX, BWD, SEQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -419,9 +498,49 @@ void launch_main(const char* name, const lx::ms::MainArgs<R>& a, cudaStream_t st
 template <class R, int NC>
 void launch_carry(const R* aggp, const R* aggq, R* cp, R* cq, const R* sl, const R* sf, uint32_t T, int rows,
                   unsigned pm, unsigned qm, cudaStream_t st) {
-    launch("lx_carry", st, [&] {
-        lx::ms::lx_carry<R, NC><<<dim3(rows, 2), lx::ms::kCarryThreads, 0, st>>>(aggp, aggq, cp, cq, sl, sf, T, rows, pm, qm);
-    });
+    using namespace lx::ms;
+    CarryArgs<R, NC> a;
+    std::memset(&a, 0, sizeof(a));
+    a.aggp = aggp;
+    a.aggq = aggq;
+    a.outp = cp;
+    a.outq = cq;
+    a.s_last = sl;
+    a.s_first = sf;
+    a.T = T;
+    a.rows = rows;
+    a.pst_mask = pm;
+    a.qst_mask = qm;
+    if (T <= kCarryBlock) {
+        launch("lx_carry", st, [&] { lx_carry<R, NC, 0><<<dim3(rows, 2, 1), kCarryThreads, 0, st>>>(a); });
+        return;
+    }
+    // reduce -> spine -> apply
+    const uint32_t NB = (T + kCarryBlock - 1) / kCarryBlock;
+    const size_t slots = 2 * NC;
+    DBuf bagp(slots * rows * NB * sizeof(R), st), bagq(slots * rows * NB * sizeof(R), st);
+    DBuf bcp(slots * rows * NB * sizeof(R), st), bcq(slots * rows * NB * sizeof(R), st);
+    DBuf bsl(NB * sizeof(R), st), bsf(NB * sizeof(R), st);
+    a.chunk = kCarryBlock;
+    a.NB = NB;
+    a.baggp = bagp.as<R>();
+    a.baggq = bagq.as<R>();
+    a.bs_last = bsl.as<R>();
+    a.bs_first = bsf.as<R>();
+    launch("lx_carry", st, [&] { lx_carry<R, NC, 1><<<dim3(rows, 2, NB), kCarryThreads, 0, st>>>(a); });
+    CarryArgs<R, NC> sp = a;
+    sp.aggp = bagp.as<R>();
+    sp.aggq = bagq.as<R>();
+    sp.outp = bcp.as<R>();
+    sp.outq = bcq.as<R>();
+    sp.s_last = bsl.as<R>();
+    sp.s_first = bsf.as<R>();
+    sp.T = NB;
+    sp.NB = 1;
+    launch("lx_carry", st, [&] { lx_carry<R, NC, 0><<<dim3(rows, 2, 1), kCarryThreads, 0, st>>>(sp); });
+    a.bcp = bcp.as<R>();
+    a.bcq = bcq.as<R>();
+    launch("lx_carry", st, [&] { lx_carry<R, NC, 2><<<dim3(rows, 2, NB), kCarryThreads, 0, st>>>(a); });
 }
 
 struct Scratch {
@@ -442,7 +561,14 @@ void apply_fwd(const View<R>& v, const R* X, int rows, R* Y, cudaStream_t st) {
     DBuf wa1(NX == 2 ? (size_t)rows * v.n * sizeof(R) : 0, st);
     Scratch s(2 * NC, rows, v.T, sizeof(R), st);
     auto a = main_args(v, rows);
-    a.X = X;
+    DBuf xst;
+    if (v.dst_b) {  // gather x through the cols plan
+        xst = stage_gather<R>(X, v.k, v.dst_b, v.k, rows, st);
+        a.X = xst.as<R>();
+        a.perm_b = v.pos_b;
+    } else {
+        a.X = X;
+    }
     a.ldx = v.k;
     a.wa[0] = wa0.as<R>();
     a.wa[1] = wa1.as<R>();
@@ -460,11 +586,18 @@ void apply_fwd(const View<R>& v, const R* X, int rows, R* Y, cudaStream_t st) {
     f.s_first = s.sf.as<R>();
     f.wa[0] = wa0.as<R>();
     f.wa[1] = wa1.as<R>();
-    f.y = Y;
+    DBuf yst;
+    if (v.dst_a) {  // write bucket-staged, then scatter through the rows plan
+        yst = DBuf((size_t)rows * v.n * sizeof(R), st);
+        f.y = yst.as<R>();
+        f.perm_a = v.pos_a;
+    } else {
+        f.y = Y;
+    }
     f.ldy = v.n;
-    launch("lx_fix_fwd", st, [&] {
-        lx::ms::lx_fix_fwd<R, NX><<<v.T, lx::ms::kFixThreads, 0, st>>>(f);
-    });
+    launch("lx_fix_fwd", st, [&] { lx::ms::lx_fix_fwd<R, NX><<<v.T, lx::ms::kFixThreads, 0, st>>>(f); });
+    if (v.dst_a)
+        stage_scatter<R>(v.dst_a, v.n, yst.as<R>(), Y, v.n, rows, nullptr, nullptr, nullptr, nullptr, st);
 }
 
 template <class R>
@@ -472,7 +605,14 @@ void apply_trn(const View<R>& v, const R* G, int rows, R* Y, cudaStream_t st) {
     DBuf wb0((size_t)rows * v.k * sizeof(R), st);
     Scratch s(2, rows, v.T, sizeof(R), st);
     auto a = main_args(v, rows);
-    a.G = G;
+    DBuf gst;
+    if (v.dst_a) {
+        gst = stage_gather<R>(G, v.n, v.dst_a, v.n, rows, st);
+        a.G = gst.as<R>();
+        a.perm_a = v.pos_a;
+    } else {
+        a.G = G;
+    }
     a.ldg = v.n;
     a.wb[0] = wb0.as<R>();
     a.aggp = s.aggp.as<R>();
@@ -488,11 +628,18 @@ void apply_trn(const View<R>& v, const R* G, int rows, R* Y, cudaStream_t st) {
     f.s_last = s.sl.as<R>();
     f.s_first = s.sf.as<R>();
     f.wb[0] = wb0.as<R>();
-    f.y = Y;
+    DBuf yst;
+    if (v.dst_b) {
+        yst = DBuf((size_t)rows * v.k * sizeof(R), st);
+        f.y = yst.as<R>();
+        f.perm_b = v.pos_b;
+    } else {
+        f.y = Y;
+    }
     f.ldy = v.k;
-    launch("lx_fix_trn", st, [&] {
-        lx::ms::lx_fix_trn<R><<<v.T, lx::ms::kFixThreads, 0, st>>>(f);
-    });
+    launch("lx_fix_trn", st, [&] { lx::ms::lx_fix_trn<R><<<v.T, lx::ms::kFixThreads, 0, st>>>(f); });
+    if (v.dst_b)
+        stage_scatter<R>(v.dst_b, v.k, yst.as<R>(), Y, v.k, rows, nullptr, nullptr, nullptr, nullptr, st);
 }
 
 template <class R, int NCH>
@@ -510,9 +657,22 @@ void backward_impl(const View<R>& v, const R* X, const R* G, int rows, R* xbar, 
     DBuf gsave((size_t)rows * v.n * rs, st), xsave((size_t)rows * v.k * rs, st);
     Scratch s(2 * NC, rows, v.T, rs, st);
     auto a = main_args(v, rows);
-    a.X = X;
+    DBuf xst, gst;
+    if (v.dst_b) {
+        xst = stage_gather<R>(X, v.k, v.dst_b, v.k, rows, st);
+        a.X = xst.as<R>();
+        a.perm_b = v.pos_b;
+    } else {
+        a.X = X;
+    }
+    if (v.dst_a) {
+        gst = stage_gather<R>(G, v.n, v.dst_a, v.n, rows, st);
+        a.G = gst.as<R>();
+        a.perm_a = v.pos_a;
+    } else {
+        a.G = G;
+    }
     a.ldx = v.k;
-    a.G = G;
     a.ldg = v.n;
     for (int c = 0; c < NCH; ++c) {
         a.wa[c] = wa[c].as<R>();
@@ -527,6 +687,8 @@ void backward_impl(const View<R>& v, const R* X, const R* G, int rows, R* xbar, 
     a.s_last = s.sl.as<R>();
     a.s_first = s.sf.as<R>();
     launch_main<R, NCH, NCH, true>(NCH == 2 ? "lx_main_bwd_phased" : "lx_main_bwd", a, st);
+    xst.release();
+    gst.release();
     const unsigned gmask = (1u << NCH) - 1u;
     launch_carry<R, NC>(s.aggp.as<R>(), s.aggq.as<R>(), s.cp.as<R>(), s.cq.as<R>(), s.sl.as<R>(), s.sf.as<R>(), v.T,
                         rows, gmask, gmask << NCH, st);
@@ -543,15 +705,39 @@ void backward_impl(const View<R>& v, const R* X, const R* G, int rows, R* xbar, 
     }
     f.gsave = gsave.as<R>();
     f.xsave = xsave.as<R>();
-    f.xbar = xbar;
-    f.ldxb = v.k;
-    f.abar = abar;
-    f.bbar = bbar;
-    f.phibar = phibar;
-    f.psibar = psibar;
-    launch("lx_fix_bwd", st, [&] {
-        lx::ms::lx_fix_bwd<R, NCH><<<v.T, lx::ms::kFixThreads, 0, st>>>(f);
-    });
+    DBuf sxb, sbb, sqb, sab, spb;  // bucket-staged outputs
+    if (v.dst_b) {
+        sxb = DBuf((size_t)rows * v.k * rs, st);
+        sbb = DBuf((size_t)v.k * rs, st);
+        if (NCH == 2) sqb = DBuf((size_t)v.k * rs, st);
+        f.xbar = sxb.as<R>();
+        f.ldxb = v.k;
+        f.bbar = sbb.as<R>();
+        f.psibar = sqb.as<R>();
+        f.perm_b = v.pos_b;
+    } else {
+        f.xbar = xbar;
+        f.ldxb = v.k;
+        f.bbar = bbar;
+        f.psibar = psibar;
+    }
+    if (v.dst_a) {
+        sab = DBuf((size_t)v.n * rs, st);
+        if (NCH == 2) spb = DBuf((size_t)v.n * rs, st);
+        f.abar = sab.as<R>();
+        f.phibar = spb.as<R>();
+        f.perm_a = v.pos_a;
+    } else {
+        f.abar = abar;
+        f.phibar = phibar;
+    }
+    launch("lx_fix_bwd", st, [&] { lx::ms::lx_fix_bwd<R, NCH><<<v.T, lx::ms::kFixThreads, 0, st>>>(f); });
+    if (v.dst_b)
+        stage_scatter<R>(v.dst_b, v.k, sxb.as<R>(), xbar, v.k, rows, sbb.as<R>(), bbar,
+                         NCH == 2 ? sqb.as<R>() : nullptr, psibar, st);
+    if (v.dst_a)
+        stage_scatter<R>(v.dst_a, v.n, sab.as<R>(), abar, v.n, 1, NCH == 2 ? spb.as<R>() : nullptr, phibar, nullptr,
+                         nullptr, st);
 }
 
 template <class R>
@@ -712,7 +898,7 @@ void do_scan(const R* sorted, uint32_t m, const R* payload, R* pre, R* suf, cuda
     init_pool();
     using namespace lx::ms;
     const uint32_t T = tiles_for(m);
-    DBuf vals((size_t)m * sizeof(R), st), pay((size_t)m * sizeof(R), st);
+    DBuf vals((size_t)m * sizeof(R) + kTmaPad, st), pay((size_t)m * sizeof(R), st);
     ck(cudaMemcpyAsync(vals.p, sorted, (size_t)m * sizeof(R), cudaMemcpyHostToDevice, st), "H2D");
     ck(cudaMemcpyAsync(pay.p, payload, (size_t)m * sizeof(R), cudaMemcpyHostToDevice, st), "H2D");
     DBuf part((size_t)(T + 1) * 4, st);

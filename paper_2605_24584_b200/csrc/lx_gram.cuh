@@ -51,7 +51,7 @@ __global__ void lx_gram_buckets(const R* __restrict__ A, uint32_t n, const R* __
         const R d = D[u];
         R w[NCH];
         if constexpr (NCH == 3) {
-            const R cc = cpsi[u], ss = spsi[u];
+            const R cc = cpsi[s], ss = spsi[s];  // sorted-order phases
             w[0] = xmul(xmul(cc, cc), d);
             w[1] = xmul(xmul(cc, ss), d);
             w[2] = xmul(xmul(ss, ss), d);
@@ -109,8 +109,8 @@ __global__ void lx_gram_out(const R* __restrict__ A, uint32_t n, const uint32_t*
     if constexpr (NCH == 3) {
         // operator.hpp:240-242 evaluated with (i, j) = (max, min) user index so
         // the mirrored entries are literally the same value
-        const uint32_t hi = ui > uj ? ui : uj, lo = ui > uj ? uj : ui;
-        const R ci = cphi[hi], si = sphi[hi], cj = cphi[lo], sj = sphi[lo];
+        const uint32_t hs = ui > uj ? is : js, ls = ui > uj ? js : is;  // sorted-order phases
+        const R ci = cphi[hs], si = sphi[hs], cj = cphi[ls], sj = sphi[ls];
         m = xadd(xadd(xmul(xmul(ci, cj), g[0]), xmul(xadd(xmul(ci, sj), xmul(si, cj)), g[1])),
                  xmul(xmul(si, sj), g[2]));
     }

@@ -77,13 +77,6 @@ __global__ void lx_partition(const R* __restrict__ A, uint32_t n, const R* __res
     part[t] = (uint32_t)merge_path<AFIRST, R, unsigned long long>(A, n, B, k, diag);
 }
 
-// Per-thread merge of kItems consecutive merged positions of one tile held in
-// shared memory (sA = tile rows, sB = tile cols).
-template <bool AFIRST, class R>
-struct TileMerge {
-    int ia, ib;  // counters at the thread's first item
-};
-
 // ---------------------------------------------------------------------------
 // co-ranks (accessor path): AFIRST gives J<[i] and R<=[j]; !AFIRST gives
 // J<=[i] and R<[j]  (operator.hpp:110-120 are the two tie-inclusive ones).
@@ -138,11 +131,14 @@ struct MainArgs {
     const uint32_t* part;  // T+1 row offsets of the merged tiles
     uint32_t n, k, T;
     int rows;
-    const R* X;  // payload on columns, rows x ldx, caller order
+    // payloads are read as X[r*ldx + perm_b[j]] / G[r*ldg + perm_a[i]]: either
+    // the caller's arrays with the true permutations, or (large sides) the
+    // bucket-staged copies with the plan's pos[] tables (lx_perm_stage_gather)
+    const R* X;
     size_t ldx;
-    const R* G;  // payload on rows, rows x ldg, caller order
+    const R* G;
     size_t ldg;
-    const R* cpsi;  // phase modulation (caller order), phased only
+    const R* cpsi;  // phase modulation cos/sin, SORTED order, phased only
     const R* spsi;
     const R* cphi;
     const R* sphi;
@@ -171,25 +167,69 @@ struct Ch {
 template <class R, int NG, int NX>
 struct MainSmem {
     static constexpr int NC = NG + NX;
+    static constexpr int kPad = 16 / sizeof(R);  // TMA bulk copies start 16-byte aligned
+    unsigned long long bar;
     R wsl[kWarps];  // warp last anchors
     R wsf[kWarps];  // warp first anchors
-    R pv[NC][kWarps], pw[NC][kWarps];  // warp prefix totals (inclusive, strict)
-    R qv[NC][kWarps], qw[NC][kWarps];  // warp suffix totals
+    R pv[NC][kWarps], pw[NC][kWarps];    // warp prefix totals (inclusive, strict)
+    R qv[NC][kWarps], qw[NC][kWarps];    // warp suffix totals
     R xpv[NC][kWarps], xpw[NC][kWarps];  // warp exclusive prefix
     R xqv[NC][kWarps], xqw[NC][kWarps];  // warp exclusive suffix
+    alignas(16) R sA[kTile + 2 * kPad];  // tile rows (TMA destination)
+    alignas(16) R sB[kTile + 2 * kPad];  // tile cols
+    R payA[NG > 0 ? kTile : 1];          // gathered g of the tile rows (cp.async)
+    R payB[NX > 0 ? kTile : 1];          // gathered x of the tile cols
 };
+
+// Issue the async gathers of one row's payloads into shared memory.
+template <class R, int NG, int NX, bool SEQ>
+__device__ __forceinline__ void issue_payload(const MainArgs<R>& p, MainSmem<R, NG, NX>& sm, int r, uint32_t a0,
+                                              int na, uint32_t b0, int nb) {
+    if constexpr (SEQ) {
+        for (int i = threadIdx.x; i < na; i += kThreads) {
+            if constexpr (sizeof(R) == 4)
+                cp_async4(&sm.payB[i], &p.X[(size_t)r * p.ldx + a0 + i]);
+            else
+                cp_async8(&sm.payB[i], &p.X[(size_t)r * p.ldx + a0 + i]);
+        }
+        return;
+    }
+    if constexpr (NG > 0) {
+        for (int i = threadIdx.x; i < na; i += kThreads) {
+            const uint32_t u = p.perm_a[a0 + i];
+            if constexpr (sizeof(R) == 4)
+                cp_async4(&sm.payA[i], &p.G[(size_t)r * p.ldg + u]);
+            else
+                cp_async8(&sm.payA[i], &p.G[(size_t)r * p.ldg + u]);
+        }
+    }
+    if constexpr (NX > 0) {
+        for (int j = threadIdx.x; j < nb; j += kThreads) {
+            const uint32_t u = p.perm_b[b0 + j];
+            if constexpr (sizeof(R) == 4)
+                cp_async4(&sm.payB[j], &p.X[(size_t)r * p.ldx + u]);
+            else
+                cp_async8(&sm.payB[j], &p.X[(size_t)r * p.ldx + u]);
+        }
+    }
+}
 
 // SEQ: single sorted sequence (k = 0, part[t] = t*kTile): every element is a
 // "row" carrying its own payload X[r][i] (sorted order) and receiving both the
 // inclusive prefix (wa[0]) and inclusive suffix (wa2[0]) -- the free functions
 // prefix_decay_scan / suffix_decay_scan of scan.hpp:50-73.
+//
+// Per tile: the two anchor ranges arrive by TMA bulk copy (cp.async.bulk +
+// mbarrier) while the payload gathers are issued as cp.async into shared
+// memory; the merge runs as soon as the anchors land, overlapping the gathers.
 template <class R, int NG, int NX, bool BWD, bool SEQ = false>
 __global__ void __launch_bounds__(kThreads, 2) lx_main(MainArgs<R> p) {
     using C = Ch<NG, NX, BWD>;
     constexpr int NC = C::NC;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    MainSmem<R, NG, NX>& sm = *reinterpret_cast<MainSmem<R, NG, NX>*>(smem_raw);
-    R* sAB = reinterpret_cast<R*>(smem_raw + ((sizeof(MainSmem<R, NG, NX>) + 15) & ~size_t(15)));
+    using SM = MainSmem<R, NG, NX>;
+    constexpr int kPad = SM::kPad;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    SM& sm = *reinterpret_cast<SM*>(smem_raw);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t t = blockIdx.x;
@@ -200,11 +240,25 @@ __global__ void __launch_bounds__(kThreads, 2) lx_main(MainArgs<R> p) {
     const uint32_t b0 = (uint32_t)(d0 - a0), b1 = (uint32_t)(d1 - a1);
     const int na = (int)(a1 - a0), nb = (int)(b1 - b0), len = na + nb;
 
-    for (int i = tid; i < na; i += kThreads) sAB[i] = p.A[a0 + i];
-    for (int i = tid; i < nb; i += kThreads) sAB[na + i] = p.B[b0 + i];
+    // ---- prologue: TMA the anchors, cp.async the row-0 payloads ----
+    const uint32_t a0al = a0 & ~uint32_t(kPad - 1), b0al = b0 & ~uint32_t(kPad - 1);
+    const int offA = (int)(a0 - a0al), offB = (int)(b0 - b0al);
+    const uint32_t bytesA = na ? (uint32_t)(((offA + na + kPad - 1) / kPad) * 16) : 0u;
+    const uint32_t bytesB = nb ? (uint32_t)(((offB + nb + kPad - 1) / kPad) * 16) : 0u;
+    if (tid == 0) {
+        mbar_init(&sm.bar, 1);
+        fence_mbar_init();
+    }
     __syncthreads();
-    const R* sA = sAB;
-    const R* sB = sAB + na;
+    if (tid == 0) {
+        mbar_expect_tx(&sm.bar, bytesA + bytesB);
+        if (bytesA) bulk_g2s(sm.sA, p.A + a0al, bytesA, &sm.bar);
+        if (bytesB) bulk_g2s(sm.sB, p.B + b0al, bytesB, &sm.bar);
+    }
+    issue_payload<R, NG, NX, SEQ>(p, sm, 0, a0, na, b0, nb);
+    mbar_wait(&sm.bar, 0);
+    const R* sA = sm.sA + offA;
+    const R* sB = sm.sB + offB;
     // anchor of the tile's last merged element (pads trailing empty slots)
     R s_end;
     if (na == 0)
@@ -261,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 2) lx_main(MainArgs<R> p) {
     }
     if (lane == 31) sm.wsl[warp] = sl;
     if (lane == 0) sm.wsf[warp] = sf;
-    const R S1 = shfl_up(sl, 1);   // previous lane's last anchor
+    const R S1 = shfl_up(sl, 1);     // previous lane's last anchor
     const R S1q = shfl_down(sf, 1);  // next lane's first anchor
     __syncthreads();
     // warp-0 geometry for the scan over warp totals
@@ -283,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, 2) lx_main(MainArgs<R> p) {
     }
     // thread-exclusive anchors and the exps that fold them into each item
     const bool hasP = tid > 0, hasQ = tid < kThreads - 1;
-    const R SW = warp > 0 ? sm.wsl[warp - 1] : sf;          // prev warp's last anchor
+    const R SW = warp > 0 ? sm.wsl[warp - 1] : sf;            // prev warp's last anchor
     const R SWq = warp < kWarps - 1 ? sm.wsf[warp + 1] : sl;  // next warp's first anchor
     const R eTW = (lane > 0 && warp > 0) ? xexp(xsub(SW, S1)) : R(0);
     const bool ltTW = SW < S1;
@@ -308,7 +362,13 @@ __global__ void __launch_bounds__(kThreads, 2) lx_main(MainArgs<R> p) {
     const size_t T = p.T;
 
     for (int r = 0; r < p.rows; ++r) {
-        // ---- payloads ----
+        if (r > 0) {
+            __syncthreads();  // previous row's payload reads are done
+            issue_payload<R, NG, NX, SEQ>(p, sm, r, a0, na, b0, nb);
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        // ---- payloads (from shared memory) ----
         R pay[NC][kItems];
 #pragma unroll
         for (int q = 0; q < kItems; ++q) {
@@ -319,26 +379,24 @@ __global__ void __launch_bounds__(kThreads, 2) lx_main(MainArgs<R> p) {
             const uint32_t li = cd & 0x3fffffffu;
             if (cd & 0x80000000u) {
                 if constexpr (SEQ) {
-                    pay[0][q] = p.X[(size_t)r * p.ldx + a0 + li];
+                    pay[0][q] = sm.payB[li];
                 } else if constexpr (NG > 0) {
-                    const uint32_t u = p.perm_a[a0 + li];
-                    const R g = p.G[(size_t)r * p.ldg + u];
+                    const R g = sm.payA[li];
                     if constexpr (BWD) p.gsave[(size_t)r * p.n + a0 + li] = g;
                     if constexpr (NG == 2) {
-                        pay[0][q] = xmul(cphi[u], g);
-                        pay[1][q] = xmul(sphi[u], g);
+                        pay[0][q] = xmul(cphi[a0 + li], g);
+                        pay[1][q] = xmul(sphi[a0 + li], g);
                     } else {
                         pay[0][q] = g;
                     }
                 }
             } else {
                 if constexpr (NX > 0) {
-                    const uint32_t u = p.perm_b[b0 + li];
-                    const R x = p.X[(size_t)r * p.ldx + u];
+                    const R x = sm.payB[li];
                     if constexpr (BWD) p.xsave[(size_t)r * p.k + b0 + li] = x;
                     if constexpr (NX == 2) {
-                        pay[NG][q] = xmul(cpsi[u], x);
-                        pay[NG + 1][q] = xmul(spsi[u], x);
+                        pay[NG][q] = xmul(cpsi[b0 + li], x);
+                        pay[NG + 1][q] = xmul(spsi[b0 + li], x);
                     } else {
                         pay[NG][q] = x;
                     }
@@ -346,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, 2) lx_main(MainArgs<R> p) {
             }
         }
 
-        // ---- prefix: thread-serial, warp Kogge-Stone, block ----
+        // ---- prefix: thread-serial, warp Kogge-Stone ----
         R pi[NC][kItems], ps[NC][kItems];
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
@@ -475,8 +533,7 @@ __global__ void __launch_bounds__(kThreads, 2) lx_main(MainArgs<R> p) {
         }
         __syncthreads();
 
-        // ---- thread-exclusive carries, item finals ----
-        R fp[NC][kItems], fps[NC][kItems], fq[NC][kItems], fqs[NC][kItems];
+        // ---- thread-exclusive carries folded into the items (in place) ----
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
             R VE = R(0), WE = R(0), VEq = R(0), WEq = R(0);
@@ -506,10 +563,10 @@ __global__ void __launch_bounds__(kThreads, 2) lx_main(MainArgs<R> p) {
             }
 #pragma unroll
             for (int q = 0; q < kItems; ++q) {
-                fp[c][q] = xfma(eI[q], VE, pi[c][q]);
-                if (C::pst(c)) fps[c][q] = xadd(ps[c][q], ((ltI >> q) & 1) ? xmul(eI[q], VE) : WE);
-                fq[c][q] = xfma(eIq[q], VEq, qi[c][q]);
-                if (C::qst(c)) fqs[c][q] = xadd(qs[c][q], ((ltIq >> q) & 1) ? xmul(eIq[q], VEq) : WEq);
+                if (C::pst(c)) ps[c][q] = xadd(ps[c][q], ((ltI >> q) & 1) ? xmul(eI[q], VE) : WE);
+                pi[c][q] = xfma(eI[q], VE, pi[c][q]);
+                if (C::qst(c)) qs[c][q] = xadd(qs[c][q], ((ltIq >> q) & 1) ? xmul(eIq[q], VEq) : WEq);
+                qi[c][q] = xfma(eIq[q], VEq, qi[c][q]);
             }
         }
 
@@ -522,25 +579,25 @@ __global__ void __launch_bounds__(kThreads, 2) lx_main(MainArgs<R> p) {
             if (cd & 0x80000000u) {
                 const size_t o = (size_t)r * p.n + a0 + li;
                 if constexpr (SEQ) {
-                    p.wa[0][o] = fp[0][q];
-                    p.wa2[0][o] = fq[0][q];
+                    p.wa[0][o] = pi[0][q];
+                    p.wa2[0][o] = qi[0][q];
                     continue;
                 }
 #pragma unroll
                 for (int c = NG; c < NC; ++c) {
                     if constexpr (BWD) {
-                        p.wa[c - NG][o] = xsub(fqs[c][q], fp[c][q]);
-                        if constexpr (NX == 2) p.wa2[c - NG][o] = xadd(fp[c][q], fq[c][q]);
+                        p.wa[c - NG][o] = xsub(qs[c][q], pi[c][q]);
+                        if constexpr (NX == 2) p.wa2[c - NG][o] = xadd(pi[c][q], qi[c][q]);
                     } else {
-                        p.wa[c - NG][o] = xadd(fp[c][q], fq[c][q]);
+                        p.wa[c - NG][o] = xadd(pi[c][q], qi[c][q]);
                     }
                 }
             } else {
                 const size_t o = (size_t)r * p.k + b0 + li;
 #pragma unroll
                 for (int c = 0; c < NG; ++c) {
-                    p.wb[c][o] = xadd(fp[c][q], fq[c][q]);
-                    if constexpr (BWD) p.wb2[c][o] = xsub(fq[c][q], fps[c][q]);
+                    p.wb[c][o] = xadd(pi[c][q], qi[c][q]);
+                    if constexpr (BWD) p.wb2[c][o] = xsub(qi[c][q], ps[c][q]);
                 }
             }
         }
@@ -552,69 +609,95 @@ __global__ void __launch_bounds__(kThreads, 2) lx_main(MainArgs<R> p) {
 }
 
 // ---------------------------------------------------------------------------
-// tile-carry scan (fp64), both directions: grid (rows, 2)
+// tile-carry scan (fp64), both directions: grid (rows, 2, blocks)
 // out = inclusive scan over tiles; fix-up of tile t reads prefix[t-1], suffix[t+1]
+//
+// MODE 0: one CTA scans all T elements of a (row, direction).
+// MODE 1: CTA z reduces elements [z*chunk, (z+1)*chunk) to one block
+//         aggregate (written to bagg*, anchors to bS*).
+// MODE 2: like MODE 0 on block z's range, seeded with the inclusive carry of
+//         the neighbouring block (bcarry*, produced by MODE 0 over the block
+//         aggregates).  MODE 1 -> 0 -> 2 is a reduce-then-scan with every
+//         carry applied as exp(anchor difference).
 // ---------------------------------------------------------------------------
 constexpr int kCarryThreads = 1024;
+constexpr uint32_t kCarryBlock = 16384;  // tiles per CTA in the multi-CTA path
 
 template <class R, int NC>
-__global__ void __launch_bounds__(kCarryThreads) lx_carry(const R* __restrict__ aggp, const R* __restrict__ aggq,
-                                                         R* __restrict__ cp, R* __restrict__ cq,
-                                                         const R* __restrict__ s_last,
-                                                         const R* __restrict__ s_first, uint32_t T, int rows,
-                                                         unsigned pst_mask, unsigned qst_mask) {
+struct CarryArgs {
+    const R* aggp;
+    const R* aggq;
+    R* outp;
+    R* outq;
+    const R* s_last;
+    const R* s_first;
+    uint32_t T;
+    int rows;
+    unsigned pst_mask, qst_mask;
+    uint32_t chunk;  // elements per CTA (MODE 1/2)
+    uint32_t NB;     // number of CTAs along z
+    R* baggp;        // MODE 1 outputs [slot][rows][NB]
+    R* baggq;
+    R* bs_last;      // [NB]
+    R* bs_first;
+    const R* bcp;    // MODE 2 inputs: inclusive block carries [slot][rows][NB]
+    const R* bcq;
+};
+
+template <class R, int NC, int MODE>
+__global__ void __launch_bounds__(kCarryThreads) lx_carry(CarryArgs<R, NC> a) {
     const int r = blockIdx.x;
     const bool suffix = blockIdx.y == 1;
-    const R* agg = suffix ? aggq : aggp;
-    R* out = suffix ? cq : cp;
-    const R* S = suffix ? s_first : s_last;
-    const unsigned stm = suffix ? qst_mask : pst_mask;
+    const uint32_t z = blockIdx.z;
+    const R* agg = suffix ? a.aggq : a.aggp;
+    const R* S = suffix ? a.s_first : a.s_last;
+    const unsigned stm = suffix ? a.qst_mask : a.pst_mask;
+    const int rows = a.rows;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = kCarryThreads / 32;
-    const uint32_t chunk = (T + kCarryThreads - 1) / kCarryThreads;
-    // suffix direction: thread tid owns the chunk counted from the right
-    auto pos = [&](uint32_t q) -> uint32_t { return suffix ? T - 1 - q : q; };
-    const uint32_t q0 = (uint32_t)tid * chunk;
-    const uint32_t q1 = min(q0 + chunk, T);
-    auto at = [&](int c, int st, uint32_t u) -> double {
-        return (double)agg[((size_t)(2 * c + st) * rows + r) * T + u];
-    };
-    // pass 1: chunk aggregate (anchor = last element of the chunk in scan order)
-    double v[NC], w[NC];
-    double sa;  // anchor of running aggregate
-    for (int c = 0; c < NC; ++c) v[c] = w[c] = 0.0;
-    sa = (double)S[pos(T - 1)];  // identity padding (never ahead of real elements)
-    bool has = false;
-    for (uint32_t q = q0; q < q1; ++q) {
-        const uint32_t u = pos(q);
-        const double su = (double)S[u];
+    const uint32_t lo = MODE == 0 ? 0 : z * a.chunk;
+    const uint32_t hi = MODE == 0 ? a.T : min(a.T, lo + a.chunk);
+    const uint32_t cnt = hi - lo;
+    const size_t TT = a.T;
+    const uint32_t per = (cnt + kCarryThreads - 1) / kCarryThreads;
+    // scan order q -> array position
+    auto pos = [&](uint32_t q) -> uint32_t { return suffix ? hi - 1 - q : lo + q; };
+    const uint32_t q0 = (uint32_t)tid * per;
+    const uint32_t q1 = min(q0 + per, cnt);
+    auto at = [&](int c, int st, uint32_t u) -> double { return (double)agg[((size_t)(2 * c + st) * rows + r) * TT + u]; };
+    // combine "state (sa, v, w)" with element at anchor su (scan order: state precedes element)
+    auto step = [&](double& sa, double* v, double* w, bool& has, double su, const double* ev, const double* ew) {
         if (!has) {
             for (int c = 0; c < NC; ++c) {
-                v[c] = at(c, 0, u);
-                w[c] = ((stm >> c) & 1) ? at(c, 1, u) : 0.0;
+                v[c] = ev[c];
+                w[c] = ew[c];
             }
             has = true;
         } else {
             const double e = suffix ? exp(su - sa) : exp(sa - su);
             const bool lt = suffix ? su < sa : sa < su;
             for (int c = 0; c < NC; ++c) {
-                if ((stm >> c) & 1) w[c] = at(c, 1, u) + (lt ? e * v[c] : w[c]);
-                v[c] = fma(e, v[c], at(c, 0, u));
+                if ((stm >> c) & 1) w[c] = ew[c] + (lt ? e * v[c] : w[c]);
+                v[c] = fma(e, v[c], ev[c]);
             }
         }
         sa = su;
+    };
+    // pass 1: per-thread chunk aggregate
+    double v[NC], w[NC];
+    double sa = (double)S[suffix ? lo : hi - 1];  // identity padding at the far end of the scan
+    bool has = false;
+    for (int c = 0; c < NC; ++c) v[c] = w[c] = 0.0;
+    for (uint32_t q = q0; q < q1; ++q) {
+        const uint32_t u = pos(q);
+        double ev[NC], ew[NC];
+        for (int c = 0; c < NC; ++c) {
+            ev[c] = at(c, 0, u);
+            ew[c] = ((stm >> c) & 1) ? at(c, 1, u) : 0.0;
+        }
+        step(sa, v, w, has, (double)S[u], ev, ew);
     }
-    // block exclusive scan of chunk aggregates (sequential in warp 0 over warps)
-    __shared__ double s_sa[kCarryThreads];
-    __shared__ double s_v[NC][kCarryThreads];
-    __shared__ double s_w[NC][kCarryThreads];
-    s_sa[tid] = sa;
-    for (int c = 0; c < NC; ++c) {
-        s_v[c][tid] = v[c];
-        s_w[c][tid] = w[c];
-    }
-    __syncthreads();
-    // warp-level inclusive KS over thread aggregates
+    // warp-level inclusive Kogge-Stone over thread aggregates
     double kv[NC], kw[NC];
     for (int c = 0; c < NC; ++c) {
         kv[c] = v[c];
@@ -623,7 +706,7 @@ __global__ void __launch_bounds__(kCarryThreads) lx_carry(const R* __restrict__ 
     for (int j = 0; j < 5; ++j) {
         const int off = 1 << j;
         const double so = __shfl_up_sync(FULL, sa, off);
-        const double e = exp(suffix ? sa - so : so - sa);  // partner precedes in scan order
+        const double e = exp(suffix ? sa - so : so - sa);
         const bool lt = suffix ? sa < so : so < sa;
         for (int c = 0; c < NC; ++c) {
             const double vo = __shfl_up_sync(FULL, kv[c], off);
@@ -649,6 +732,22 @@ __global__ void __launch_bounds__(kCarryThreads) lx_carry(const R* __restrict__ 
         double ca = 0.0, cv[NC], cw[NC];
         bool ch = false;
         for (int c = 0; c < NC; ++c) cv[c] = cw[c] = 0.0;
+        if (MODE == 2) {
+            // seed with the inclusive carry of the neighbouring block in scan order
+            const bool hasn = suffix ? (z + 1 < a.NB) : (z > 0);
+            if (hasn) {
+                const uint32_t nb = suffix ? z + 1 : z - 1;
+                const R* bc = suffix ? a.bcq : a.bcp;
+                const R* bS = suffix ? a.s_first : a.s_last;
+                // anchor of that carry = anchor of the neighbouring block's edge element
+                ca = (double)bS[suffix ? (nb * a.chunk) : min(a.T, (nb + 1) * a.chunk) - 1];
+                for (int c = 0; c < NC; ++c) {
+                    cv[c] = (double)bc[((size_t)(2 * c) * rows + r) * a.NB + nb];
+                    cw[c] = ((stm >> c) & 1) ? (double)bc[((size_t)(2 * c + 1) * rows + r) * a.NB + nb] : 0.0;
+                }
+                ch = true;
+            }
+        }
         for (int u = 0; u < NW; ++u) {
             x_has[u] = ch;
             x_sa[u] = ca;
@@ -656,24 +755,28 @@ __global__ void __launch_bounds__(kCarryThreads) lx_carry(const R* __restrict__ 
                 x_v[c][u] = cv[c];
                 x_w[c][u] = cw[c];
             }
-            const double su = w_sa[u];
-            if (!ch) {
-                for (int c = 0; c < NC; ++c) {
-                    cv[c] = w_v[c][u];
-                    cw[c] = w_w[c][u];
-                }
-                ch = true;
-            } else {
-                const double e = exp(suffix ? su - ca : ca - su);
-                const bool lt = suffix ? su < ca : ca < su;
-                for (int c = 0; c < NC; ++c) {
-                    if ((stm >> c) & 1) cw[c] = w_w[c][u] + (lt ? e * cv[c] : cw[c]);
-                    cv[c] = fma(e, cv[c], w_v[c][u]);
-                }
+            double ev[NC], ew[NC];
+            for (int c = 0; c < NC; ++c) {
+                ev[c] = w_v[c][u];
+                ew[c] = w_w[c][u];
             }
-            ca = su;
+            step(ca, cv, cw, ch, w_sa[u], ev, ew);
+        }
+        if (MODE == 1) {
+            R* bo = suffix ? a.baggq : a.baggp;
+            for (int c = 0; c < NC; ++c) {
+                bo[((size_t)(2 * c) * rows + r) * a.NB + z] = (R)cv[c];
+                if ((stm >> c) & 1) bo[((size_t)(2 * c + 1) * rows + r) * a.NB + z] = (R)cw[c];
+            }
+            if (r == 0) {
+                if (suffix)
+                    a.bs_first[z] = S[lo];
+                else
+                    a.bs_last[z] = S[hi - 1];
+            }
         }
     }
+    if (MODE == 1) return;
     __syncthreads();
     // exclusive carry-in for this thread: warp exclusive (+) lane exclusive
     bool hin = x_has[warp] != 0;
@@ -707,27 +810,18 @@ __global__ void __launch_bounds__(kCarryThreads) lx_carry(const R* __restrict__ 
         }
     }
     // pass 2: rescan the chunk with the carry-in and write inclusive values
+    R* out = suffix ? a.outq : a.outp;
     for (uint32_t q = q0; q < q1; ++q) {
         const uint32_t u = pos(q);
-        const double su = (double)S[u];
-        if (!hin) {
-            for (int c = 0; c < NC; ++c) {
-                iv[c] = at(c, 0, u);
-                iw[c] = ((stm >> c) & 1) ? at(c, 1, u) : 0.0;
-            }
-            hin = true;
-        } else {
-            const double e = suffix ? exp(su - ia) : exp(ia - su);
-            const bool lt = suffix ? su < ia : ia < su;
-            for (int c = 0; c < NC; ++c) {
-                if ((stm >> c) & 1) iw[c] = at(c, 1, u) + (lt ? e * iv[c] : iw[c]);
-                iv[c] = fma(e, iv[c], at(c, 0, u));
-            }
-        }
-        ia = su;
+        double ev[NC], ew[NC];
         for (int c = 0; c < NC; ++c) {
-            out[((size_t)(2 * c) * rows + r) * T + u] = (R)iv[c];
-            if ((stm >> c) & 1) out[((size_t)(2 * c + 1) * rows + r) * T + u] = (R)iw[c];
+            ev[c] = at(c, 0, u);
+            ew[c] = ((stm >> c) & 1) ? at(c, 1, u) : 0.0;
+        }
+        step(ia, iv, iw, hin, (double)S[u], ev, ew);
+        for (int c = 0; c < NC; ++c) {
+            out[((size_t)(2 * c) * rows + r) * TT + u] = (R)iv[c];
+            if ((stm >> c) & 1) out[((size_t)(2 * c + 1) * rows + r) * TT + u] = (R)iw[c];
         }
     }
 }
@@ -775,31 +869,87 @@ __device__ __forceinline__ R carry_at(const R* c, int slot, int rows, int r, siz
     return c[((size_t)slot * rows + r) * T + t];
 }
 
+// Fix-up kernels: one CTA per merged tile; each thread owns up to kFixItems
+// elements of each side (a tile has at most kTile = kFixThreads * kFixItems)
+// and issues all of their loads before any use, so every thread keeps
+// kFixItems x (arrays) independent requests in flight.
+constexpr int kFixItems = kTile / kFixThreads;
+
+struct TileRange {
+    uint32_t a0, a1, b0, b1;
+    bool hl, hr;
+};
+
+template <class R>
+__device__ __forceinline__ TileRange tile_range(const FixArgs<R>& p, uint32_t t) {
+    TileRange r;
+    r.a0 = p.part[t];
+    r.a1 = p.part[t + 1];
+    const unsigned long long d0 = (unsigned long long)t * kTile;
+    const unsigned long long total = (unsigned long long)p.n + p.k;
+    const unsigned long long d1 = d0 + kTile < total ? d0 + kTile : total;
+    r.b0 = (uint32_t)(d0 - r.a0);
+    r.b1 = (uint32_t)(d1 - r.a1);
+    r.hl = t > 0;
+    r.hr = t + 1 < p.T;
+    return r;
+}
+
 // Forward fix-up (NG == 0): outputs at row elements.
 template <class R, int NX>
 __global__ void __launch_bounds__(kFixThreads) lx_fix_fwd(FixArgs<R> p) {
     const uint32_t t = blockIdx.x;
     const size_t T = p.T;
-    const uint32_t a0 = p.part[t], a1 = p.part[t + 1];
-    const bool hl = t > 0, hr = t + 1 < p.T;
-    const R SL = hl ? p.s_last[t - 1] : R(0);
-    const R SR = hr ? p.s_first[t + 1] : R(0);
-    for (uint32_t i = a0 + threadIdx.x; i < a1; i += kFixThreads) {
-        const R s = p.A[i];
-        const R eL = hl ? xexp(xsub(SL, s)) : R(0);
-        const R eR = hr ? xexp(xsub(s, SR)) : R(0);
-        const uint32_t u = p.perm_a[i];
-        for (int r = 0; r < p.rows; ++r) {
+    const TileRange tr = tile_range(p, t);
+    const R SL = tr.hl ? p.s_last[t - 1] : R(0);
+    const R SR = tr.hr ? p.s_first[t + 1] : R(0);
+    R s[kFixItems], eL[kFixItems], eR[kFixItems];
+    uint32_t u[kFixItems];
+#pragma unroll
+    for (int j = 0; j < kFixItems; ++j) {
+        const uint32_t i = tr.a0 + threadIdx.x + j * kFixThreads;
+        const bool ok = i < tr.a1;
+        s[j] = ok ? p.A[i] : R(0);
+        u[j] = ok ? p.perm_a[i] : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < kFixItems; ++j) {
+        eL[j] = tr.hl ? xexp(xsub(SL, s[j])) : R(0);
+        eR[j] = tr.hr ? xexp(xsub(s[j], SR)) : R(0);
+    }
+    for (int r = 0; r < p.rows; ++r) {
+        R cpv[2], cqv[2];
+#pragma unroll
+        for (int c = 0; c < NX; ++c) {
+            cpv[c] = tr.hl ? carry_at(p.cp, 2 * c, p.rows, r, T, t - 1) : R(0);
+            cqv[c] = tr.hr ? carry_at(p.cq, 2 * c, p.rows, r, T, t + 1) : R(0);
+        }
+        R w[2][kFixItems];
+#pragma unroll
+        for (int j = 0; j < kFixItems; ++j) {
+            const uint32_t i = tr.a0 + threadIdx.x + j * kFixThreads;
+#pragma unroll
+            for (int c = 0; c < NX; ++c) w[c][j] = i < tr.a1 ? p.wa[c][(size_t)r * p.n + i] : R(0);
+        }
+        R ph0[kFixItems], ph1[kFixItems];
+        if constexpr (NX == 2) {
+#pragma unroll
+            for (int j = 0; j < kFixItems; ++j) {
+                const uint32_t i = tr.a0 + threadIdx.x + j * kFixThreads;
+                ph0[j] = i < tr.a1 ? p.cphi[i] : R(0);
+                ph1[j] = i < tr.a1 ? p.sphi[i] : R(0);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kFixItems; ++j) {
+            const uint32_t i = tr.a0 + threadIdx.x + j * kFixThreads;
+            if (i >= tr.a1) continue;
             R val[2];
 #pragma unroll
-            for (int c = 0; c < NX; ++c) {
-                const R cpv = hl ? carry_at(p.cp, 2 * c, p.rows, r, T, t - 1) : R(0);
-                const R cqv = hr ? carry_at(p.cq, 2 * c, p.rows, r, T, t + 1) : R(0);
-                val[c] = xfma(eR, cqv, xfma(eL, cpv, p.wa[c][(size_t)r * p.n + i]));
-            }
+            for (int c = 0; c < NX; ++c) val[c] = xfma(eR[j], cqv[c], xfma(eL[j], cpv[c], w[c][j]));
             R out = val[0];
-            if constexpr (NX == 2) out = xadd(xmul(p.cphi[u], val[0]), xmul(p.sphi[u], val[1]));
-            p.y[(size_t)r * p.ldy + u] = out;
+            if constexpr (NX == 2) out = xadd(xmul(ph0[j], val[0]), xmul(ph1[j], val[1]));
+            p.y[(size_t)r * p.ldy + u[j]] = out;
         }
     }
 }
@@ -816,23 +966,36 @@ template <class R>
 __global__ void __launch_bounds__(kFixThreads) lx_fix_trn(FixArgs<R> p) {
     const uint32_t t = blockIdx.x;
     const size_t T = p.T;
-    const uint32_t a0 = p.part[t], a1 = p.part[t + 1];
-    const unsigned long long d0 = (unsigned long long)t * kTile;
-    const unsigned long long total = (unsigned long long)p.n + p.k;
-    const unsigned long long d1 = d0 + kTile < total ? d0 + kTile : total;
-    const uint32_t b0 = (uint32_t)(d0 - a0), b1 = (uint32_t)(d1 - a1);
-    const bool hl = t > 0, hr = t + 1 < p.T;
-    const R SL = hl ? p.s_last[t - 1] : R(0);
-    const R SR = hr ? p.s_first[t + 1] : R(0);
-    for (uint32_t j = b0 + threadIdx.x; j < b1; j += kFixThreads) {
-        const R s = p.B[j];
-        const R eL = hl ? xexp(xsub(SL, s)) : R(0);
-        const R eR = hr ? xexp(xsub(s, SR)) : R(0);
-        const uint32_t u = p.perm_b[j];
-        for (int r = 0; r < p.rows; ++r) {
-            const R cpv = hl ? carry_at(p.cp, 0, p.rows, r, T, t - 1) : R(0);
-            const R cqv = hr ? carry_at(p.cq, 0, p.rows, r, T, t + 1) : R(0);
-            p.y[(size_t)r * p.ldy + u] = xbar_value(p.wb[0][(size_t)r * p.k + j], eL, cpv, eR, cqv);
+    const TileRange tr = tile_range(p, t);
+    const R SL = tr.hl ? p.s_last[t - 1] : R(0);
+    const R SR = tr.hr ? p.s_first[t + 1] : R(0);
+    R s[kFixItems], eL[kFixItems], eR[kFixItems];
+    uint32_t u[kFixItems];
+#pragma unroll
+    for (int j = 0; j < kFixItems; ++j) {
+        const uint32_t i = tr.b0 + threadIdx.x + j * kFixThreads;
+        const bool ok = i < tr.b1;
+        s[j] = ok ? p.B[i] : R(0);
+        u[j] = ok ? p.perm_b[i] : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < kFixItems; ++j) {
+        eL[j] = tr.hl ? xexp(xsub(SL, s[j])) : R(0);
+        eR[j] = tr.hr ? xexp(xsub(s[j], SR)) : R(0);
+    }
+    for (int r = 0; r < p.rows; ++r) {
+        const R cpv = tr.hl ? carry_at(p.cp, 0, p.rows, r, T, t - 1) : R(0);
+        const R cqv = tr.hr ? carry_at(p.cq, 0, p.rows, r, T, t + 1) : R(0);
+        R w[kFixItems];
+#pragma unroll
+        for (int j = 0; j < kFixItems; ++j) {
+            const uint32_t i = tr.b0 + threadIdx.x + j * kFixThreads;
+            w[j] = i < tr.b1 ? p.wb[0][(size_t)r * p.k + i] : R(0);
+        }
+#pragma unroll
+        for (int j = 0; j < kFixItems; ++j) {
+            const uint32_t i = tr.b0 + threadIdx.x + j * kFixThreads;
+            if (i < tr.b1) p.y[(size_t)r * p.ldy + u[j]] = xbar_value(w[j], eL[j], cpv, eR[j], cqv);
         }
     }
 }
@@ -844,95 +1007,164 @@ __global__ void __launch_bounds__(kFixThreads) lx_fix_bwd(FixArgs<R> p) {
     // channels: g = 0..NCH-1, x = NCH..2*NCH-1
     const uint32_t t = blockIdx.x;
     const size_t T = p.T;
-    const uint32_t a0 = p.part[t], a1 = p.part[t + 1];
-    const unsigned long long d0 = (unsigned long long)t * kTile;
-    const unsigned long long total = (unsigned long long)p.n + p.k;
-    const unsigned long long d1 = d0 + kTile < total ? d0 + kTile : total;
-    const uint32_t b0 = (uint32_t)(d0 - a0), b1 = (uint32_t)(d1 - a1);
-    const bool hl = t > 0, hr = t + 1 < p.T;
-    const R SL = hl ? p.s_last[t - 1] : R(0);
-    const R SR = hr ? p.s_first[t + 1] : R(0);
+    const TileRange tr = tile_range(p, t);
+    const R SL = tr.hl ? p.s_last[t - 1] : R(0);
+    const R SR = tr.hr ? p.s_first[t + 1] : R(0);
     const int rows = p.rows;
-    // column side
-    for (uint32_t j = b0 + threadIdx.x; j < b1; j += kFixThreads) {
-        const R s = p.B[j];
-        const R eL = hl ? xexp(xsub(SL, s)) : R(0);
-        const R eR = hr ? xexp(xsub(s, SR)) : R(0);
-        const bool ltL = SL < s;
-        const uint32_t u = p.perm_b[j];
-        R m0 = R(1), m1 = R(0);
-        if constexpr (NCH == 2) {
-            m0 = p.cpsi[u];
-            m1 = p.spsi[u];
+    // ---------------- column side ----------------
+    {
+        R s[kFixItems], eL[kFixItems], eR[kFixItems], m0[kFixItems], m1[kFixItems];
+        uint32_t u[kFixItems];
+#pragma unroll
+        for (int j = 0; j < kFixItems; ++j) {
+            const uint32_t i = tr.b0 + threadIdx.x + j * kFixThreads;
+            const bool ok = i < tr.b1;
+            s[j] = ok ? p.B[i] : R(0);
+            u[j] = ok ? p.perm_b[i] : 0u;
+            m0[j] = R(1);
+            m1[j] = R(0);
+            if constexpr (NCH == 2) {
+                m0[j] = ok ? p.cpsi[i] : R(0);
+                m1[j] = ok ? p.spsi[i] : R(0);
+            }
         }
-        R acc_b = R(0), acc_psi = R(0);
+#pragma unroll
+        for (int j = 0; j < kFixItems; ++j) {
+            eL[j] = tr.hl ? xexp(xsub(SL, s[j])) : R(0);
+            eR[j] = tr.hr ? xexp(xsub(s[j], SR)) : R(0);
+        }
+        R acc_b[kFixItems], acc_psi[kFixItems];
+#pragma unroll
+        for (int j = 0; j < kFixItems; ++j) acc_b[j] = acc_psi[j] = R(0);
         for (int r = 0; r < rows; ++r) {
-            R xb[NCH], inner[NCH];
+            R cpv[NCH], cps[NCH], cqv[NCH];
 #pragma unroll
             for (int c = 0; c < NCH; ++c) {
-                const R cpv = hl ? carry_at(p.cp, 2 * c, rows, r, T, t - 1) : R(0);
-                const R cps = hl ? carry_at(p.cp, 2 * c + 1, rows, r, T, t - 1) : R(0);
-                const R cqv = hr ? carry_at(p.cq, 2 * c, rows, r, T, t + 1) : R(0);
-                xb[c] = xbar_value(p.wb[c][(size_t)r * p.k + j], eL, cpv, eR, cqv);
-                const R strict_left = hl ? (ltL ? xmul(eL, cpv) : cps) : R(0);
-                inner[c] = xsub(xfma(eR, cqv, p.wb2[c][(size_t)r * p.k + j]), strict_left);
+                cpv[c] = tr.hl ? carry_at(p.cp, 2 * c, rows, r, T, t - 1) : R(0);
+                cps[c] = tr.hl ? carry_at(p.cp, 2 * c + 1, rows, r, T, t - 1) : R(0);
+                cqv[c] = tr.hr ? carry_at(p.cq, 2 * c, rows, r, T, t + 1) : R(0);
             }
-            const R xr = p.xsave[(size_t)r * p.k + j];
-            if constexpr (NCH == 2) {
-                p.xbar[(size_t)r * p.ldxb + u] = xadd(xmul(m0, xb[0]), xmul(m1, xb[1]));
-                acc_psi = xfma(xr, xadd(xmul(-m1, xb[0]), xmul(m0, xb[1])), acc_psi);
-                acc_b = xfma(xmul(xmul(m0, xr), p.inv_t), inner[0], acc_b);
-                acc_b = xfma(xmul(xmul(m1, xr), p.inv_t), inner[1], acc_b);
-            } else {
-                p.xbar[(size_t)r * p.ldxb + u] = xb[0];
-                acc_b = xfma(xmul(xr, p.inv_t), inner[0], acc_b);
+            R wb[NCH][kFixItems], wb2[NCH][kFixItems], xr[kFixItems];
+#pragma unroll
+            for (int j = 0; j < kFixItems; ++j) {
+                const uint32_t i = tr.b0 + threadIdx.x + j * kFixThreads;
+                const bool ok = i < tr.b1;
+                const size_t o = (size_t)r * p.k + i;
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) {
+                    wb[c][j] = ok ? p.wb[c][o] : R(0);
+                    wb2[c][j] = ok ? p.wb2[c][o] : R(0);
+                }
+                xr[j] = ok ? p.xsave[o] : R(0);
+            }
+#pragma unroll
+            for (int j = 0; j < kFixItems; ++j) {
+                const uint32_t i = tr.b0 + threadIdx.x + j * kFixThreads;
+                if (i >= tr.b1) continue;
+                const bool ltL = SL < s[j];
+                R xb[NCH], inner[NCH];
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) {
+                    xb[c] = xbar_value(wb[c][j], eL[j], cpv[c], eR[j], cqv[c]);
+                    const R strict_left = tr.hl ? (ltL ? xmul(eL[j], cpv[c]) : cps[c]) : R(0);
+                    inner[c] = xsub(xfma(eR[j], cqv[c], wb2[c][j]), strict_left);
+                }
+                if constexpr (NCH == 2) {
+                    p.xbar[(size_t)r * p.ldxb + u[j]] = xadd(xmul(m0[j], xb[0]), xmul(m1[j], xb[1]));
+                    acc_psi[j] = xfma(xr[j], xadd(xmul(-m1[j], xb[0]), xmul(m0[j], xb[1])), acc_psi[j]);
+                    acc_b[j] = xfma(xmul(xmul(m0[j], xr[j]), p.inv_t), inner[0], acc_b[j]);
+                    acc_b[j] = xfma(xmul(xmul(m1[j], xr[j]), p.inv_t), inner[1], acc_b[j]);
+                } else {
+                    p.xbar[(size_t)r * p.ldxb + u[j]] = xb[0];
+                    acc_b[j] = xfma(xmul(xr[j], p.inv_t), inner[0], acc_b[j]);
+                }
             }
         }
-        p.bbar[u] = acc_b;
-        if constexpr (NCH == 2) p.psibar[u] = acc_psi;
+#pragma unroll
+        for (int j = 0; j < kFixItems; ++j) {
+            const uint32_t i = tr.b0 + threadIdx.x + j * kFixThreads;
+            if (i >= tr.b1) continue;
+            p.bbar[u[j]] = acc_b[j];
+            if constexpr (NCH == 2) p.psibar[u[j]] = acc_psi[j];
+        }
     }
-    // row side
-    for (uint32_t i = a0 + threadIdx.x; i < a1; i += kFixThreads) {
-        const R s = p.A[i];
-        const R eL = hl ? xexp(xsub(SL, s)) : R(0);
-        const R eR = hr ? xexp(xsub(s, SR)) : R(0);
-        const bool ltR = s < SR;
-        const uint32_t u = p.perm_a[i];
-        R m0 = R(1), m1 = R(0);
-        if constexpr (NCH == 2) {
-            m0 = p.cphi[u];
-            m1 = p.sphi[u];
+    // ---------------- row side ----------------
+    {
+        R s[kFixItems], eL[kFixItems], eR[kFixItems], m0[kFixItems], m1[kFixItems];
+        uint32_t u[kFixItems];
+#pragma unroll
+        for (int j = 0; j < kFixItems; ++j) {
+            const uint32_t i = tr.a0 + threadIdx.x + j * kFixThreads;
+            const bool ok = i < tr.a1;
+            s[j] = ok ? p.A[i] : R(0);
+            u[j] = ok ? p.perm_a[i] : 0u;
+            m0[j] = R(1);
+            m1[j] = R(0);
+            if constexpr (NCH == 2) {
+                m0[j] = ok ? p.cphi[i] : R(0);
+                m1[j] = ok ? p.sphi[i] : R(0);
+            }
         }
-        R acc_a = R(0), acc_phi = R(0);
+#pragma unroll
+        for (int j = 0; j < kFixItems; ++j) {
+            eL[j] = tr.hl ? xexp(xsub(SL, s[j])) : R(0);
+            eR[j] = tr.hr ? xexp(xsub(s[j], SR)) : R(0);
+        }
+        R acc_a[kFixItems], acc_phi[kFixItems];
+#pragma unroll
+        for (int j = 0; j < kFixItems; ++j) acc_a[j] = acc_phi[j] = R(0);
         for (int r = 0; r < rows; ++r) {
-            R inner[NCH], pq[NCH];
+            R cpv[NCH], cqv[NCH], cqs[NCH];
 #pragma unroll
             for (int c = 0; c < NCH; ++c) {
                 const int cc = NCH + c;
-                const R cpv = hl ? carry_at(p.cp, 2 * cc, rows, r, T, t - 1) : R(0);
-                const R cqv = hr ? carry_at(p.cq, 2 * cc, rows, r, T, t + 1) : R(0);
-                const R cqs = hr ? carry_at(p.cq, 2 * cc + 1, rows, r, T, t + 1) : R(0);
-                const R strict_right = hr ? (ltR ? xmul(eR, cqv) : cqs) : R(0);
-                inner[c] = xsub(xadd(p.wa[c][(size_t)r * p.n + i], strict_right), xmul(eL, cpv));
-                if constexpr (NCH == 2)
-                    pq[c] = xfma(eR, cqv, xfma(eL, cpv, p.wa2[c][(size_t)r * p.n + i]));
-                else
-                    pq[c] = R(0);
+                cpv[c] = tr.hl ? carry_at(p.cp, 2 * cc, rows, r, T, t - 1) : R(0);
+                cqv[c] = tr.hr ? carry_at(p.cq, 2 * cc, rows, r, T, t + 1) : R(0);
+                cqs[c] = tr.hr ? carry_at(p.cq, 2 * cc + 1, rows, r, T, t + 1) : R(0);
             }
-            const R gr = p.gsave[(size_t)r * p.n + i];
-            if constexpr (NCH == 2) {
-                acc_a = xfma(xmul(xmul(m0, gr), p.inv_t), inner[0], acc_a);
-                acc_a = xfma(xmul(xmul(m1, gr), p.inv_t), inner[1], acc_a);
-                acc_phi = xfma(gr, xadd(xmul(-m1, pq[0]), xmul(m0, pq[1])), acc_phi);
-            } else {
-                acc_a = xfma(xmul(gr, p.inv_t), inner[0], acc_a);
+            R wa[NCH][kFixItems], wa2[NCH][kFixItems], gr[kFixItems];
+#pragma unroll
+            for (int j = 0; j < kFixItems; ++j) {
+                const uint32_t i = tr.a0 + threadIdx.x + j * kFixThreads;
+                const bool ok = i < tr.a1;
+                const size_t o = (size_t)r * p.n + i;
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) {
+                    wa[c][j] = ok ? p.wa[c][o] : R(0);
+                    wa2[c][j] = (NCH == 2 && ok) ? p.wa2[c][o] : R(0);
+                }
+                gr[j] = ok ? p.gsave[o] : R(0);
+            }
+#pragma unroll
+            for (int j = 0; j < kFixItems; ++j) {
+                const uint32_t i = tr.a0 + threadIdx.x + j * kFixThreads;
+                if (i >= tr.a1) continue;
+                const bool ltR = s[j] < SR;
+                R inner[NCH], pq[NCH];
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) {
+                    const R strict_right = tr.hr ? (ltR ? xmul(eR[j], cqv[c]) : cqs[c]) : R(0);
+                    inner[c] = xsub(xadd(wa[c][j], strict_right), xmul(eL[j], cpv[c]));
+                    pq[c] = NCH == 2 ? xfma(eR[j], cqv[c], xfma(eL[j], cpv[c], wa2[c][j])) : R(0);
+                }
+                if constexpr (NCH == 2) {
+                    acc_a[j] = xfma(xmul(xmul(m0[j], gr[j]), p.inv_t), inner[0], acc_a[j]);
+                    acc_a[j] = xfma(xmul(xmul(m1[j], gr[j]), p.inv_t), inner[1], acc_a[j]);
+                    acc_phi[j] = xfma(gr[j], xadd(xmul(-m1[j], pq[0]), xmul(m0[j], pq[1])), acc_phi[j]);
+                } else {
+                    acc_a[j] = xfma(xmul(gr[j], p.inv_t), inner[0], acc_a[j]);
+                }
             }
         }
-        p.abar[u] = acc_a;
-        if constexpr (NCH == 2) p.phibar[u] = acc_phi;
+#pragma unroll
+        for (int j = 0; j < kFixItems; ++j) {
+            const uint32_t i = tr.a0 + threadIdx.x + j * kFixThreads;
+            if (i >= tr.a1) continue;
+            p.abar[u[j]] = acc_a[j];
+            if constexpr (NCH == 2) p.phibar[u[j]] = acc_phi[j];
+        }
     }
 }
-
 
 // SEQ fix-up: prefix/suffix in sorted order (no permutation).
 template <class R>

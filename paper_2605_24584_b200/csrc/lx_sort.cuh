@@ -8,14 +8,16 @@
 //
 // Structure (Merrill & Adinets "onesweep"):
 //   1. lx_sort_hist     one read of the keys -> all digit histograms
-//                       (warp-aggregated via match.any, then smem atomics)
+//                       (per-warp shared-memory sub-histograms)
 //   2. lx_sort_bases    exclusive scan of each pass's 256 counts
 //   3. lx_sort_pass x P one kernel per 8-bit digit; each CTA takes a dynamic
-//                       tile id, ranks its keys stably (warp multi-split with
-//                       match.any), publishes per-digit counts and resolves
+//                       tile id, counts its digits (smem atomics) and publishes
+//                       them at once, ranks its keys stably (warp multi-split:
+//                       8 ballots give each key's peer mask), then resolves
 //                       its global offsets by DECOUPLED LOOK-BACK over the
-//                       tiles before it, then scatters through shared memory
-//                       so global writes are digit-contiguous runs.
+//                       tiles before it (by then usually one probe) and
+//                       scatters through shared memory so global writes are
+//                       digit-contiguous runs.
 // LSD with stable passes == std::stable_sort on the IEEE order; the last pass
 // writes the sorted Real values (sign of zero restored) and the u32 perm.
 #pragma once
@@ -41,37 +43,50 @@ __device__ __forceinline__ unsigned long long status(unsigned long long flag, ui
     return flag | ((unsigned long long)(epoch & 0x3fffffffu) << 32) | c;
 }
 
+// Upfront digit histograms of all passes in one read of the keys.  Each warp
+// owns a private sub-histogram in shared memory (no cross-warp contention);
+// each thread keeps kHistItems independent loads in flight.
+constexpr int kHistThreads = 512;
+constexpr int kHistItems = 8;
+
 template <class R>
-__global__ void __launch_bounds__(kThreads) lx_sort_hist(const R* __restrict__ raw, size_t n, R t,
-                                                        uint32_t* __restrict__ hist, int* __restrict__ bad) {
+__global__ void __launch_bounds__(kHistThreads) lx_sort_hist(const R* __restrict__ raw, size_t n, R t,
+                                                            uint32_t* __restrict__ hist, int* __restrict__ bad) {
     using K = typename Traits<R>::Key;
     constexpr int P = Traits<R>::kPasses;
-    __shared__ uint32_t sh[P][kRadix];
-    for (int i = threadIdx.x; i < P * kRadix; i += kThreads) (&sh[0][0])[i] = 0;
+    constexpr int W = kHistThreads / 32;
+    constexpr int SUB = 4;  // sub-histograms per block (warp % SUB)
+    extern __shared__ uint32_t shh[];  // [SUB][P][kRadix]
+    for (int i = threadIdx.x; i < SUB * P * kRadix; i += kHistThreads) shh[i] = 0;
     __syncthreads();
-    const int lane = threadIdx.x & 31;
+    uint32_t* mine = shh + ((threadIdx.x >> 5) % SUB) * P * kRadix;
+    (void)W;
     int any_bad = 0;
-    const size_t stride = (size_t)gridDim.x * kThreads;
-    for (size_t base = (size_t)blockIdx.x * kThreads; base < n; base += stride) {
-        const size_t i = base + threadIdx.x;
-        const bool valid = i < n;
-        K key = 0;
-        if (valid) {
-            const R v = raw[i];
-            if (!isfinite(v)) any_bad = 1;
-            key = radix_key<R>(xdiv(v, t));
+    const size_t per_block = (size_t)kHistThreads * kHistItems;
+    for (size_t base = (size_t)blockIdx.x * per_block; base < n; base += (size_t)gridDim.x * per_block) {
+        R v[kHistItems];
+#pragma unroll
+        for (int q = 0; q < kHistItems; ++q) {
+            const size_t i = base + (size_t)q * kHistThreads + threadIdx.x;
+            v[q] = i < n ? raw[i] : R(0);
         }
 #pragma unroll
-        for (int p = 0; p < P; ++p) {
-            const int d = valid ? (int)((key >> (p * kBits)) & (kRadix - 1)) : kRadix;
-            const unsigned peers = __match_any_sync(FULL, d);
-            if (d < kRadix && lane == __ffs(peers) - 1) atomicAdd(&sh[p][d], (uint32_t)__popc(peers));
+        for (int q = 0; q < kHistItems; ++q) {
+            const size_t i = base + (size_t)q * kHistThreads + threadIdx.x;
+            if (i < n) {
+                if (!isfinite(v[q])) any_bad = 1;
+                const K key = radix_key<R>(xdiv(v[q], t));
+#pragma unroll
+                for (int p = 0; p < P; ++p) atomicAdd(&mine[p * kRadix + (int)((key >> (p * kBits)) & (kRadix - 1))], 1u);
+            }
         }
     }
     if (any_bad) atomicOr(bad, 1);
     __syncthreads();
-    for (int i = threadIdx.x; i < P * kRadix; i += kThreads) {
-        const uint32_t c = (&sh[0][0])[i];
+    for (int i = threadIdx.x; i < P * kRadix; i += kHistThreads) {
+        uint32_t c = 0;
+#pragma unroll
+        for (int sub = 0; sub < SUB; ++sub) c += shh[sub * P * kRadix + i];
         if (c) atomicAdd(&hist[i], c);
     }
 }
@@ -108,7 +123,13 @@ struct PassSmem {
 
 // One digit pass.  FIRST reads the raw anchors and builds keys+payload on the
 // fly; LAST writes sorted values (Real) and perm (u32) instead of key/payload.
-template <class R, bool FIRST, bool LAST>
+// SPLAN is the same machinery run once over a permutation P (sorted -> caller
+// index) with digit = P[i] >> shift: it writes pos[i] = o (the stable position
+// of i in caller-index-bucket order, out_vals) and dst[o] = P[i] (out_keys);
+// the bucket bases are d << shift (a permutation fills every bucket exactly).
+// That is the B200 form of the reference's cache-blocked ScatterPlan
+// (operator.hpp:26-60,130-136).
+template <class R, bool FIRST, bool LAST, bool SPLAN = false>
 __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict__ in_keys,
                                                         const uint32_t* __restrict__ in_vals,
                                                         void* __restrict__ out_keys,
@@ -138,7 +159,10 @@ __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict_
     for (int k = 0; k < kItems; ++k) {
         const size_t i = wbase + (size_t)k * 32 + lane;
         if (i < n) {
-            if constexpr (FIRST) {
+            if constexpr (SPLAN) {
+                key[k] = reinterpret_cast<const K*>(in_keys)[i];
+                val[k] = 0;
+            } else if constexpr (FIRST) {
                 const R s = xdiv(reinterpret_cast<const R*>(in_keys)[i], t);
                 const bool nz = as_bits(s) == Traits<R>::kSign;
                 key[k] = radix_key<R>(s);
@@ -153,38 +177,72 @@ __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict_
         }
     }
 
-    // ---- stable warp multi-split ranking ----
-    uint32_t rank[kItems];
-    const unsigned lt = lanemask_lt();
+#if !defined(LX_SORT_LATE)
+    // ---- early counts: per-warp digit histogram (order-free smem atomics),
+    // published before ranking so successors' look-back overlaps our ranking ----
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
         const size_t i = wbase + (size_t)k * 32 + lane;
-        const int d = i < n ? (int)((key[k] >> shift) & (kRadix - 1)) : kRadix;
-        const unsigned peers = __match_any_sync(FULL, d);
-        const int leader = __ffs(peers) - 1;
-        uint32_t cnt = 0;
-        if (d < kRadix && lane == leader) cnt = sm.whist[warp][d];
-        cnt = __shfl_sync(FULL, cnt, leader);
-        if (d < kRadix && lane == leader) sm.whist[warp][d] = cnt + __popc(peers);
-        rank[k] = cnt + __popc(peers & lt);
-        __syncwarp();
+        if (i < n) atomicAdd(&sm.whist[warp][(int)((key[k] >> shift) & (kRadix - 1))], 1u);
     }
     __syncthreads();
-
-    // ---- per digit: warp-exclusive offsets, tile count ----
+#endif
     const int d = tid;  // kThreads == kRadix
     uint32_t count = 0;
+    unsigned long long* my_status = lookback + (size_t)tile * kRadix + d;
+#if !defined(LX_SORT_LATE)
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) {
         const uint32_t c = sm.whist[w][d];
         sm.whist[w][d] = count;
         count += c;
     }
-    unsigned long long* my_status = lookback + (size_t)tile * kRadix + d;
-    if (tile == 0)
-        st_relaxed_u64(my_status, status(kFlagInc, epoch, count));
-    else
-        st_relaxed_u64(my_status, status(kFlagAgg, epoch, count));
+    st_relaxed_u64(my_status, status(tile == 0 ? kFlagInc : kFlagAgg, epoch, count));
+#endif
+
+    // ---- stable in-warp ranks: peer mask per key (8 ballots or match.any) and a
+    // running per-warp digit cursor ----
+    uint32_t rank[kItems];
+    const unsigned lt = lanemask_lt();
+#if !defined(LX_SORT_LATE)
+    __syncthreads();  // warp-exclusive offsets visible before the cursors start
+#endif
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+        // invalid tail items use digit 255 and are never counted: they follow
+        // every valid item of the warp, so they never shift a valid rank
+        const size_t i = wbase + (size_t)k * 32 + lane;
+        const int dk = (int)((key[k] >> shift) & (kRadix - 1));
+#if defined(LX_SORT_MATCH_ANY)
+        const unsigned peers = __match_any_sync(FULL, i < n ? dk : kRadix);
+#else
+        unsigned peers = __ballot_sync(FULL, i < n);
+        if (i >= n) peers = ~peers;
+#pragma unroll
+        for (int b = 0; b < kBits; ++b) {
+            const bool bit = (dk >> b) & 1;
+            const unsigned m = __ballot_sync(FULL, bit);
+            peers &= bit ? m : ~m;
+        }
+#endif
+        const int leader = __ffs(peers) - 1;
+        uint32_t cnt = 0;
+        if (lane == leader) cnt = sm.whist[warp][dk];
+        cnt = __shfl_sync(FULL, cnt, leader);
+        if (lane == leader && i < n) sm.whist[warp][dk] = cnt + __popc(peers);
+        rank[k] = cnt + __popc(peers & lt);
+        __syncwarp();
+    }
+#if defined(LX_SORT_LATE)
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {  // per digit: warp-exclusive offsets, tile count
+        const uint32_t c = sm.whist[w][d];
+        sm.whist[w][d] = count;
+        count += c;
+    }
+    st_relaxed_u64(my_status, status(tile == 0 ? kFlagInc : kFlagAgg, epoch, count));
+#endif
 
     // block exclusive scan of counts over digits -> shared-memory positions
     uint32_t incl = count;
@@ -209,7 +267,12 @@ __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict_
             const unsigned long long s = ld_relaxed_u64(lookback + (size_t)j * kRadix + d);
             const uint32_t e = (uint32_t)(s >> 32) & 0x3fffffffu;
             const unsigned long long f = s & (3ull << 62);
-            if (f == 0 || e != (epoch & 0x3fffffffu)) continue;  // predecessor not published yet
+            if (f == 0 || e != (epoch & 0x3fffffffu)) {  // predecessor not published yet
+#if defined(LX_SORT_BACKOFF)
+                __nanosleep(LX_SORT_BACKOFF);
+#endif
+                continue;
+            }
             excl += (uint32_t)s;
             if (f == kFlagInc) break;
             --j;
@@ -217,7 +280,10 @@ __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict_
         st_relaxed_u64(my_status, status(kFlagInc, epoch, excl + count));
     }
     sm.dstart[d] = dstart;
-    sm.gbase[d] = bases[d] + excl - dstart;
+    if constexpr (SPLAN)
+        sm.gbase[d] = ((uint32_t)d << shift) + excl - dstart;
+    else
+        sm.gbase[d] = bases[d] + excl - dstart;
     __syncthreads();
 
     // ---- scatter into shared memory in digit order ----
@@ -226,9 +292,16 @@ __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict_
         const size_t i = wbase + (size_t)k * 32 + lane;
         if (i < n) {
             const int dk = (int)((key[k] >> shift) & (kRadix - 1));
+#if !defined(LX_SORT_LATE)
+            const uint32_t pos = sm.dstart[dk] + rank[k];  // rank includes the warp offset
+#else
             const uint32_t pos = sm.dstart[dk] + sm.whist[warp][dk] + rank[k];
+#endif
             sm.keys[pos] = key[k];
-            sm.vals[pos] = val[k];
+            if constexpr (SPLAN)
+                out_vals[i] = sm.gbase[dk] + pos;
+            else
+                sm.vals[pos] = val[k];
         }
     }
     __syncthreads();
@@ -236,10 +309,12 @@ __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict_
     // ---- digit-contiguous global writes ----
     for (int i = tid; i < tile_n; i += kThreads) {
         const K kk = sm.keys[i];
-        const uint32_t v = sm.vals[i];
+        const uint32_t v = SPLAN ? 0u : sm.vals[i];
         const int dk = (int)((kk >> shift) & (kRadix - 1));
         const uint32_t o = sm.gbase[dk] + (uint32_t)i;
-        if constexpr (LAST) {
+        if constexpr (SPLAN) {
+            reinterpret_cast<K*>(out_keys)[o] = kk;
+        } else if constexpr (LAST) {
             reinterpret_cast<R*>(out_keys)[o] = radix_value<R>(kk, (v >> 31) != 0);
             out_vals[o] = v & 0x7fffffffu;
         } else {
@@ -247,6 +322,81 @@ __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict_
             out_vals[o] = v;
         }
     }
+}
+
+// ---- permutation plans: the two L2-window passes --------------------------
+// Blocks cover contiguous, launch-ordered chunks of the bucketed index q, so
+// the resident blocks always sit in one or two caller-index buckets and the
+// random side of each pass stays inside an L2-resident window.
+constexpr int kPermThreads = 256;
+constexpr int kPermItems = 8;
+constexpr int kPermChunk = kPermThreads * kPermItems;
+
+// gather (caller order -> sorted order), first half: stage[r][q] = src[r][dst[q]];
+// the consumer then reads stage[r][pos[i]].  grid: (chunks, rows)
+template <class R>
+__global__ void __launch_bounds__(kPermThreads) lx_perm_stage_gather(const R* __restrict__ src, size_t ld_src,
+                                                                    const uint32_t* __restrict__ dst, uint32_t m,
+                                                                    R* __restrict__ stage) {
+    const size_t r = blockIdx.y;
+    const size_t q0 = (size_t)blockIdx.x * kPermChunk + threadIdx.x;
+    uint32_t u[kPermItems];
+#pragma unroll
+    for (int j = 0; j < kPermItems; ++j) {
+        const size_t q = q0 + (size_t)j * kPermThreads;
+        u[j] = q < m ? dst[q] : 0u;
+    }
+    R v[kPermItems];
+#pragma unroll
+    for (int j = 0; j < kPermItems; ++j) {
+        const size_t q = q0 + (size_t)j * kPermThreads;
+        v[j] = q < m ? src[r * ld_src + u[j]] : R(0);
+    }
+#pragma unroll
+    for (int j = 0; j < kPermItems; ++j) {
+        const size_t q = q0 + (size_t)j * kPermThreads;
+        if (q < m) stage[r * m + q] = v[j];
+    }
+}
+
+// scatter (sorted order -> caller order), second half: out[r][dst[q]] = stage[r][q]
+// for up to three arrays sharing the permutation (s2/s3 may be null).
+template <class R>
+__global__ void __launch_bounds__(kPermThreads) lx_perm_stage_scatter(const uint32_t* __restrict__ dst, uint32_t m,
+                                                                     const R* __restrict__ s1, R* __restrict__ o1,
+                                                                     size_t ld1, int rows1, const R* __restrict__ s2,
+                                                                     R* __restrict__ o2, const R* __restrict__ s3,
+                                                                     R* __restrict__ o3) {
+    const size_t q0 = (size_t)blockIdx.x * kPermChunk + threadIdx.x;
+    uint32_t u[kPermItems];
+#pragma unroll
+    for (int j = 0; j < kPermItems; ++j) {
+        const size_t q = q0 + (size_t)j * kPermThreads;
+        u[j] = q < m ? dst[q] : 0u;
+    }
+    for (int r = 0; r < rows1; ++r) {
+#pragma unroll
+        for (int j = 0; j < kPermItems; ++j) {
+            const size_t q = q0 + (size_t)j * kPermThreads;
+            if (q < m) o1[(size_t)r * ld1 + u[j]] = s1[(size_t)r * m + q];
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < kPermItems; ++j) {
+        const size_t q = q0 + (size_t)j * kPermThreads;
+        if (q < m) {
+            if (s2) o2[u[j]] = s2[q];
+            if (s3) o3[u[j]] = s3[q];
+        }
+    }
+}
+
+// gather of a per-element caller-order vector into sorted order (plan build)
+template <class R>
+__global__ void lx_gather_sorted(const R* __restrict__ src, const uint32_t* __restrict__ perm, uint32_t m,
+                                 R* __restrict__ out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) out[i] = src[perm[i]];
 }
 
 // Neighbour decays of the sorted values: decays[i] = exp(v_i - v_{i+1})
