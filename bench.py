@@ -42,14 +42,12 @@ def kernel_model_bytes(name, n, k, rows=1):
     return {
         "lx_sort_hist": 4 * m2,                       # read raw keys once
         "lx_sort_pass": (12 + 16 + 16 + 16) * m2,     # pass1 r4 w8; passes 2-4 r8 w8
-        # A, Bh, perm_b once; per row: x (gathered) in, row partials out
-        "lx_main_fwd": 4 * n + 8 * k + rows * (4 * k + 4 * n),
-        # A, perm_a once; per row: partials in, y out (scattered)
-        "lx_fix_fwd": 8 * n + rows * 8 * n,
-        # A, Bh, perm_a, perm_b once; per row: g, x in; wa, wb, wb2, gsave, xsave out
-        "lx_main_bwd": 8 * n + 8 * k + rows * (12 * n + 16 * k),
-        # Bh, perm_b, A, perm_a once + a_bar, b_bar out; per row: wb, wb2, xsave, x_bar; wa, gsave
-        "lx_fix_bwd": 12 * n + 12 * k + rows * (8 * n + 16 * k),
+        # tile aggregates: fwd reads Bh, pos_b, x-stage; bwd reads both sides
+        "lx_tileagg": (12 * k + rows * 0) + (12 * n + 12 * k),
+        # fwd: A, Bh, pos_b, x-stage in; pos_a in, y-stage out
+        "lx_main_fwd": 4 * n + 4 * k + 4 * k + rows * (4 * k + 4 * n) + 4 * n,
+        # bwd: A, Bh, pos_a, pos_b, g-stage, x-stage in; x_bar, b_bar, a_bar stage out
+        "lx_main_bwd": 8 * n + 8 * k + rows * (4 * n + 4 * k + 4 * k) + 4 * n + 4 * k,
         # permutation plan build: read perm, write pos (sequential) and dst (bucket streams)
         "lx_splan": 12 * m2,
         # stage passes: x (fwd), g and x (bwd): read dst + src (L2 window), write stage

@@ -461,25 +461,11 @@ lx::ms::MainArgs<R> main_args(const View<R>& v, int rows) {
     return a;
 }
 
-template <class R>
-lx::ms::FixArgs<R> fix_args(const View<R>& v, int rows) {
-    lx::ms::FixArgs<R> f;
-    std::memset(&f, 0, sizeof(f));
-    f.A = v.A;
-    f.perm_a = v.pa;
-    f.B = v.B;
-    f.perm_b = v.pb;
-    f.part = v.part;
-    f.n = v.n;
-    f.k = v.k;
-    f.T = v.T;
-    f.rows = rows;
-    f.inv_t = v.inv_t;
-    f.cphi = v.cphi;
-    f.sphi = v.sphi;
-    f.cpsi = v.cpsi;
-    f.spsi = v.spsi;
-    return f;
+template <class R, int NG, int NX, bool BWD, bool SEQ = false>
+void launch_tileagg(const lx::ms::MainArgs<R>& a, cudaStream_t st) {
+    launch("lx_tileagg", st, [&] {
+        lx::ms::lx_tileagg<R, NG, NX, BWD, SEQ><<<a.T, lx::ms::kAggThreads, 0, st>>>(a);
+    });
 }
 
 template <class R, int NG, int NX, bool BWD, bool SEQ = false>
@@ -554,14 +540,31 @@ struct Scratch {
           sf((size_t)T * rs, st) {}
 };
 
+// One merged pass: tile aggregates -> fp64 tile carries -> main kernel with
+// final outputs.  `a` already holds inputs, index arrays and output pointers.
+template <class R, int NG, int NX, bool BWD, bool SEQ = false>
+void run_merged(lx::ms::MainArgs<R>& a, const char* name, cudaStream_t st) {
+    constexpr int NC = NG + NX;
+    Scratch s(2 * NC, a.rows, a.T, sizeof(R), st);
+    a.aggp = s.aggp.as<R>();
+    a.aggq = s.aggq.as<R>();
+    a.s_last = s.sl.as<R>();
+    a.s_first = s.sf.as<R>();
+    a.cp = s.cp.as<R>();
+    a.cq = s.cq.as<R>();
+    launch_tileagg<R, NG, NX, BWD, SEQ>(a, st);
+    const unsigned gmask = BWD ? (1u << NG) - 1u : 0u;
+    const unsigned xmask = BWD ? ((1u << NX) - 1u) << NG : 0u;
+    launch_carry<R, NC>(s.aggp.as<R>(), s.aggq.as<R>(), s.cp.as<R>(), s.cq.as<R>(), s.sl.as<R>(), s.sf.as<R>(), a.T,
+                        a.rows, gmask, xmask, st);
+    launch_main<R, NG, NX, BWD, SEQ>(name, a, st);
+}
+
 template <class R, int NX>
 void apply_fwd(const View<R>& v, const R* X, int rows, R* Y, cudaStream_t st) {
-    constexpr int NC = NX;
-    DBuf wa0((size_t)rows * v.n * sizeof(R), st);
-    DBuf wa1(NX == 2 ? (size_t)rows * v.n * sizeof(R) : 0, st);
-    Scratch s(2 * NC, rows, v.T, sizeof(R), st);
     auto a = main_args(v, rows);
-    DBuf xst;
+    a.inv_t = v.inv_t;
+    DBuf xst, yst;
     if (v.dst_b) {  // gather x through the cols plan
         xst = stage_gather<R>(X, v.k, v.dst_b, v.k, rows, st);
         a.X = xst.as<R>();
@@ -570,42 +573,25 @@ void apply_fwd(const View<R>& v, const R* X, int rows, R* Y, cudaStream_t st) {
         a.X = X;
     }
     a.ldx = v.k;
-    a.wa[0] = wa0.as<R>();
-    a.wa[1] = wa1.as<R>();
-    a.aggp = s.aggp.as<R>();
-    a.aggq = s.aggq.as<R>();
-    a.s_last = s.sl.as<R>();
-    a.s_first = s.sf.as<R>();
-    launch_main<R, 0, NX, false>(NX == 2 ? "lx_main_fwd_phased" : "lx_main_fwd", a, st);
-    launch_carry<R, NC>(s.aggp.as<R>(), s.aggq.as<R>(), s.cp.as<R>(), s.cq.as<R>(), s.sl.as<R>(), s.sf.as<R>(), v.T,
-                        rows, 0u, 0u, st);
-    auto f = fix_args(v, rows);
-    f.cp = s.cp.as<R>();
-    f.cq = s.cq.as<R>();
-    f.s_last = s.sl.as<R>();
-    f.s_first = s.sf.as<R>();
-    f.wa[0] = wa0.as<R>();
-    f.wa[1] = wa1.as<R>();
-    DBuf yst;
     if (v.dst_a) {  // write bucket-staged, then scatter through the rows plan
         yst = DBuf((size_t)rows * v.n * sizeof(R), st);
-        f.y = yst.as<R>();
-        f.perm_a = v.pos_a;
+        a.y = yst.as<R>();
+        a.perm_a = v.pos_a;
     } else {
-        f.y = Y;
+        a.y = Y;
     }
-    f.ldy = v.n;
-    launch("lx_fix_fwd", st, [&] { lx::ms::lx_fix_fwd<R, NX><<<v.T, lx::ms::kFixThreads, 0, st>>>(f); });
+    a.ldy = v.n;
+    run_merged<R, 0, NX, false>(a, NX == 2 ? "lx_main_fwd_phased" : "lx_main_fwd", st);
+    xst.release();
     if (v.dst_a)
         stage_scatter<R>(v.dst_a, v.n, yst.as<R>(), Y, v.n, rows, nullptr, nullptr, nullptr, nullptr, st);
 }
 
 template <class R>
 void apply_trn(const View<R>& v, const R* G, int rows, R* Y, cudaStream_t st) {
-    DBuf wb0((size_t)rows * v.k * sizeof(R), st);
-    Scratch s(2, rows, v.T, sizeof(R), st);
     auto a = main_args(v, rows);
-    DBuf gst;
+    a.inv_t = v.inv_t;
+    DBuf gst, yst;
     if (v.dst_a) {
         gst = stage_gather<R>(G, v.n, v.dst_a, v.n, rows, st);
         a.G = gst.as<R>();
@@ -614,30 +600,16 @@ void apply_trn(const View<R>& v, const R* G, int rows, R* Y, cudaStream_t st) {
         a.G = G;
     }
     a.ldg = v.n;
-    a.wb[0] = wb0.as<R>();
-    a.aggp = s.aggp.as<R>();
-    a.aggq = s.aggq.as<R>();
-    a.s_last = s.sl.as<R>();
-    a.s_first = s.sf.as<R>();
-    launch_main<R, 1, 0, false>("lx_main_trn", a, st);
-    launch_carry<R, 1>(s.aggp.as<R>(), s.aggq.as<R>(), s.cp.as<R>(), s.cq.as<R>(), s.sl.as<R>(), s.sf.as<R>(), v.T,
-                       rows, 0u, 0u, st);
-    auto f = fix_args(v, rows);
-    f.cp = s.cp.as<R>();
-    f.cq = s.cq.as<R>();
-    f.s_last = s.sl.as<R>();
-    f.s_first = s.sf.as<R>();
-    f.wb[0] = wb0.as<R>();
-    DBuf yst;
     if (v.dst_b) {
         yst = DBuf((size_t)rows * v.k * sizeof(R), st);
-        f.y = yst.as<R>();
-        f.perm_b = v.pos_b;
+        a.y = yst.as<R>();
+        a.perm_b = v.pos_b;
     } else {
-        f.y = Y;
+        a.y = Y;
     }
-    f.ldy = v.k;
-    launch("lx_fix_trn", st, [&] { lx::ms::lx_fix_trn<R><<<v.T, lx::ms::kFixThreads, 0, st>>>(f); });
+    a.ldy = v.k;
+    run_merged<R, 1, 0, false>(a, "lx_main_trn", st);
+    gst.release();
     if (v.dst_b)
         stage_scatter<R>(v.dst_b, v.k, yst.as<R>(), Y, v.k, rows, nullptr, nullptr, nullptr, nullptr, st);
 }
@@ -645,93 +617,45 @@ void apply_trn(const View<R>& v, const R* G, int rows, R* Y, cudaStream_t st) {
 template <class R, int NCH>
 void backward_impl(const View<R>& v, const R* X, const R* G, int rows, R* xbar, R* abar, R* bbar, R* phibar,
                    R* psibar, cudaStream_t st) {
-    constexpr int NC = 2 * NCH;
     const size_t rs = sizeof(R);
-    DBuf wa[2], wa2[2], wb[2], wb2[2];
-    for (int c = 0; c < NCH; ++c) {
-        wa[c] = DBuf((size_t)rows * v.n * rs, st);
-        wb[c] = DBuf((size_t)rows * v.k * rs, st);
-        wb2[c] = DBuf((size_t)rows * v.k * rs, st);
-        if (NCH == 2) wa2[c] = DBuf((size_t)rows * v.n * rs, st);
-    }
-    DBuf gsave((size_t)rows * v.n * rs, st), xsave((size_t)rows * v.k * rs, st);
-    Scratch s(2 * NC, rows, v.T, rs, st);
     auto a = main_args(v, rows);
-    DBuf xst, gst;
+    a.inv_t = v.inv_t;
+    DBuf xst, gst, sxb, sbb, sqb, sab, spb;
     if (v.dst_b) {
         xst = stage_gather<R>(X, v.k, v.dst_b, v.k, rows, st);
         a.X = xst.as<R>();
         a.perm_b = v.pos_b;
+        sxb = DBuf((size_t)rows * v.k * rs, st);
+        sbb = DBuf((size_t)v.k * rs, st);
+        if (NCH == 2) sqb = DBuf((size_t)v.k * rs, st);
+        a.xbar = sxb.as<R>();
+        a.bbar = sbb.as<R>();
+        a.psibar = sqb.as<R>();
     } else {
         a.X = X;
+        a.xbar = xbar;
+        a.bbar = bbar;
+        a.psibar = psibar;
     }
     if (v.dst_a) {
         gst = stage_gather<R>(G, v.n, v.dst_a, v.n, rows, st);
         a.G = gst.as<R>();
         a.perm_a = v.pos_a;
+        sab = DBuf((size_t)v.n * rs, st);
+        if (NCH == 2) spb = DBuf((size_t)v.n * rs, st);
+        a.abar = sab.as<R>();
+        a.phibar = spb.as<R>();
     } else {
         a.G = G;
+        a.abar = abar;
+        a.phibar = phibar;
     }
     a.ldx = v.k;
     a.ldg = v.n;
-    for (int c = 0; c < NCH; ++c) {
-        a.wa[c] = wa[c].as<R>();
-        a.wa2[c] = wa2[c].as<R>();
-        a.wb[c] = wb[c].as<R>();
-        a.wb2[c] = wb2[c].as<R>();
-    }
-    a.gsave = gsave.as<R>();
-    a.xsave = xsave.as<R>();
-    a.aggp = s.aggp.as<R>();
-    a.aggq = s.aggq.as<R>();
-    a.s_last = s.sl.as<R>();
-    a.s_first = s.sf.as<R>();
-    launch_main<R, NCH, NCH, true>(NCH == 2 ? "lx_main_bwd_phased" : "lx_main_bwd", a, st);
+    a.ldxb = v.k;
+    run_merged<R, NCH, NCH, true>(a, NCH == 2 ? "lx_main_bwd_phased" : "lx_main_bwd", st);
     xst.release();
     gst.release();
-    const unsigned gmask = (1u << NCH) - 1u;
-    launch_carry<R, NC>(s.aggp.as<R>(), s.aggq.as<R>(), s.cp.as<R>(), s.cq.as<R>(), s.sl.as<R>(), s.sf.as<R>(), v.T,
-                        rows, gmask, gmask << NCH, st);
-    auto f = fix_args(v, rows);
-    f.cp = s.cp.as<R>();
-    f.cq = s.cq.as<R>();
-    f.s_last = s.sl.as<R>();
-    f.s_first = s.sf.as<R>();
-    for (int c = 0; c < NCH; ++c) {
-        f.wa[c] = wa[c].as<R>();
-        f.wa2[c] = wa2[c].as<R>();
-        f.wb[c] = wb[c].as<R>();
-        f.wb2[c] = wb2[c].as<R>();
-    }
-    f.gsave = gsave.as<R>();
-    f.xsave = xsave.as<R>();
-    DBuf sxb, sbb, sqb, sab, spb;  // bucket-staged outputs
-    if (v.dst_b) {
-        sxb = DBuf((size_t)rows * v.k * rs, st);
-        sbb = DBuf((size_t)v.k * rs, st);
-        if (NCH == 2) sqb = DBuf((size_t)v.k * rs, st);
-        f.xbar = sxb.as<R>();
-        f.ldxb = v.k;
-        f.bbar = sbb.as<R>();
-        f.psibar = sqb.as<R>();
-        f.perm_b = v.pos_b;
-    } else {
-        f.xbar = xbar;
-        f.ldxb = v.k;
-        f.bbar = bbar;
-        f.psibar = psibar;
-    }
-    if (v.dst_a) {
-        sab = DBuf((size_t)v.n * rs, st);
-        if (NCH == 2) spb = DBuf((size_t)v.n * rs, st);
-        f.abar = sab.as<R>();
-        f.phibar = spb.as<R>();
-        f.perm_a = v.pos_a;
-    } else {
-        f.abar = abar;
-        f.phibar = phibar;
-    }
-    launch("lx_fix_bwd", st, [&] { lx::ms::lx_fix_bwd<R, NCH><<<v.T, lx::ms::kFixThreads, 0, st>>>(f); });
     if (v.dst_b)
         stage_scatter<R>(v.dst_b, v.k, sxb.as<R>(), xbar, v.k, rows, sbb.as<R>(), bbar,
                          NCH == 2 ? sqb.as<R>() : nullptr, psibar, st);
@@ -905,9 +829,7 @@ void do_scan(const R* sorted, uint32_t m, const R* payload, R* pre, R* suf, cuda
     launch("lx_seq_partition", st, [&] {
         lx_seq_partition<<<(T + 256) / 256, 256, 0, st>>>(m, part.as<uint32_t>(), T);
     });
-    DBuf wa((size_t)m * sizeof(R), st), wa2((size_t)m * sizeof(R), st);
     DBuf dpre((size_t)m * sizeof(R), st), dsuf((size_t)m * sizeof(R), st);
-    Scratch s(2, 1, T, sizeof(R), st);
     MainArgs<R> a;
     std::memset(&a, 0, sizeof(a));
     a.A = vals.as<R>();
@@ -918,31 +840,9 @@ void do_scan(const R* sorted, uint32_t m, const R* payload, R* pre, R* suf, cuda
     a.rows = 1;
     a.X = pay.as<R>();
     a.ldx = m;
-    a.wa[0] = wa.as<R>();
-    a.wa2[0] = wa2.as<R>();
-    a.aggp = s.aggp.as<R>();
-    a.aggq = s.aggq.as<R>();
-    a.s_last = s.sl.as<R>();
-    a.s_first = s.sf.as<R>();
-    launch_main<R, 0, 1, false, true>("lx_main_seq", a, st);
-    launch_carry<R, 1>(s.aggp.as<R>(), s.aggq.as<R>(), s.cp.as<R>(), s.cq.as<R>(), s.sl.as<R>(), s.sf.as<R>(), T, 1,
-                       0u, 0u, st);
-    FixArgs<R> f;
-    std::memset(&f, 0, sizeof(f));
-    f.A = vals.as<R>();
-    f.part = part.as<uint32_t>();
-    f.n = m;
-    f.T = T;
-    f.rows = 1;
-    f.cp = s.cp.as<R>();
-    f.cq = s.cq.as<R>();
-    f.s_last = s.sl.as<R>();
-    f.s_first = s.sf.as<R>();
-    f.wa[0] = wa.as<R>();
-    f.wa2[0] = wa2.as<R>();
-    launch("lx_fix_seq", st, [&] {
-        lx_fix_seq<R><<<T, kFixThreads, 0, st>>>(f, dpre.as<R>(), dsuf.as<R>());
-    });
+    a.pre = dpre.as<R>();
+    a.suf = dsuf.as<R>();
+    run_merged<R, 0, 1, false, true>(a, "lx_main_seq", st);
     if (pre) ck(cudaMemcpyAsync(pre, dpre.p, (size_t)m * sizeof(R), cudaMemcpyDeviceToHost, st), "D2H");
     if (suf) ck(cudaMemcpyAsync(suf, dsuf.p, (size_t)m * sizeof(R), cudaMemcpyDeviceToHost, st), "D2H");
     ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");

@@ -142,16 +142,25 @@ struct MainArgs {
     const R* spsi;
     const R* cphi;
     const R* sphi;
-    R* wa[2];   // row-side outputs per x channel, [rows][n] sorted order
-    R* wa2[2];  // phased backward: P^x + Q^x at rows
-    R* wb[2];   // col-side outputs per g channel, [rows][k] sorted order
-    R* wb2[2];  // backward: Q^g - Pstrict^g at cols
-    R* gsave;   // backward: gathered g, [rows][n] sorted order
-    R* xsave;   // backward: gathered x, [rows][k] sorted order
-    R* aggp;    // [slot][rows][T] prefix tile aggregates, slot = 2*c + strict
-    R* aggq;    // suffix tile aggregates
-    R* s_last;  // [T] anchor of each tile's last merged element
+    R* aggp;    // [slot][rows][T] tile aggregates (lx_tileagg), slot = 2*c + strict
+    R* aggq;
+    R* s_last;  // [T] anchor of each tile's last merged element (lx_tileagg)
     R* s_first; // [T] anchor of each tile's first merged element
+    const R* cp;  // inclusive tile carries (lx_carry), [slot][rows][T]
+    const R* cq;
+    R inv_t;
+    // final outputs, written at index perm_a[i] / perm_b[j] (caller order, or
+    // the bucket-staged position when perm_* holds a plan's pos[] table)
+    R* y;       // forward: rows x ldy (row side);  transpose: rows x ldy (col side)
+    size_t ldy;
+    R* xbar;    // backward: rows x ldxb (col side)
+    size_t ldxb;
+    R* abar;    // backward: n, summed over rows
+    R* bbar;    // backward: k
+    R* phibar;  // phased backward
+    R* psibar;
+    R* pre;     // SEQ: inclusive prefix / suffix, sorted order
+    R* suf;
 };
 
 // Channel layout: g channels first (c < NG), then x channels.  Strict prefix
@@ -180,6 +189,13 @@ struct MainSmem {
     R payA[NG > 0 ? kTile : 1];          // gathered g of the tile rows (cp.async)
     R payB[NX > 0 ? kTile : 1];          // gathered x of the tile cols
 };
+
+// x_bar at one column element (shared by transpose and VJP so both produce
+// bit-identical x_bar): local P+Q, then the left and right tile carries.
+template <class R>
+__device__ __forceinline__ R xbar_value(R w, R eL, R cpv, R eR, R cqv) {
+    return xfma(eR, cqv, xfma(eL, cpv, w));
+}
 
 // Issue the async gathers of one row's payloads into shared memory.
 template <class R, int NG, int NX, bool SEQ>
@@ -360,6 +376,13 @@ __global__ void __launch_bounds__(kThreads, 2) lx_main(MainArgs<R> p) {
     const R* cpsi = p.cpsi;
     const R* spsi = p.spsi;
     const size_t T = p.T;
+    // neighbouring tiles' edge anchors: the carries' reference points
+    const bool hl = t > 0, hr = t + 1 < p.T;
+    const R SL = hl ? p.s_last[t - 1] : R(0);
+    const R SR = hr ? p.s_first[t + 1] : R(0);
+    R acc1[kItems], acc2[kItems];  // backward: a_bar/b_bar and phi_bar/psi_bar over rows
+#pragma unroll
+    for (int q = 0; q < kItems; ++q) acc1[q] = acc2[q] = R(0);
 
     for (int r = 0; r < p.rows; ++r) {
         if (r > 0) {
@@ -382,7 +405,6 @@ __global__ void __launch_bounds__(kThreads, 2) lx_main(MainArgs<R> p) {
                     pay[0][q] = sm.payB[li];
                 } else if constexpr (NG > 0) {
                     const R g = sm.payA[li];
-                    if constexpr (BWD) p.gsave[(size_t)r * p.n + a0 + li] = g;
                     if constexpr (NG == 2) {
                         pay[0][q] = xmul(cphi[a0 + li], g);
                         pay[1][q] = xmul(sphi[a0 + li], g);
@@ -393,7 +415,6 @@ __global__ void __launch_bounds__(kThreads, 2) lx_main(MainArgs<R> p) {
             } else {
                 if constexpr (NX > 0) {
                     const R x = sm.payB[li];
-                    if constexpr (BWD) p.xsave[(size_t)r * p.k + b0 + li] = x;
                     if constexpr (NX == 2) {
                         pay[NG][q] = xmul(cpsi[b0 + li], x);
                         pay[NG + 1][q] = xmul(spsi[b0 + li], x);
@@ -511,15 +532,6 @@ __global__ void __launch_bounds__(kThreads, 2) lx_main(MainArgs<R> p) {
                     sm.xqv[c][lane] = yv;
                     sm.xqw[c][lane] = yw;
                 }
-                // tile aggregates (inclusive over the whole tile)
-                if (lane == kWarps - 1) {
-                    p.aggp[((size_t)(2 * c) * p.rows + r) * T + t] = bv;
-                    if (C::pst(c)) p.aggp[((size_t)(2 * c + 1) * p.rows + r) * T + t] = bw;
-                }
-                if (lane == 0) {
-                    p.aggq[((size_t)(2 * c) * p.rows + r) * T + t] = cv;
-                    if (C::qst(c)) p.aggq[((size_t)(2 * c + 1) * p.rows + r) * T + t] = cw;
-                }
             }
         }
         // lane-exclusive values within the warp
@@ -570,41 +582,238 @@ __global__ void __launch_bounds__(kThreads, 2) lx_main(MainArgs<R> p) {
             }
         }
 
-        // ---- outputs (sorted order; the fix-up pass scatters) ----
+        // ---- fold in the tile carries (from lx_tileagg + lx_carry) and write
+        // final outputs; every carry is one exp of an anchor difference ----
+        R cpv[NC], cps[NC], cqv[NC], cqs[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            cpv[c] = hl ? p.cp[((size_t)(2 * c) * p.rows + r) * T + t - 1] : R(0);
+            cps[c] = (hl && C::pst(c)) ? p.cp[((size_t)(2 * c + 1) * p.rows + r) * T + t - 1] : R(0);
+            cqv[c] = hr ? p.cq[((size_t)(2 * c) * p.rows + r) * T + t + 1] : R(0);
+            cqs[c] = (hr && C::qst(c)) ? p.cq[((size_t)(2 * c + 1) * p.rows + r) * T + t + 1] : R(0);
+        }
+#pragma unroll
+        for (int q = 0; q < kItems; ++q) {
+            const uint32_t cd = code[q];
+            if (!(cd & 0x40000000u)) continue;
+            const uint32_t li = cd & 0x3fffffffu;
+            const R eL = hl ? xexp(xsub(SL, s[q])) : R(0);
+            const R eR = hr ? xexp(xsub(s[q], SR)) : R(0);
+            if (cd & 0x80000000u) {  // ---- row element ----
+                const uint32_t i = a0 + li;
+                if constexpr (SEQ) {
+                    p.pre[(size_t)r * p.n + i] = xfma(eL, cpv[0], pi[0][q]);
+                    p.suf[(size_t)r * p.n + i] = xfma(eR, cqv[0], qi[0][q]);
+                } else if constexpr (!BWD && NX > 0) {
+                    R val[2];
+#pragma unroll
+                    for (int c = 0; c < NX; ++c)
+                        val[c] = xfma(eR, cqv[NG + c], xfma(eL, cpv[NG + c], xadd(pi[NG + c][q], qi[NG + c][q])));
+                    R out = val[0];
+                    if constexpr (NX == 2) out = xadd(xmul(cphi[i], val[0]), xmul(sphi[i], val[1]));
+                    p.y[(size_t)r * p.ldy + p.perm_a[i]] = out;
+                } else if constexpr (BWD) {
+                    const R g = sm.payA[li];
+                    R m0 = R(1), m1 = R(0);
+                    if constexpr (NG == 2) {
+                        m0 = cphi[i];
+                        m1 = sphi[i];
+                    }
+                    R inner[NX], pq[NX];
+#pragma unroll
+                    for (int c = 0; c < NX; ++c) {
+                        const int cc = NG + c;
+                        const R strict_right = hr ? ((s[q] < SR) ? xmul(eR, cqv[cc]) : cqs[cc]) : R(0);
+                        inner[c] = xsub(xadd(xsub(qs[cc][q], pi[cc][q]), strict_right), xmul(eL, cpv[cc]));
+                        pq[c] = xfma(eR, cqv[cc], xfma(eL, cpv[cc], xadd(pi[cc][q], qi[cc][q])));
+                    }
+                    if constexpr (NX == 2) {
+                        acc1[q] = xfma(xmul(xmul(m0, g), p.inv_t), inner[0], acc1[q]);
+                        acc1[q] = xfma(xmul(xmul(m1, g), p.inv_t), inner[1], acc1[q]);
+                        acc2[q] = xfma(g, xadd(xmul(-m1, pq[0]), xmul(m0, pq[1])), acc2[q]);
+                    } else {
+                        acc1[q] = xfma(xmul(g, p.inv_t), inner[0], acc1[q]);
+                    }
+                }
+            } else {  // ---- column element ----
+                if constexpr (NG > 0) {
+                    const uint32_t j = b0 + li;
+                    R xb[NG];
+#pragma unroll
+                    for (int c = 0; c < NG; ++c)
+                        xb[c] = xbar_value(xadd(pi[c][q], qi[c][q]), eL, cpv[c], eR, cqv[c]);
+                    if constexpr (!BWD) {
+                        p.y[(size_t)r * p.ldy + p.perm_b[j]] = xb[0];
+                    } else {
+                        const R x = sm.payB[li];
+                        R m0 = R(1), m1 = R(0);
+                        if constexpr (NG == 2) {
+                            m0 = cpsi[j];
+                            m1 = spsi[j];
+                        }
+                        R inner[NG];
+#pragma unroll
+                        for (int c = 0; c < NG; ++c) {
+                            const R strict_left = hl ? ((SL < s[q]) ? xmul(eL, cpv[c]) : cps[c]) : R(0);
+                            inner[c] = xsub(xfma(eR, cqv[c], xsub(qi[c][q], ps[c][q])), strict_left);
+                        }
+                        const uint32_t u = p.perm_b[j];
+                        if constexpr (NG == 2) {
+                            p.xbar[(size_t)r * p.ldxb + u] = xadd(xmul(m0, xb[0]), xmul(m1, xb[1]));
+                            acc2[q] = xfma(x, xadd(xmul(-m1, xb[0]), xmul(m0, xb[1])), acc2[q]);
+                            acc1[q] = xfma(xmul(xmul(m0, x), p.inv_t), inner[0], acc1[q]);
+                            acc1[q] = xfma(xmul(xmul(m1, x), p.inv_t), inner[1], acc1[q]);
+                        } else {
+                            p.xbar[(size_t)r * p.ldxb + u] = xb[0];
+                            acc1[q] = xfma(xmul(x, p.inv_t), inner[0], acc1[q]);
+                        }
+                    }
+                }
+            }
+        }
+    }
+    if constexpr (BWD) {  // anchor cotangents summed over rows
 #pragma unroll
         for (int q = 0; q < kItems; ++q) {
             const uint32_t cd = code[q];
             if (!(cd & 0x40000000u)) continue;
             const uint32_t li = cd & 0x3fffffffu;
             if (cd & 0x80000000u) {
-                const size_t o = (size_t)r * p.n + a0 + li;
-                if constexpr (SEQ) {
-                    p.wa[0][o] = pi[0][q];
-                    p.wa2[0][o] = qi[0][q];
-                    continue;
-                }
-#pragma unroll
-                for (int c = NG; c < NC; ++c) {
-                    if constexpr (BWD) {
-                        p.wa[c - NG][o] = xsub(qs[c][q], pi[c][q]);
-                        if constexpr (NX == 2) p.wa2[c - NG][o] = xadd(pi[c][q], qi[c][q]);
-                    } else {
-                        p.wa[c - NG][o] = xadd(pi[c][q], qi[c][q]);
-                    }
-                }
+                const uint32_t u = p.perm_a[a0 + li];
+                p.abar[u] = acc1[q];
+                if constexpr (NG == 2) p.phibar[u] = acc2[q];
             } else {
-                const size_t o = (size_t)r * p.k + b0 + li;
-#pragma unroll
-                for (int c = 0; c < NG; ++c) {
-                    p.wb[c][o] = xadd(pi[c][q], qi[c][q]);
-                    if constexpr (BWD) p.wb2[c][o] = xsub(qi[c][q], ps[c][q]);
-                }
+                const uint32_t u = p.perm_b[b0 + li];
+                p.bbar[u] = acc1[q];
+                if constexpr (NG == 2) p.psibar[u] = acc2[q];
             }
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// tile aggregates (pre-pass): for every merge tile and row, per channel
+//   prefix  sum_e exp(s_e - S_last) pay_e     (+ strict: only s_e < S_last)
+//   suffix  sum_e exp(S_first - s_e) pay_e    (+ strict: only s_e > S_first)
+// summed directly (every term one exp of an anchor difference) in a fixed
+// order (thread-strided partials, then a fixed tree), so they are
+// deterministic and independent of the batch size.  Only the elements that
+// carry payload contribute: rows for g channels, cols for x channels.
+// ---------------------------------------------------------------------------
+constexpr int kAggThreads = 256;
+
+template <class R, int NG, int NX, bool BWD, bool SEQ = false>
+__global__ void __launch_bounds__(kAggThreads) lx_tileagg(MainArgs<R> p) {
+    using C = Ch<NG, NX, BWD>;
+    constexpr int NC = C::NC;
+    constexpr int NW = kAggThreads / 32;
+    const uint32_t t = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t a0 = p.part[t], a1 = p.part[t + 1];
+    const unsigned long long d0 = (unsigned long long)t * kTile;
+    const unsigned long long total = (unsigned long long)p.n + p.k;
+    const unsigned long long d1 = d0 + kTile < total ? d0 + kTile : total;
+    const uint32_t b0 = (uint32_t)(d0 - a0), b1 = (uint32_t)(d1 - a1);
+    const int na = (int)(a1 - a0), nb = (int)(b1 - b0);
+    R S_last, S_first;
+    if (na == 0) {
+        S_last = p.B[b1 - 1];
+        S_first = p.B[b0];
+    } else if (nb == 0) {
+        S_last = p.A[a1 - 1];
+        S_first = p.A[a0];
+    } else {
+        const R al = p.A[a1 - 1], bl = p.B[b1 - 1], af = p.A[a0], bf = p.B[b0];
+        S_last = al > bl ? al : bl;
+        S_first = af < bf ? af : bf;
+    }
+    __shared__ R red[4 * NC][NW];
+    const size_t T = p.T;
+    for (int r = 0; r < p.rows; ++r) {
+        R pi[NC], ps[NC], qi[NC], qs[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) pi[c] = ps[c] = qi[c] = qs[c] = R(0);
+        if constexpr (NG > 0 || SEQ) {
+            for (int i = tid; i < na; i += kAggThreads) {
+                const R s = p.A[a0 + i];
+                const R e1 = xexp(xsub(s, S_last)), e2 = xexp(xsub(S_first, s));
+                if constexpr (SEQ) {
+                    const R x = p.X[(size_t)r * p.ldx + a0 + i];
+                    pi[0] = xfma(e1, x, pi[0]);
+                    qi[0] = xfma(e2, x, qi[0]);
+                } else {
+                    const R g = p.G[(size_t)r * p.ldg + p.perm_a[a0 + i]];
+                    R pay[NG > 0 ? NG : 1];
+                    if constexpr (NG == 2) {
+                        pay[0] = xmul(p.cphi[a0 + i], g);
+                        pay[1] = xmul(p.sphi[a0 + i], g);
+                    } else {
+                        pay[0] = g;
+                    }
+#pragma unroll
+                    for (int c = 0; c < NG; ++c) {
+                        const R pe = xmul(e1, pay[c]);
+                        pi[c] = xadd(pi[c], pe);
+                        if (C::pst(c) && s < S_last) ps[c] = xadd(ps[c], pe);
+                        qi[c] = xfma(e2, pay[c], qi[c]);
+                    }
+                }
+            }
+        }
+        if constexpr (NX > 0 && !SEQ) {
+            for (int j = tid; j < nb; j += kAggThreads) {
+                const R s = p.B[b0 + j];
+                const R e1 = xexp(xsub(s, S_last)), e2 = xexp(xsub(S_first, s));
+                const R x = p.X[(size_t)r * p.ldx + p.perm_b[b0 + j]];
+                R pay[NX];
+                if constexpr (NX == 2) {
+                    pay[0] = xmul(p.cpsi[b0 + j], x);
+                    pay[1] = xmul(p.spsi[b0 + j], x);
+                } else {
+                    pay[0] = x;
+                }
+#pragma unroll
+                for (int c = NG; c < NC; ++c) {
+                    pi[c] = xfma(e1, pay[c - NG], pi[c]);
+                    const R qe = xmul(e2, pay[c - NG]);
+                    qi[c] = xadd(qi[c], qe);
+                    if (C::qst(c) && S_first < s) qs[c] = xadd(qs[c], qe);
+                }
+            }
+        }
+        // fixed-order block reduction
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                pi[c] = xadd(pi[c], __shfl_xor_sync(FULL, pi[c], off));
+                ps[c] = xadd(ps[c], __shfl_xor_sync(FULL, ps[c], off));
+                qi[c] = xadd(qi[c], __shfl_xor_sync(FULL, qi[c], off));
+                qs[c] = xadd(qs[c], __shfl_xor_sync(FULL, qs[c], off));
+            }
+            if (lane == 0) {
+                red[4 * c + 0][warp] = pi[c];
+                red[4 * c + 1][warp] = ps[c];
+                red[4 * c + 2][warp] = qi[c];
+                red[4 * c + 3][warp] = qs[c];
+            }
+        }
+        __syncthreads();
+        if (tid < 4 * NC) {
+            R v = red[tid][0];
+#pragma unroll
+            for (int w = 1; w < NW; ++w) v = xadd(v, red[tid][w]);
+            const int c = tid >> 2, kind = tid & 3;
+            if (kind == 0) p.aggp[((size_t)(2 * c) * p.rows + r) * T + t] = v;
+            if (kind == 1 && C::pst(c)) p.aggp[((size_t)(2 * c + 1) * p.rows + r) * T + t] = v;
+            if (kind == 2) p.aggq[((size_t)(2 * c) * p.rows + r) * T + t] = v;
+            if (kind == 3 && C::qst(c)) p.aggq[((size_t)(2 * c + 1) * p.rows + r) * T + t] = v;
+        }
+        __syncthreads();
+    }
     if (tid == 0) {
-        p.s_last[t] = s_end;
-        p.s_first[t] = na == 0 ? sB[0] : (nb == 0 ? sA[0] : (sA[0] < sB[0] ? sA[0] : sB[0]));
+        p.s_last[t] = S_last;
+        p.s_first[t] = S_first;
     }
 }
 
@@ -822,369 +1031,6 @@ __global__ void __launch_bounds__(kCarryThreads) lx_carry(CarryArgs<R, NC> a) {
         for (int c = 0; c < NC; ++c) {
             out[((size_t)(2 * c) * rows + r) * TT + u] = (R)iv[c];
             if ((stm >> c) & 1) out[((size_t)(2 * c + 1) * rows + r) * TT + u] = (R)iw[c];
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// fix-up passes: fold the tile carries in, apply phases, scatter to caller order
-// ---------------------------------------------------------------------------
-template <class R>
-struct FixArgs {
-    const R* A;
-    const uint32_t* perm_a;
-    const R* B;
-    const uint32_t* perm_b;
-    const uint32_t* part;
-    uint32_t n, k, T;
-    int rows;
-    R inv_t;
-    const R* cp;  // carries, [slot][rows][T]
-    const R* cq;
-    const R* s_last;
-    const R* s_first;
-    const R* wa[2];
-    const R* wa2[2];
-    const R* wb[2];
-    const R* wb2[2];
-    const R* gsave;
-    const R* xsave;
-    const R* cpsi;
-    const R* spsi;
-    const R* cphi;
-    const R* sphi;
-    R* y;  // forward: rows x ldy (caller row order); transpose: rows x ldy over cols
-    size_t ldy;
-    R* xbar;  // backward
-    size_t ldxb;
-    R* abar;
-    R* bbar;
-    R* phibar;
-    R* psibar;
-};
-
-// shared: tile-carry lookups (value of channel-slot at tile t-1 / t+1 for row r)
-template <class R>
-__device__ __forceinline__ R carry_at(const R* c, int slot, int rows, int r, size_t T, size_t t) {
-    return c[((size_t)slot * rows + r) * T + t];
-}
-
-// Fix-up kernels: one CTA per merged tile; each thread owns up to kFixItems
-// elements of each side (a tile has at most kTile = kFixThreads * kFixItems)
-// and issues all of their loads before any use, so every thread keeps
-// kFixItems x (arrays) independent requests in flight.
-constexpr int kFixItems = kTile / kFixThreads;
-
-struct TileRange {
-    uint32_t a0, a1, b0, b1;
-    bool hl, hr;
-};
-
-template <class R>
-__device__ __forceinline__ TileRange tile_range(const FixArgs<R>& p, uint32_t t) {
-    TileRange r;
-    r.a0 = p.part[t];
-    r.a1 = p.part[t + 1];
-    const unsigned long long d0 = (unsigned long long)t * kTile;
-    const unsigned long long total = (unsigned long long)p.n + p.k;
-    const unsigned long long d1 = d0 + kTile < total ? d0 + kTile : total;
-    r.b0 = (uint32_t)(d0 - r.a0);
-    r.b1 = (uint32_t)(d1 - r.a1);
-    r.hl = t > 0;
-    r.hr = t + 1 < p.T;
-    return r;
-}
-
-// Forward fix-up (NG == 0): outputs at row elements.
-template <class R, int NX>
-__global__ void __launch_bounds__(kFixThreads) lx_fix_fwd(FixArgs<R> p) {
-    const uint32_t t = blockIdx.x;
-    const size_t T = p.T;
-    const TileRange tr = tile_range(p, t);
-    const R SL = tr.hl ? p.s_last[t - 1] : R(0);
-    const R SR = tr.hr ? p.s_first[t + 1] : R(0);
-    R s[kFixItems], eL[kFixItems], eR[kFixItems];
-    uint32_t u[kFixItems];
-#pragma unroll
-    for (int j = 0; j < kFixItems; ++j) {
-        const uint32_t i = tr.a0 + threadIdx.x + j * kFixThreads;
-        const bool ok = i < tr.a1;
-        s[j] = ok ? p.A[i] : R(0);
-        u[j] = ok ? p.perm_a[i] : 0u;
-    }
-#pragma unroll
-    for (int j = 0; j < kFixItems; ++j) {
-        eL[j] = tr.hl ? xexp(xsub(SL, s[j])) : R(0);
-        eR[j] = tr.hr ? xexp(xsub(s[j], SR)) : R(0);
-    }
-    for (int r = 0; r < p.rows; ++r) {
-        R cpv[2], cqv[2];
-#pragma unroll
-        for (int c = 0; c < NX; ++c) {
-            cpv[c] = tr.hl ? carry_at(p.cp, 2 * c, p.rows, r, T, t - 1) : R(0);
-            cqv[c] = tr.hr ? carry_at(p.cq, 2 * c, p.rows, r, T, t + 1) : R(0);
-        }
-        R w[2][kFixItems];
-#pragma unroll
-        for (int j = 0; j < kFixItems; ++j) {
-            const uint32_t i = tr.a0 + threadIdx.x + j * kFixThreads;
-#pragma unroll
-            for (int c = 0; c < NX; ++c) w[c][j] = i < tr.a1 ? p.wa[c][(size_t)r * p.n + i] : R(0);
-        }
-        R ph0[kFixItems], ph1[kFixItems];
-        if constexpr (NX == 2) {
-#pragma unroll
-            for (int j = 0; j < kFixItems; ++j) {
-                const uint32_t i = tr.a0 + threadIdx.x + j * kFixThreads;
-                ph0[j] = i < tr.a1 ? p.cphi[i] : R(0);
-                ph1[j] = i < tr.a1 ? p.sphi[i] : R(0);
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < kFixItems; ++j) {
-            const uint32_t i = tr.a0 + threadIdx.x + j * kFixThreads;
-            if (i >= tr.a1) continue;
-            R val[2];
-#pragma unroll
-            for (int c = 0; c < NX; ++c) val[c] = xfma(eR[j], cqv[c], xfma(eL[j], cpv[c], w[c][j]));
-            R out = val[0];
-            if constexpr (NX == 2) out = xadd(xmul(ph0[j], val[0]), xmul(ph1[j], val[1]));
-            p.y[(size_t)r * p.ldy + u[j]] = out;
-        }
-    }
-}
-
-// x_bar at one column element for g channel c (shared by transpose and VJP so
-// both produce bit-identical x_bar).
-template <class R>
-__device__ __forceinline__ R xbar_value(R wb, R eL, R cpv, R eR, R cqv) {
-    return xfma(eR, cqv, xfma(eL, cpv, wb));
-}
-
-// Transpose fix-up (NX == 0, NG == 1): outputs at column elements.
-template <class R>
-__global__ void __launch_bounds__(kFixThreads) lx_fix_trn(FixArgs<R> p) {
-    const uint32_t t = blockIdx.x;
-    const size_t T = p.T;
-    const TileRange tr = tile_range(p, t);
-    const R SL = tr.hl ? p.s_last[t - 1] : R(0);
-    const R SR = tr.hr ? p.s_first[t + 1] : R(0);
-    R s[kFixItems], eL[kFixItems], eR[kFixItems];
-    uint32_t u[kFixItems];
-#pragma unroll
-    for (int j = 0; j < kFixItems; ++j) {
-        const uint32_t i = tr.b0 + threadIdx.x + j * kFixThreads;
-        const bool ok = i < tr.b1;
-        s[j] = ok ? p.B[i] : R(0);
-        u[j] = ok ? p.perm_b[i] : 0u;
-    }
-#pragma unroll
-    for (int j = 0; j < kFixItems; ++j) {
-        eL[j] = tr.hl ? xexp(xsub(SL, s[j])) : R(0);
-        eR[j] = tr.hr ? xexp(xsub(s[j], SR)) : R(0);
-    }
-    for (int r = 0; r < p.rows; ++r) {
-        const R cpv = tr.hl ? carry_at(p.cp, 0, p.rows, r, T, t - 1) : R(0);
-        const R cqv = tr.hr ? carry_at(p.cq, 0, p.rows, r, T, t + 1) : R(0);
-        R w[kFixItems];
-#pragma unroll
-        for (int j = 0; j < kFixItems; ++j) {
-            const uint32_t i = tr.b0 + threadIdx.x + j * kFixThreads;
-            w[j] = i < tr.b1 ? p.wb[0][(size_t)r * p.k + i] : R(0);
-        }
-#pragma unroll
-        for (int j = 0; j < kFixItems; ++j) {
-            const uint32_t i = tr.b0 + threadIdx.x + j * kFixThreads;
-            if (i < tr.b1) p.y[(size_t)r * p.ldy + u[j]] = xbar_value(w[j], eL[j], cpv, eR[j], cqv);
-        }
-    }
-}
-
-// Backward fix-up: x_bar (per row), b_bar / psi_bar (summed over rows) at
-// column elements; a_bar / phi_bar (summed over rows) at row elements.
-template <class R, int NCH>
-__global__ void __launch_bounds__(kFixThreads) lx_fix_bwd(FixArgs<R> p) {
-    // channels: g = 0..NCH-1, x = NCH..2*NCH-1
-    const uint32_t t = blockIdx.x;
-    const size_t T = p.T;
-    const TileRange tr = tile_range(p, t);
-    const R SL = tr.hl ? p.s_last[t - 1] : R(0);
-    const R SR = tr.hr ? p.s_first[t + 1] : R(0);
-    const int rows = p.rows;
-    // ---------------- column side ----------------
-    {
-        R s[kFixItems], eL[kFixItems], eR[kFixItems], m0[kFixItems], m1[kFixItems];
-        uint32_t u[kFixItems];
-#pragma unroll
-        for (int j = 0; j < kFixItems; ++j) {
-            const uint32_t i = tr.b0 + threadIdx.x + j * kFixThreads;
-            const bool ok = i < tr.b1;
-            s[j] = ok ? p.B[i] : R(0);
-            u[j] = ok ? p.perm_b[i] : 0u;
-            m0[j] = R(1);
-            m1[j] = R(0);
-            if constexpr (NCH == 2) {
-                m0[j] = ok ? p.cpsi[i] : R(0);
-                m1[j] = ok ? p.spsi[i] : R(0);
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < kFixItems; ++j) {
-            eL[j] = tr.hl ? xexp(xsub(SL, s[j])) : R(0);
-            eR[j] = tr.hr ? xexp(xsub(s[j], SR)) : R(0);
-        }
-        R acc_b[kFixItems], acc_psi[kFixItems];
-#pragma unroll
-        for (int j = 0; j < kFixItems; ++j) acc_b[j] = acc_psi[j] = R(0);
-        for (int r = 0; r < rows; ++r) {
-            R cpv[NCH], cps[NCH], cqv[NCH];
-#pragma unroll
-            for (int c = 0; c < NCH; ++c) {
-                cpv[c] = tr.hl ? carry_at(p.cp, 2 * c, rows, r, T, t - 1) : R(0);
-                cps[c] = tr.hl ? carry_at(p.cp, 2 * c + 1, rows, r, T, t - 1) : R(0);
-                cqv[c] = tr.hr ? carry_at(p.cq, 2 * c, rows, r, T, t + 1) : R(0);
-            }
-            R wb[NCH][kFixItems], wb2[NCH][kFixItems], xr[kFixItems];
-#pragma unroll
-            for (int j = 0; j < kFixItems; ++j) {
-                const uint32_t i = tr.b0 + threadIdx.x + j * kFixThreads;
-                const bool ok = i < tr.b1;
-                const size_t o = (size_t)r * p.k + i;
-#pragma unroll
-                for (int c = 0; c < NCH; ++c) {
-                    wb[c][j] = ok ? p.wb[c][o] : R(0);
-                    wb2[c][j] = ok ? p.wb2[c][o] : R(0);
-                }
-                xr[j] = ok ? p.xsave[o] : R(0);
-            }
-#pragma unroll
-            for (int j = 0; j < kFixItems; ++j) {
-                const uint32_t i = tr.b0 + threadIdx.x + j * kFixThreads;
-                if (i >= tr.b1) continue;
-                const bool ltL = SL < s[j];
-                R xb[NCH], inner[NCH];
-#pragma unroll
-                for (int c = 0; c < NCH; ++c) {
-                    xb[c] = xbar_value(wb[c][j], eL[j], cpv[c], eR[j], cqv[c]);
-                    const R strict_left = tr.hl ? (ltL ? xmul(eL[j], cpv[c]) : cps[c]) : R(0);
-                    inner[c] = xsub(xfma(eR[j], cqv[c], wb2[c][j]), strict_left);
-                }
-                if constexpr (NCH == 2) {
-                    p.xbar[(size_t)r * p.ldxb + u[j]] = xadd(xmul(m0[j], xb[0]), xmul(m1[j], xb[1]));
-                    acc_psi[j] = xfma(xr[j], xadd(xmul(-m1[j], xb[0]), xmul(m0[j], xb[1])), acc_psi[j]);
-                    acc_b[j] = xfma(xmul(xmul(m0[j], xr[j]), p.inv_t), inner[0], acc_b[j]);
-                    acc_b[j] = xfma(xmul(xmul(m1[j], xr[j]), p.inv_t), inner[1], acc_b[j]);
-                } else {
-                    p.xbar[(size_t)r * p.ldxb + u[j]] = xb[0];
-                    acc_b[j] = xfma(xmul(xr[j], p.inv_t), inner[0], acc_b[j]);
-                }
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < kFixItems; ++j) {
-            const uint32_t i = tr.b0 + threadIdx.x + j * kFixThreads;
-            if (i >= tr.b1) continue;
-            p.bbar[u[j]] = acc_b[j];
-            if constexpr (NCH == 2) p.psibar[u[j]] = acc_psi[j];
-        }
-    }
-    // ---------------- row side ----------------
-    {
-        R s[kFixItems], eL[kFixItems], eR[kFixItems], m0[kFixItems], m1[kFixItems];
-        uint32_t u[kFixItems];
-#pragma unroll
-        for (int j = 0; j < kFixItems; ++j) {
-            const uint32_t i = tr.a0 + threadIdx.x + j * kFixThreads;
-            const bool ok = i < tr.a1;
-            s[j] = ok ? p.A[i] : R(0);
-            u[j] = ok ? p.perm_a[i] : 0u;
-            m0[j] = R(1);
-            m1[j] = R(0);
-            if constexpr (NCH == 2) {
-                m0[j] = ok ? p.cphi[i] : R(0);
-                m1[j] = ok ? p.sphi[i] : R(0);
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < kFixItems; ++j) {
-            eL[j] = tr.hl ? xexp(xsub(SL, s[j])) : R(0);
-            eR[j] = tr.hr ? xexp(xsub(s[j], SR)) : R(0);
-        }
-        R acc_a[kFixItems], acc_phi[kFixItems];
-#pragma unroll
-        for (int j = 0; j < kFixItems; ++j) acc_a[j] = acc_phi[j] = R(0);
-        for (int r = 0; r < rows; ++r) {
-            R cpv[NCH], cqv[NCH], cqs[NCH];
-#pragma unroll
-            for (int c = 0; c < NCH; ++c) {
-                const int cc = NCH + c;
-                cpv[c] = tr.hl ? carry_at(p.cp, 2 * cc, rows, r, T, t - 1) : R(0);
-                cqv[c] = tr.hr ? carry_at(p.cq, 2 * cc, rows, r, T, t + 1) : R(0);
-                cqs[c] = tr.hr ? carry_at(p.cq, 2 * cc + 1, rows, r, T, t + 1) : R(0);
-            }
-            R wa[NCH][kFixItems], wa2[NCH][kFixItems], gr[kFixItems];
-#pragma unroll
-            for (int j = 0; j < kFixItems; ++j) {
-                const uint32_t i = tr.a0 + threadIdx.x + j * kFixThreads;
-                const bool ok = i < tr.a1;
-                const size_t o = (size_t)r * p.n + i;
-#pragma unroll
-                for (int c = 0; c < NCH; ++c) {
-                    wa[c][j] = ok ? p.wa[c][o] : R(0);
-                    wa2[c][j] = (NCH == 2 && ok) ? p.wa2[c][o] : R(0);
-                }
-                gr[j] = ok ? p.gsave[o] : R(0);
-            }
-#pragma unroll
-            for (int j = 0; j < kFixItems; ++j) {
-                const uint32_t i = tr.a0 + threadIdx.x + j * kFixThreads;
-                if (i >= tr.a1) continue;
-                const bool ltR = s[j] < SR;
-                R inner[NCH], pq[NCH];
-#pragma unroll
-                for (int c = 0; c < NCH; ++c) {
-                    const R strict_right = tr.hr ? (ltR ? xmul(eR[j], cqv[c]) : cqs[c]) : R(0);
-                    inner[c] = xsub(xadd(wa[c][j], strict_right), xmul(eL[j], cpv[c]));
-                    pq[c] = NCH == 2 ? xfma(eR[j], cqv[c], xfma(eL[j], cpv[c], wa2[c][j])) : R(0);
-                }
-                if constexpr (NCH == 2) {
-                    acc_a[j] = xfma(xmul(xmul(m0[j], gr[j]), p.inv_t), inner[0], acc_a[j]);
-                    acc_a[j] = xfma(xmul(xmul(m1[j], gr[j]), p.inv_t), inner[1], acc_a[j]);
-                    acc_phi[j] = xfma(gr[j], xadd(xmul(-m1[j], pq[0]), xmul(m0[j], pq[1])), acc_phi[j]);
-                } else {
-                    acc_a[j] = xfma(xmul(gr[j], p.inv_t), inner[0], acc_a[j]);
-                }
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < kFixItems; ++j) {
-            const uint32_t i = tr.a0 + threadIdx.x + j * kFixThreads;
-            if (i >= tr.a1) continue;
-            p.abar[u[j]] = acc_a[j];
-            if constexpr (NCH == 2) p.phibar[u[j]] = acc_phi[j];
-        }
-    }
-}
-
-// SEQ fix-up: prefix/suffix in sorted order (no permutation).
-template <class R>
-__global__ void __launch_bounds__(kFixThreads) lx_fix_seq(FixArgs<R> p, R* pre, R* suf) {
-    const uint32_t t = blockIdx.x;
-    const size_t T = p.T;
-    const uint32_t a0 = p.part[t], a1 = p.part[t + 1];
-    const bool hl = t > 0, hr = t + 1 < p.T;
-    const R SL = hl ? p.s_last[t - 1] : R(0);
-    const R SR = hr ? p.s_first[t + 1] : R(0);
-    for (uint32_t i = a0 + threadIdx.x; i < a1; i += kFixThreads) {
-        const R s = p.A[i];
-        const R eL = hl ? xexp(xsub(SL, s)) : R(0);
-        const R eR = hr ? xexp(xsub(s, SR)) : R(0);
-        for (int r = 0; r < p.rows; ++r) {
-            const R cpv = hl ? carry_at(p.cp, 0, p.rows, r, T, t - 1) : R(0);
-            const R cqv = hr ? carry_at(p.cq, 0, p.rows, r, T, t + 1) : R(0);
-            const size_t o = (size_t)r * p.n + i;
-            if (pre) pre[o] = xfma(eL, cpv, p.wa[0][o]);
-            if (suf) suf[o] = xfma(eR, cqv, p.wa2[0][o]);
         }
     }
 }
