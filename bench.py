@@ -73,8 +73,9 @@ class ClockSampler:
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index):
+    def __init__(self, index, interval=1.0):
         self.index = index
+        self.interval = interval
         self.samples = []
         self._stop = threading.Event()
         self._t = None
@@ -89,7 +90,7 @@ class ClockSampler:
                     self.samples.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(self.interval)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -227,7 +228,7 @@ def run_ours(args, rank, world, dist):
     launches0 = L.kernel_launches()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(local, args.clock_interval) as clk:
         barrier()
         ev0.record(stream)
         for _ in range(args.steps):
@@ -352,7 +353,7 @@ def run_e2e(args, torch, lib, n, k):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--log2n", type=int, default=30)
@@ -362,6 +363,8 @@ def main():
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--clock-interval", type=float, default=1.0,
+                    help="seconds between nvidia-smi samples during the timed region")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -161,6 +161,7 @@ struct Core {
     Side side[2];  // [ROWS], [COLS]
     std::mutex mu;
     DBuf part[2];  // merge-path tiles with side 0 (resp. 1) as the "A" operand, A-first
+    DBuf desc[2], sfirst[2], slast[2];  // per-tile descriptors and edge anchors
     uint32_t T[2] = {0, 0};
     DBuf ranks[4];  // [side*2 + strict]
     bool has_ranks[4] = {false, false, false, false};
@@ -201,6 +202,9 @@ struct View {
     uint32_t k;
     const R *cphi, *sphi, *cpsi, *spsi;
     const uint32_t* part;
+    const lx::ms::TileDesc<R>* desc;
+    const R* s_first;
+    const R* s_last;
     uint32_t T;
     R inv_t;
     const uint32_t *pos_a, *dst_a, *pos_b, *dst_b;  // null = direct permutation
@@ -214,9 +218,17 @@ void build_partition(Core& c, int which, cudaStream_t st) {
     const Side& b = c.side[1 - which];
     const uint32_t T = tiles_for((uint64_t)a.m + b.m);
     c.part[which] = DBuf((size_t)(T + 1) * 4, st);
+    c.desc[which] = DBuf((size_t)(T + 1) * sizeof(lx::ms::TileDesc<R>), st);
+    c.sfirst[which] = DBuf((size_t)T * sizeof(R), st);
+    c.slast[which] = DBuf((size_t)T * sizeof(R), st);
     launch("lx_partition", st, [&] {
         lx::ms::lx_partition<R, true><<<(T + 1 + 255) / 256, 256, 0, st>>>(
             a.vals.as<R>(), a.m, b.vals.as<R>(), b.m, c.part[which].as<uint32_t>(), T);
+    });
+    launch("lx_tiledesc", st, [&] {
+        lx::ms::lx_tiledesc<R><<<(T + 1 + 255) / 256, 256, 0, st>>>(
+            a.vals.as<R>(), a.m, b.vals.as<R>(), b.m, c.part[which].as<uint32_t>(), T,
+            c.desc[which].as<lx::ms::TileDesc<R>>(), c.sfirst[which].as<R>(), c.slast[which].as<R>());
     });
     c.T[which] = T;
 }
@@ -242,6 +254,9 @@ View<R> view(Core& c, bool swapped, cudaStream_t st) {
     v.cpsi = b.cph.as<R>();
     v.spsi = b.sph.as<R>();
     v.part = c.part[ia].as<uint32_t>();
+    v.desc = c.desc[ia].as<lx::ms::TileDesc<R>>();
+    v.s_first = c.sfirst[ia].as<R>();
+    v.s_last = c.slast[ia].as<R>();
     v.T = c.T[ia];
     v.inv_t = R(1) / R(c.t);
     v.pos_a = a.staged ? a.spos.as<uint32_t>() : nullptr;
@@ -450,6 +465,9 @@ lx::ms::MainArgs<R> main_args(const View<R>& v, int rows) {
     a.B = v.B;
     a.perm_b = v.pb;
     a.part = v.part;
+    a.desc = v.desc;
+    a.s_last = v.s_last;
+    a.s_first = v.s_first;
     a.n = v.n;
     a.k = v.k;
     a.T = v.T;
@@ -458,14 +476,8 @@ lx::ms::MainArgs<R> main_args(const View<R>& v, int rows) {
     a.sphi = v.sphi;
     a.cpsi = v.cpsi;
     a.spsi = v.spsi;
+    a.inv_t = v.inv_t;
     return a;
-}
-
-template <class R, int NG, int NX, bool BWD, bool SEQ = false>
-void launch_tileagg(const lx::ms::MainArgs<R>& a, cudaStream_t st) {
-    launch("lx_tileagg", st, [&] {
-        lx::ms::lx_tileagg<R, NG, NX, BWD, SEQ><<<a.T, lx::ms::kAggThreads, 0, st>>>(a);
-    });
 }
 
 template <class R, int NG, int NX, bool BWD, bool SEQ = false>
@@ -529,50 +541,75 @@ void launch_carry(const R* aggp, const R* aggq, R* cp, R* cq, const R* sl, const
     launch("lx_carry", st, [&] { lx_carry<R, NC, 2><<<dim3(rows, 2, NB), kCarryThreads, 0, st>>>(a); });
 }
 
+// sorted-payload row stride: 16-byte multiple so every row start is TMA-aligned
+size_t padded_ld(uint32_t m) { return ((size_t)m + 3) & ~size_t(3); }
+
 struct Scratch {
-    DBuf aggp, aggq, cp, cq, sl, sf;
+    DBuf aggp, aggq, cp, cq;
     Scratch(size_t slots, int rows, uint32_t T, size_t rs, cudaStream_t st)
-        : aggp(slots * rows * T * rs, st),
-          aggq(slots * rows * T * rs, st),
-          cp(slots * rows * T * rs, st),
-          cq(slots * rows * T * rs, st),
-          sl((size_t)T * rs, st),
-          sf((size_t)T * rs, st) {}
+        : aggp(slots * rows * T * rs, st), aggq(slots * rows * T * rs, st), cp(slots * rows * T * rs, st),
+          cq(slots * rows * T * rs, st) {}
 };
 
-// One merged pass: tile aggregates -> fp64 tile carries -> main kernel with
-// final outputs.  `a` already holds inputs, index arrays and output pointers.
-template <class R, int NG, int NX, bool BWD, bool SEQ = false>
-void run_merged(lx::ms::MainArgs<R>& a, const char* name, cudaStream_t st) {
-    constexpr int NC = NG + NX;
-    Scratch s(2 * NC, a.rows, a.T, sizeof(R), st);
-    a.aggp = s.aggp.as<R>();
-    a.aggq = s.aggq.as<R>();
-    a.s_last = s.sl.as<R>();
-    a.s_first = s.sf.as<R>();
-    a.cp = s.cp.as<R>();
-    a.cq = s.cq.as<R>();
-    launch_tileagg<R, NG, NX, BWD, SEQ>(a, st);
-    const unsigned gmask = BWD ? (1u << NG) - 1u : 0u;
-    const unsigned xmask = BWD ? ((1u << NX) - 1u) << NG : 0u;
-    launch_carry<R, NC>(s.aggp.as<R>(), s.aggq.as<R>(), s.cp.as<R>(), s.cq.as<R>(), s.sl.as<R>(), s.sf.as<R>(), a.T,
-                        a.rows, gmask, xmask, st);
-    launch_main<R, NG, NX, BWD, SEQ>(name, a, st);
+// Gather one payload side into sorted order (through the side's permutation
+// plan when it has one) and compute its tile aggregates in the same pass.
+template <class R, int NCH, bool SIDE_A, bool GFORM, bool STRICT>
+DBuf sorted_payload(const View<R>& v, int rows, const R* user, const Scratch& sc, int cbase, size_t& ld_out,
+                    cudaStream_t st, bool already_sorted = false) {
+    const uint32_t m = SIDE_A ? v.n : v.k;
+    const uint32_t* dst = SIDE_A ? v.dst_a : v.dst_b;
+    const uint32_t* pos = SIDE_A ? v.pos_a : v.pos_b;
+    const uint32_t* perm = SIDE_A ? v.pa : v.pb;
+    ld_out = padded_ld(m);
+    DBuf out((size_t)rows * ld_out * sizeof(R) + kTmaPad, st);
+    DBuf stg;
+    lx::ms::GatherAggArgs<R> g;
+    std::memset(&g, 0, sizeof(g));
+    g.desc = v.desc;
+    g.T = v.T;
+    g.rows = rows;
+    g.V = SIDE_A ? v.A : v.B;
+    g.out = out.as<R>();
+    g.ld_out = ld_out;
+    g.cph = SIDE_A ? v.cphi : v.cpsi;
+    g.sph = SIDE_A ? v.sphi : v.spsi;
+    g.aggp = sc.aggp.as<R>();
+    g.aggq = sc.aggq.as<R>();
+    g.cbase = cbase;
+    g.ld_src = m;
+    if (already_sorted) {
+        g.src = user;
+        g.idx = nullptr;
+    } else if (dst) {
+        stg = stage_gather<R>(user, m, dst, m, rows, st);
+        g.src = stg.as<R>();
+        g.idx = pos;
+    } else {
+        g.src = user;
+        g.idx = perm;
+    }
+    launch("lx_gather_agg", st, [&] {
+        lx::ms::lx_gather_agg<R, NCH, SIDE_A, GFORM, STRICT><<<v.T, lx::ms::kAggThreads, 0, st>>>(g);
+    });
+    return out;
+}
+
+template <class R, int NC>
+void scan_carries(const View<R>& v, const Scratch& sc, int rows, unsigned pm, unsigned qm, cudaStream_t st) {
+    launch_carry<R, NC>(sc.aggp.as<R>(), sc.aggq.as<R>(), sc.cp.as<R>(), sc.cq.as<R>(), v.s_last, v.s_first, v.T,
+                        rows, pm, qm, st);
 }
 
 template <class R, int NX>
 void apply_fwd(const View<R>& v, const R* X, int rows, R* Y, cudaStream_t st) {
     auto a = main_args(v, rows);
-    a.inv_t = v.inv_t;
-    DBuf xst, yst;
-    if (v.dst_b) {  // gather x through the cols plan
-        xst = stage_gather<R>(X, v.k, v.dst_b, v.k, rows, st);
-        a.X = xst.as<R>();
-        a.perm_b = v.pos_b;
-    } else {
-        a.X = X;
-    }
-    a.ldx = v.k;
+    Scratch sc(2 * NX, rows, v.T, sizeof(R), st);
+    DBuf xs = sorted_payload<R, NX, false, false, false>(v, rows, X, sc, 0, a.ldxs, st);
+    a.Xs = xs.as<R>();
+    scan_carries<R, NX>(v, sc, rows, 0u, 0u, st);
+    a.cp = sc.cp.as<R>();
+    a.cq = sc.cq.as<R>();
+    DBuf yst;
     if (v.dst_a) {  // write bucket-staged, then scatter through the rows plan
         yst = DBuf((size_t)rows * v.n * sizeof(R), st);
         a.y = yst.as<R>();
@@ -581,8 +618,8 @@ void apply_fwd(const View<R>& v, const R* X, int rows, R* Y, cudaStream_t st) {
         a.y = Y;
     }
     a.ldy = v.n;
-    run_merged<R, 0, NX, false>(a, NX == 2 ? "lx_main_fwd_phased" : "lx_main_fwd", st);
-    xst.release();
+    launch_main<R, 0, NX, false>(NX == 2 ? "lx_main_fwd_phased" : "lx_main_fwd", a, st);
+    xs.release();
     if (v.dst_a)
         stage_scatter<R>(v.dst_a, v.n, yst.as<R>(), Y, v.n, rows, nullptr, nullptr, nullptr, nullptr, st);
 }
@@ -590,16 +627,13 @@ void apply_fwd(const View<R>& v, const R* X, int rows, R* Y, cudaStream_t st) {
 template <class R>
 void apply_trn(const View<R>& v, const R* G, int rows, R* Y, cudaStream_t st) {
     auto a = main_args(v, rows);
-    a.inv_t = v.inv_t;
-    DBuf gst, yst;
-    if (v.dst_a) {
-        gst = stage_gather<R>(G, v.n, v.dst_a, v.n, rows, st);
-        a.G = gst.as<R>();
-        a.perm_a = v.pos_a;
-    } else {
-        a.G = G;
-    }
-    a.ldg = v.n;
+    Scratch sc(2, rows, v.T, sizeof(R), st);
+    DBuf gs = sorted_payload<R, 1, true, true, false>(v, rows, G, sc, 0, a.ldgs, st);
+    a.Gs = gs.as<R>();
+    scan_carries<R, 1>(v, sc, rows, 0u, 0u, st);
+    a.cp = sc.cp.as<R>();
+    a.cq = sc.cq.as<R>();
+    DBuf yst;
     if (v.dst_b) {
         yst = DBuf((size_t)rows * v.k * sizeof(R), st);
         a.y = yst.as<R>();
@@ -608,8 +642,8 @@ void apply_trn(const View<R>& v, const R* G, int rows, R* Y, cudaStream_t st) {
         a.y = Y;
     }
     a.ldy = v.k;
-    run_merged<R, 1, 0, false>(a, "lx_main_trn", st);
-    gst.release();
+    launch_main<R, 1, 0, false>("lx_main_trn", a, st);
+    gs.release();
     if (v.dst_b)
         stage_scatter<R>(v.dst_b, v.k, yst.as<R>(), Y, v.k, rows, nullptr, nullptr, nullptr, nullptr, st);
 }
@@ -617,45 +651,46 @@ void apply_trn(const View<R>& v, const R* G, int rows, R* Y, cudaStream_t st) {
 template <class R, int NCH>
 void backward_impl(const View<R>& v, const R* X, const R* G, int rows, R* xbar, R* abar, R* bbar, R* phibar,
                    R* psibar, cudaStream_t st) {
+    constexpr int NC = 2 * NCH;
     const size_t rs = sizeof(R);
     auto a = main_args(v, rows);
-    a.inv_t = v.inv_t;
-    DBuf xst, gst, sxb, sbb, sqb, sab, spb;
+    Scratch sc(2 * NC, rows, v.T, rs, st);
+    DBuf gs = sorted_payload<R, NCH, true, true, true>(v, rows, G, sc, 0, a.ldgs, st);
+    DBuf xs = sorted_payload<R, NCH, false, false, true>(v, rows, X, sc, NCH, a.ldxs, st);
+    a.Gs = gs.as<R>();
+    a.Xs = xs.as<R>();
+    const unsigned gmask = (1u << NCH) - 1u;
+    scan_carries<R, NC>(v, sc, rows, gmask, gmask << NCH, st);
+    a.cp = sc.cp.as<R>();
+    a.cq = sc.cq.as<R>();
+    DBuf sxb, sbb, sqb, sab, spb;  // bucket-staged outputs
     if (v.dst_b) {
-        xst = stage_gather<R>(X, v.k, v.dst_b, v.k, rows, st);
-        a.X = xst.as<R>();
-        a.perm_b = v.pos_b;
         sxb = DBuf((size_t)rows * v.k * rs, st);
         sbb = DBuf((size_t)v.k * rs, st);
         if (NCH == 2) sqb = DBuf((size_t)v.k * rs, st);
         a.xbar = sxb.as<R>();
         a.bbar = sbb.as<R>();
         a.psibar = sqb.as<R>();
+        a.perm_b = v.pos_b;
     } else {
-        a.X = X;
         a.xbar = xbar;
         a.bbar = bbar;
         a.psibar = psibar;
     }
     if (v.dst_a) {
-        gst = stage_gather<R>(G, v.n, v.dst_a, v.n, rows, st);
-        a.G = gst.as<R>();
-        a.perm_a = v.pos_a;
         sab = DBuf((size_t)v.n * rs, st);
         if (NCH == 2) spb = DBuf((size_t)v.n * rs, st);
         a.abar = sab.as<R>();
         a.phibar = spb.as<R>();
+        a.perm_a = v.pos_a;
     } else {
-        a.G = G;
         a.abar = abar;
         a.phibar = phibar;
     }
-    a.ldx = v.k;
-    a.ldg = v.n;
     a.ldxb = v.k;
-    run_merged<R, NCH, NCH, true>(a, NCH == 2 ? "lx_main_bwd_phased" : "lx_main_bwd", st);
-    xst.release();
-    gst.release();
+    launch_main<R, NCH, NCH, true>(NCH == 2 ? "lx_main_bwd_phased" : "lx_main_bwd", a, st);
+    gs.release();
+    xs.release();
     if (v.dst_b)
         stage_scatter<R>(v.dst_b, v.k, sxb.as<R>(), xbar, v.k, rows, sbb.as<R>(), bbar,
                          NCH == 2 ? sqb.as<R>() : nullptr, psibar, st);
@@ -825,24 +860,36 @@ void do_scan(const R* sorted, uint32_t m, const R* payload, R* pre, R* suf, cuda
     DBuf vals((size_t)m * sizeof(R) + kTmaPad, st), pay((size_t)m * sizeof(R), st);
     ck(cudaMemcpyAsync(vals.p, sorted, (size_t)m * sizeof(R), cudaMemcpyHostToDevice, st), "H2D");
     ck(cudaMemcpyAsync(pay.p, payload, (size_t)m * sizeof(R), cudaMemcpyHostToDevice, st), "H2D");
-    DBuf part((size_t)(T + 1) * 4, st);
+    DBuf part((size_t)(T + 1) * 4, st), desc((size_t)(T + 1) * sizeof(TileDesc<R>), st);
+    DBuf sfirst((size_t)T * sizeof(R), st), slast((size_t)T * sizeof(R), st);
     launch("lx_seq_partition", st, [&] {
         lx_seq_partition<<<(T + 256) / 256, 256, 0, st>>>(m, part.as<uint32_t>(), T);
     });
+    launch("lx_tiledesc", st, [&] {
+        lx_tiledesc<R><<<(T + 1 + 255) / 256, 256, 0, st>>>(vals.as<R>(), m, vals.as<R>(), 0, part.as<uint32_t>(), T,
+                                                             desc.as<TileDesc<R>>(), sfirst.as<R>(), slast.as<R>());
+    });
+    View<R> v;
+    std::memset(&v, 0, sizeof(v));
+    v.A = vals.as<R>();
+    v.n = m;
+    v.k = 0;
+    v.part = part.as<uint32_t>();
+    v.desc = desc.as<TileDesc<R>>();
+    v.s_first = sfirst.as<R>();
+    v.s_last = slast.as<R>();
+    v.T = T;
     DBuf dpre((size_t)m * sizeof(R), st), dsuf((size_t)m * sizeof(R), st);
-    MainArgs<R> a;
-    std::memset(&a, 0, sizeof(a));
-    a.A = vals.as<R>();
-    a.part = part.as<uint32_t>();
-    a.n = m;
-    a.k = 0;
-    a.T = T;
-    a.rows = 1;
-    a.X = pay.as<R>();
-    a.ldx = m;
+    auto a = main_args(v, 1);
+    Scratch sc(2, 1, T, sizeof(R), st);
+    DBuf xs = sorted_payload<R, 1, true, false, false>(v, 1, pay.as<R>(), sc, 0, a.ldxs, st, true);
+    a.Xs = xs.as<R>();
+    scan_carries<R, 1>(v, sc, 1, 0u, 0u, st);
+    a.cp = sc.cp.as<R>();
+    a.cq = sc.cq.as<R>();
     a.pre = dpre.as<R>();
     a.suf = dsuf.as<R>();
-    run_merged<R, 0, 1, false, true>(a, "lx_main_seq", st);
+    launch_main<R, 0, 1, false, true>("lx_main_seq", a, st);
     if (pre) ck(cudaMemcpyAsync(pre, dpre.p, (size_t)m * sizeof(R), cudaMemcpyDeviceToHost, st), "D2H");
     if (suf) ck(cudaMemcpyAsync(suf, dsuf.p, (size_t)m * sizeof(R), cudaMemcpyDeviceToHost, st), "D2H");
     ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");

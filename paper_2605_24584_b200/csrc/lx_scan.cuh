@@ -77,6 +77,51 @@ __global__ void lx_partition(const R* __restrict__ A, uint32_t n, const R* __res
     part[t] = (uint32_t)merge_path<AFIRST, R, unsigned long long>(A, n, B, k, diag);
 }
 
+// Per-tile descriptor, built once per plan orientation: the tile's row/col
+// offsets and the anchors of its first and last merged element (the carries'
+// reference points).  desc[T] = {n, k} is the sentinel.
+template <class R>
+struct TileDesc {
+    uint32_t a0, b0;
+    R s_first, s_last;
+};
+
+template <class R>
+__global__ void lx_tiledesc(const R* __restrict__ A, uint32_t n, const R* __restrict__ B, uint32_t k,
+                            const uint32_t* __restrict__ part, uint32_t T, TileDesc<R>* __restrict__ desc,
+                            R* __restrict__ s_first, R* __restrict__ s_last) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t > T) return;
+    TileDesc<R> d;
+    if (t == T) {
+        d.a0 = n;
+        d.b0 = k;
+        d.s_first = d.s_last = R(0);
+        desc[t] = d;
+        return;
+    }
+    const uint32_t a0 = part[t], a1 = part[t + 1];
+    const unsigned long long d0 = (unsigned long long)t * kTile;
+    const unsigned long long total = (unsigned long long)n + k;
+    const unsigned long long d1 = d0 + kTile < total ? d0 + kTile : total;
+    const uint32_t b0 = (uint32_t)(d0 - a0), b1 = (uint32_t)(d1 - a1);
+    d.a0 = a0;
+    d.b0 = b0;
+    if (a1 == a0) {
+        d.s_first = B[b0];
+        d.s_last = B[b1 - 1];
+    } else if (b1 == b0) {
+        d.s_first = A[a0];
+        d.s_last = A[a1 - 1];
+    } else {
+        d.s_first = A[a0] < B[b0] ? A[a0] : B[b0];
+        d.s_last = A[a1 - 1] > B[b1 - 1] ? A[a1 - 1] : B[b1 - 1];
+    }
+    desc[t] = d;
+    s_first[t] = d.s_first;
+    s_last[t] = d.s_last;
+}
+
 // ---------------------------------------------------------------------------
 // co-ranks (accessor path): AFIRST gives J<[i] and R<=[j]; !AFIRST gives
 // J<=[i] and R<[j]  (operator.hpp:110-120 are the two tie-inclusive ones).
@@ -129,8 +174,14 @@ struct MainArgs {
     const R* B;
     const uint32_t* perm_b;
     const uint32_t* part;  // T+1 row offsets of the merged tiles
+    const TileDesc<R>* desc;  // T+1 tile descriptors
     uint32_t n, k, T;
     int rows;
+    // payloads in SORTED order (lx_gather_agg output), rows x ld (ld % (16/sizeof(R)) == 0)
+    const R* Gs;
+    size_t ldgs;
+    const R* Xs;
+    size_t ldxs;
     // payloads are read as X[r*ldx + perm_b[j]] / G[r*ldg + perm_a[i]]: either
     // the caller's arrays with the true permutations, or (large sides) the
     // bucket-staged copies with the plan's pos[] tables (lx_perm_stage_gather)
@@ -142,10 +193,8 @@ struct MainArgs {
     const R* spsi;
     const R* cphi;
     const R* sphi;
-    R* aggp;    // [slot][rows][T] tile aggregates (lx_tileagg), slot = 2*c + strict
-    R* aggq;
-    R* s_last;  // [T] anchor of each tile's last merged element (lx_tileagg)
-    R* s_first; // [T] anchor of each tile's first merged element
+    const R* s_last;   // [T] anchor of each tile's last merged element
+    const R* s_first;  // [T] anchor of each tile's first merged element
     const R* cp;  // inclusive tile carries (lx_carry), [slot][rows][T]
     const R* cq;
     R inv_t;
@@ -177,7 +226,8 @@ template <class R, int NG, int NX>
 struct MainSmem {
     static constexpr int NC = NG + NX;
     static constexpr int kPad = 16 / sizeof(R);  // TMA bulk copies start 16-byte aligned
-    unsigned long long bar;
+    unsigned long long bar;   // anchors
+    unsigned long long barp;  // payloads (phase = row & 1)
     R wsl[kWarps];  // warp last anchors
     R wsf[kWarps];  // warp first anchors
     R pv[NC][kWarps], pw[NC][kWarps];    // warp prefix totals (inclusive, strict)
@@ -186,8 +236,8 @@ struct MainSmem {
     R xqv[NC][kWarps], xqw[NC][kWarps];  // warp exclusive suffix
     alignas(16) R sA[kTile + 2 * kPad];  // tile rows (TMA destination)
     alignas(16) R sB[kTile + 2 * kPad];  // tile cols
-    R payA[NG > 0 ? kTile : 1];          // gathered g of the tile rows (cp.async)
-    R payB[NX > 0 ? kTile : 1];          // gathered x of the tile cols
+    alignas(16) R payA[kTile + 2 * kPad];  // g of the tile rows (TMA, sorted order)
+    alignas(16) R payB[kTile + 2 * kPad];  // x of the tile cols
 };
 
 // x_bar at one column element (shared by transpose and VJP so both produce
@@ -197,47 +247,15 @@ __device__ __forceinline__ R xbar_value(R w, R eL, R cpv, R eR, R cqv) {
     return xfma(eR, cqv, xfma(eL, cpv, w));
 }
 
-// Issue the async gathers of one row's payloads into shared memory.
-template <class R, int NG, int NX, bool SEQ>
-__device__ __forceinline__ void issue_payload(const MainArgs<R>& p, MainSmem<R, NG, NX>& sm, int r, uint32_t a0,
-                                              int na, uint32_t b0, int nb) {
-    if constexpr (SEQ) {
-        for (int i = threadIdx.x; i < na; i += kThreads) {
-            if constexpr (sizeof(R) == 4)
-                cp_async4(&sm.payB[i], &p.X[(size_t)r * p.ldx + a0 + i]);
-            else
-                cp_async8(&sm.payB[i], &p.X[(size_t)r * p.ldx + a0 + i]);
-        }
-        return;
-    }
-    if constexpr (NG > 0) {
-        for (int i = threadIdx.x; i < na; i += kThreads) {
-            const uint32_t u = p.perm_a[a0 + i];
-            if constexpr (sizeof(R) == 4)
-                cp_async4(&sm.payA[i], &p.G[(size_t)r * p.ldg + u]);
-            else
-                cp_async8(&sm.payA[i], &p.G[(size_t)r * p.ldg + u]);
-        }
-    }
-    if constexpr (NX > 0) {
-        for (int j = threadIdx.x; j < nb; j += kThreads) {
-            const uint32_t u = p.perm_b[b0 + j];
-            if constexpr (sizeof(R) == 4)
-                cp_async4(&sm.payB[j], &p.X[(size_t)r * p.ldx + u]);
-            else
-                cp_async8(&sm.payB[j], &p.X[(size_t)r * p.ldx + u]);
-        }
-    }
-}
-
 // SEQ: single sorted sequence (k = 0, part[t] = t*kTile): every element is a
 // "row" carrying its own payload X[r][i] (sorted order) and receiving both the
 // inclusive prefix (wa[0]) and inclusive suffix (wa2[0]) -- the free functions
 // prefix_decay_scan / suffix_decay_scan of scan.hpp:50-73.
 //
-// Per tile: the two anchor ranges arrive by TMA bulk copy (cp.async.bulk +
-// mbarrier) while the payload gathers are issued as cp.async into shared
-// memory; the merge runs as soon as the anchors land, overlapping the gathers.
+// Per tile: the tile descriptor gives the row/col ranges; the anchor ranges
+// and the row's payload ranges (already gathered into sorted order by
+// lx_gather_agg) arrive by TMA bulk copy (cp.async.bulk + mbarrier); the merge
+// runs as soon as the anchors land, overlapping the payload transfer.
 template <class R, int NG, int NX, bool BWD, bool SEQ = false>
 __global__ void __launch_bounds__(kThreads, 2) lx_main(MainArgs<R> p) {
     using C = Ch<NG, NX, BWD>;
@@ -249,20 +267,33 @@ __global__ void __launch_bounds__(kThreads, 2) lx_main(MainArgs<R> p) {
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t t = blockIdx.x;
-    const uint32_t a0 = p.part[t], a1 = p.part[t + 1];
-    const unsigned long long d0 = (unsigned long long)t * kTile;
-    const unsigned long long total = (unsigned long long)p.n + p.k;
-    const unsigned long long d1 = d0 + kTile < total ? d0 + kTile : total;
-    const uint32_t b0 = (uint32_t)(d0 - a0), b1 = (uint32_t)(d1 - a1);
+    const TileDesc<R> dt = p.desc[t], dn = p.desc[t + 1];
+    const uint32_t a0 = dt.a0, a1 = dn.a0, b0 = dt.b0, b1 = dn.b0;
     const int na = (int)(a1 - a0), nb = (int)(b1 - b0), len = na + nb;
+    // neighbouring tiles' edge anchors: the carries' reference points
+    const bool hl = t > 0, hr = t + 1 < p.T;
+    const R SL = hl ? p.s_last[t - 1] : R(0);
+    const R SR = hr ? dn.s_first : R(0);
+    const R s_end = dt.s_last;  // anchor of the tile's last merged element
 
-    // ---- prologue: TMA the anchors, cp.async the row-0 payloads ----
+    // ---- prologue: TMA bulk copies of the anchor ranges and row-0 payloads ----
     const uint32_t a0al = a0 & ~uint32_t(kPad - 1), b0al = b0 & ~uint32_t(kPad - 1);
     const int offA = (int)(a0 - a0al), offB = (int)(b0 - b0al);
     const uint32_t bytesA = na ? (uint32_t)(((offA + na + kPad - 1) / kPad) * 16) : 0u;
     const uint32_t bytesB = nb ? (uint32_t)(((offB + nb + kPad - 1) / kPad) * 16) : 0u;
+    constexpr bool PAY_A = SEQ || NG > 0;
+    constexpr bool PAY_B = !SEQ && NX > 0;
+    const R* srcA = SEQ ? p.Xs : p.Gs;
+    const size_t ldA = SEQ ? p.ldxs : p.ldgs;
+    auto issue_payload = [&](int r) {  // one thread
+        const uint32_t bytes = (PAY_A ? bytesA : 0u) + (PAY_B ? bytesB : 0u);
+        mbar_expect_tx(&sm.barp, bytes);
+        if (PAY_A && bytesA) bulk_g2s(sm.payA, srcA + (size_t)r * ldA + a0al, bytesA, &sm.barp);
+        if (PAY_B && bytesB) bulk_g2s(sm.payB, p.Xs + (size_t)r * p.ldxs + b0al, bytesB, &sm.barp);
+    };
     if (tid == 0) {
         mbar_init(&sm.bar, 1);
+        mbar_init(&sm.barp, 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -270,19 +301,13 @@ __global__ void __launch_bounds__(kThreads, 2) lx_main(MainArgs<R> p) {
         mbar_expect_tx(&sm.bar, bytesA + bytesB);
         if (bytesA) bulk_g2s(sm.sA, p.A + a0al, bytesA, &sm.bar);
         if (bytesB) bulk_g2s(sm.sB, p.B + b0al, bytesB, &sm.bar);
+        issue_payload(0);
     }
-    issue_payload<R, NG, NX, SEQ>(p, sm, 0, a0, na, b0, nb);
     mbar_wait(&sm.bar, 0);
     const R* sA = sm.sA + offA;
     const R* sB = sm.sB + offB;
-    // anchor of the tile's last merged element (pads trailing empty slots)
-    R s_end;
-    if (na == 0)
-        s_end = sB[nb - 1];
-    else if (nb == 0)
-        s_end = sA[na - 1];
-    else
-        s_end = sA[na - 1] > sB[nb - 1] ? sA[na - 1] : sB[nb - 1];
+    const R* pA = sm.payA + offA;
+    const R* pB = sm.payB + offB;
 
     // ---- per-thread merge: anchors, kind, local index ----
     R s[kItems];
@@ -376,10 +401,6 @@ __global__ void __launch_bounds__(kThreads, 2) lx_main(MainArgs<R> p) {
     const R* cpsi = p.cpsi;
     const R* spsi = p.spsi;
     const size_t T = p.T;
-    // neighbouring tiles' edge anchors: the carries' reference points
-    const bool hl = t > 0, hr = t + 1 < p.T;
-    const R SL = hl ? p.s_last[t - 1] : R(0);
-    const R SR = hr ? p.s_first[t + 1] : R(0);
     R acc1[kItems], acc2[kItems];  // backward: a_bar/b_bar and phi_bar/psi_bar over rows
 #pragma unroll
     for (int q = 0; q < kItems; ++q) acc1[q] = acc2[q] = R(0);
@@ -387,10 +408,9 @@ __global__ void __launch_bounds__(kThreads, 2) lx_main(MainArgs<R> p) {
     for (int r = 0; r < p.rows; ++r) {
         if (r > 0) {
             __syncthreads();  // previous row's payload reads are done
-            issue_payload<R, NG, NX, SEQ>(p, sm, r, a0, na, b0, nb);
+            if (tid == 0) issue_payload(r);
         }
-        cp_async_wait_all();
-        __syncthreads();
+        mbar_wait(&sm.barp, (uint32_t)(r & 1));
         // ---- payloads (from shared memory) ----
         R pay[NC][kItems];
 #pragma unroll
@@ -402,9 +422,9 @@ __global__ void __launch_bounds__(kThreads, 2) lx_main(MainArgs<R> p) {
             const uint32_t li = cd & 0x3fffffffu;
             if (cd & 0x80000000u) {
                 if constexpr (SEQ) {
-                    pay[0][q] = sm.payB[li];
+                    pay[0][q] = pA[li];
                 } else if constexpr (NG > 0) {
-                    const R g = sm.payA[li];
+                    const R g = pA[li];
                     if constexpr (NG == 2) {
                         pay[0][q] = xmul(cphi[a0 + li], g);
                         pay[1][q] = xmul(sphi[a0 + li], g);
@@ -414,7 +434,7 @@ __global__ void __launch_bounds__(kThreads, 2) lx_main(MainArgs<R> p) {
                 }
             } else {
                 if constexpr (NX > 0) {
-                    const R x = sm.payB[li];
+                    const R x = pB[li];
                     if constexpr (NX == 2) {
                         pay[NG][q] = xmul(cpsi[b0 + li], x);
                         pay[NG + 1][q] = xmul(spsi[b0 + li], x);
@@ -613,7 +633,7 @@ __global__ void __launch_bounds__(kThreads, 2) lx_main(MainArgs<R> p) {
                     if constexpr (NX == 2) out = xadd(xmul(cphi[i], val[0]), xmul(sphi[i], val[1]));
                     p.y[(size_t)r * p.ldy + p.perm_a[i]] = out;
                 } else if constexpr (BWD) {
-                    const R g = sm.payA[li];
+                    const R g = pA[li];
                     R m0 = R(1), m1 = R(0);
                     if constexpr (NG == 2) {
                         m0 = cphi[i];
@@ -645,7 +665,7 @@ __global__ void __launch_bounds__(kThreads, 2) lx_main(MainArgs<R> p) {
                     if constexpr (!BWD) {
                         p.y[(size_t)r * p.ldy + p.perm_b[j]] = xb[0];
                     } else {
-                        const R x = sm.payB[li];
+                        const R x = pB[li];
                         R m0 = R(1), m1 = R(0);
                         if constexpr (NG == 2) {
                             m0 = cpsi[j];
@@ -692,98 +712,107 @@ __global__ void __launch_bounds__(kThreads, 2) lx_main(MainArgs<R> p) {
 }
 
 // ---------------------------------------------------------------------------
-// tile aggregates (pre-pass): for every merge tile and row, per channel
+// gather + tile aggregates (one pass per payload side).  For every merge tile
+// and row it (1) gathers the side's payload into SORTED order (written
+// contiguous, so the main kernel loads it with TMA), and (2) sums per channel
 //   prefix  sum_e exp(s_e - S_last) pay_e     (+ strict: only s_e < S_last)
 //   suffix  sum_e exp(S_first - s_e) pay_e    (+ strict: only s_e > S_first)
-// summed directly (every term one exp of an anchor difference) in a fixed
-// order (thread-strided partials, then a fixed tree), so they are
-// deterministic and independent of the batch size.  Only the elements that
-// carry payload contribute: rows for g channels, cols for x channels.
+// directly (every term one exp of an anchor difference) in a fixed order
+// (thread-strided partials, then a fixed tree): deterministic and independent
+// of the batch size.  Rows carry the g channels (prefix-strict in the VJP),
+// cols the x channels (suffix-strict in the VJP).
 // ---------------------------------------------------------------------------
 constexpr int kAggThreads = 256;
 
-template <class R, int NG, int NX, bool BWD, bool SEQ = false>
-__global__ void __launch_bounds__(kAggThreads) lx_tileagg(MainArgs<R> p) {
-    using C = Ch<NG, NX, BWD>;
-    constexpr int NC = C::NC;
+template <class R>
+struct GatherAggArgs {
+    const TileDesc<R>* desc;
+    uint32_t T;
+    int rows;
+    const R* V;           // this side's sorted anchors
+    const uint32_t* idx;  // sorted -> source index (perm or plan pos); null: source already sorted
+    const R* src;         // payload source, rows x ld_src
+    size_t ld_src;
+    R* out;               // payload in sorted order, rows x ld_out
+    size_t ld_out;
+    const R* cph;         // sorted-order phases (2 channels)
+    const R* sph;
+    R* aggp;              // [slot][rows][T]
+    R* aggq;
+    int cbase;            // first channel index of this side
+};
+
+// SIDE_A: the tile range is the rows range; GFORM: g-channel formulas (prefix
+// strict) vs x-channel formulas (suffix strict).
+template <class R, int NCH, bool SIDE_A, bool GFORM, bool STRICT>
+__global__ void __launch_bounds__(kAggThreads) lx_gather_agg(GatherAggArgs<R> g) {
     constexpr int NW = kAggThreads / 32;
     const uint32_t t = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t a0 = p.part[t], a1 = p.part[t + 1];
-    const unsigned long long d0 = (unsigned long long)t * kTile;
-    const unsigned long long total = (unsigned long long)p.n + p.k;
-    const unsigned long long d1 = d0 + kTile < total ? d0 + kTile : total;
-    const uint32_t b0 = (uint32_t)(d0 - a0), b1 = (uint32_t)(d1 - a1);
-    const int na = (int)(a1 - a0), nb = (int)(b1 - b0);
-    R S_last, S_first;
-    if (na == 0) {
-        S_last = p.B[b1 - 1];
-        S_first = p.B[b0];
-    } else if (nb == 0) {
-        S_last = p.A[a1 - 1];
-        S_first = p.A[a0];
-    } else {
-        const R al = p.A[a1 - 1], bl = p.B[b1 - 1], af = p.A[a0], bf = p.B[b0];
-        S_last = al > bl ? al : bl;
-        S_first = af < bf ? af : bf;
-    }
-    __shared__ R red[4 * NC][NW];
-    const size_t T = p.T;
-    for (int r = 0; r < p.rows; ++r) {
-        R pi[NC], ps[NC], qi[NC], qs[NC];
+    const TileDesc<R> dt = g.desc[t];
+    const TileDesc<R> dn = g.desc[t + 1];
+    const uint32_t s0 = SIDE_A ? dt.a0 : dt.b0;
+    const uint32_t s1 = SIDE_A ? dn.a0 : dn.b0;
+    const int ns = (int)(s1 - s0);
+    const R S_first = dt.s_first, S_last = dt.s_last;
+    const uint32_t* __restrict__ idx = g.idx;
+    const R* __restrict__ src = g.src;
+    const R* __restrict__ V = g.V;
+    R* __restrict__ out = g.out;
+    __shared__ R red[4 * NCH][NW];
+    const size_t T = g.T;
+    for (int r = 0; r < g.rows; ++r) {
+        R pi[NCH], ps[NCH], qi[NCH], qs[NCH];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) pi[c] = ps[c] = qi[c] = qs[c] = R(0);
-        if constexpr (NG > 0 || SEQ) {
-            for (int i = tid; i < na; i += kAggThreads) {
-                const R s = p.A[a0 + i];
-                const R e1 = xexp(xsub(s, S_last)), e2 = xexp(xsub(S_first, s));
-                if constexpr (SEQ) {
-                    const R x = p.X[(size_t)r * p.ldx + a0 + i];
-                    pi[0] = xfma(e1, x, pi[0]);
-                    qi[0] = xfma(e2, x, qi[0]);
-                } else {
-                    const R g = p.G[(size_t)r * p.ldg + p.perm_a[a0 + i]];
-                    R pay[NG > 0 ? NG : 1];
-                    if constexpr (NG == 2) {
-                        pay[0] = xmul(p.cphi[a0 + i], g);
-                        pay[1] = xmul(p.sphi[a0 + i], g);
-                    } else {
-                        pay[0] = g;
-                    }
+        for (int c = 0; c < NCH; ++c) pi[c] = ps[c] = qi[c] = qs[c] = R(0);
+        // all loads of the thread's (up to) kGI elements are issued before use
+        constexpr int kGI = kTile / kAggThreads;
+        uint32_t ix[kGI];
+        R v[kGI], sv[kGI];
 #pragma unroll
-                    for (int c = 0; c < NG; ++c) {
-                        const R pe = xmul(e1, pay[c]);
-                        pi[c] = xadd(pi[c], pe);
-                        if (C::pst(c) && s < S_last) ps[c] = xadd(ps[c], pe);
-                        qi[c] = xfma(e2, pay[c], qi[c]);
-                    }
-                }
-            }
+        for (int q = 0; q < kGI; ++q) {
+            const int i = tid + q * kAggThreads;
+            const uint32_t e = s0 + (uint32_t)i;
+            ix[q] = i < ns ? (idx ? idx[e] : e) : 0u;
+            sv[q] = i < ns ? V[e] : R(0);
         }
-        if constexpr (NX > 0 && !SEQ) {
-            for (int j = tid; j < nb; j += kAggThreads) {
-                const R s = p.B[b0 + j];
-                const R e1 = xexp(xsub(s, S_last)), e2 = xexp(xsub(S_first, s));
-                const R x = p.X[(size_t)r * p.ldx + p.perm_b[b0 + j]];
-                R pay[NX];
-                if constexpr (NX == 2) {
-                    pay[0] = xmul(p.cpsi[b0 + j], x);
-                    pay[1] = xmul(p.spsi[b0 + j], x);
-                } else {
-                    pay[0] = x;
-                }
 #pragma unroll
-                for (int c = NG; c < NC; ++c) {
-                    pi[c] = xfma(e1, pay[c - NG], pi[c]);
-                    const R qe = xmul(e2, pay[c - NG]);
+        for (int q = 0; q < kGI; ++q) {
+            const int i = tid + q * kAggThreads;
+            v[q] = i < ns ? src[(size_t)r * g.ld_src + ix[q]] : R(0);
+        }
+#pragma unroll
+        for (int q = 0; q < kGI; ++q) {
+            const int i = tid + q * kAggThreads;
+            if (i >= ns) continue;
+            const uint32_t e = s0 + (uint32_t)i;
+            out[(size_t)r * g.ld_out + e] = v[q];
+            const R s = sv[q];
+            const R e1 = xexp(xsub(s, S_last)), e2 = xexp(xsub(S_first, s));
+            R pay[NCH];
+            if constexpr (NCH == 2) {
+                pay[0] = xmul(g.cph[e], v[q]);
+                pay[1] = xmul(g.sph[e], v[q]);
+            } else {
+                pay[0] = v[q];
+            }
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) {
+                if constexpr (GFORM) {
+                    const R pe = xmul(e1, pay[c]);
+                    pi[c] = xadd(pi[c], pe);
+                    if (STRICT && s < S_last) ps[c] = xadd(ps[c], pe);
+                    qi[c] = xfma(e2, pay[c], qi[c]);
+                } else {
+                    pi[c] = xfma(e1, pay[c], pi[c]);
+                    const R qe = xmul(e2, pay[c]);
                     qi[c] = xadd(qi[c], qe);
-                    if (C::qst(c) && S_first < s) qs[c] = xadd(qs[c], qe);
+                    if (STRICT && S_first < s) qs[c] = xadd(qs[c], qe);
                 }
             }
         }
-        // fixed-order block reduction
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
+        for (int c = 0; c < NCH; ++c) {
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) {
                 pi[c] = xadd(pi[c], __shfl_xor_sync(FULL, pi[c], off));
@@ -799,21 +828,17 @@ __global__ void __launch_bounds__(kAggThreads) lx_tileagg(MainArgs<R> p) {
             }
         }
         __syncthreads();
-        if (tid < 4 * NC) {
+        if (tid < 4 * NCH) {
             R v = red[tid][0];
 #pragma unroll
             for (int w = 1; w < NW; ++w) v = xadd(v, red[tid][w]);
-            const int c = tid >> 2, kind = tid & 3;
-            if (kind == 0) p.aggp[((size_t)(2 * c) * p.rows + r) * T + t] = v;
-            if (kind == 1 && C::pst(c)) p.aggp[((size_t)(2 * c + 1) * p.rows + r) * T + t] = v;
-            if (kind == 2) p.aggq[((size_t)(2 * c) * p.rows + r) * T + t] = v;
-            if (kind == 3 && C::qst(c)) p.aggq[((size_t)(2 * c + 1) * p.rows + r) * T + t] = v;
+            const int c = g.cbase + (tid >> 2), kind = tid & 3;
+            if (kind == 0) g.aggp[((size_t)(2 * c) * g.rows + r) * T + t] = v;
+            if (kind == 1 && STRICT && GFORM) g.aggp[((size_t)(2 * c + 1) * g.rows + r) * T + t] = v;
+            if (kind == 2) g.aggq[((size_t)(2 * c) * g.rows + r) * T + t] = v;
+            if (kind == 3 && STRICT && !GFORM) g.aggq[((size_t)(2 * c + 1) * g.rows + r) * T + t] = v;
         }
         __syncthreads();
-    }
-    if (tid == 0) {
-        p.s_last[t] = S_last;
-        p.s_first[t] = S_first;
     }
 }
 
