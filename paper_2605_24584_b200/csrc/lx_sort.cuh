@@ -112,13 +112,16 @@ __global__ void __launch_bounds__(kRadix) lx_sort_bases(const uint32_t* __restri
 template <class R>
 struct PassSmem {
     using K = typename Traits<R>::Key;
+    unsigned long long bar;
     uint32_t whist[kWarps][kRadix];
     uint32_t dstart[kRadix];
     uint32_t gbase[kRadix];
     uint32_t scan[kWarps];
     uint32_t tile;
-    K keys[kTile];
-    uint32_t vals[kTile];
+    alignas(16) K ik[kTile];         // input tile keys (raw values in the first pass)
+    alignas(16) uint32_t iv[kTile];  // input payload
+    alignas(16) K ok[kTile];         // digit-ordered staging for coalesced writes
+    alignas(16) uint32_t ov[kTile];
 };
 
 // One digit pass.  FIRST reads the raw anchors and builds keys+payload on the
@@ -129,6 +132,10 @@ struct PassSmem {
 // the bucket bases are d << shift (a permutation fills every bucket exactly).
 // That is the B200 form of the reference's cache-blocked ScatterPlan
 // (operator.hpp:26-60,130-136).
+//
+// The tile (keys, payload) arrives in shared memory by TMA bulk copy; keys are
+// then read from shared memory where needed, so no thread holds its 16 keys
+// across the load latency (register pressure, hence occupancy).
 template <class R, bool FIRST, bool LAST, bool SPLAN = false>
 __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict__ in_keys,
                                                         const uint32_t* __restrict__ in_vals,
@@ -138,52 +145,60 @@ __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict_
                                                         unsigned long long* __restrict__ lookback,
                                                         uint32_t* __restrict__ tile_counter, uint32_t epoch) {
     using K = typename Traits<R>::Key;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     PassSmem<R>& sm = *reinterpret_cast<PassSmem<R>*>(smem_raw);
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int lane = tid & 31;
+    constexpr bool HAS_VALS = !FIRST && !SPLAN;
 
-    if (tid == 0) sm.tile = atomicAdd(tile_counter, 1u);
+    if (tid == 0) {
+        sm.tile = atomicAdd(tile_counter, 1u);
+        mbar_init(&sm.bar, 1);
+        fence_mbar_init();
+    }
     for (int i = tid; i < kWarps * kRadix; i += kThreads) (&sm.whist[0][0])[i] = 0;
     __syncthreads();
     const uint32_t tile = sm.tile;
     const size_t tile_start = (size_t)tile * kTile;
     const int tile_n = (int)min((size_t)kTile, n - tile_start);
 
-    // ---- load (warp-striped: item k of lane l is element base + k*32 + l) ----
-    K key[kItems];
-    uint32_t val[kItems];
-    const size_t wbase = tile_start + (size_t)warp * 32 * kItems;
-#pragma unroll
-    for (int k = 0; k < kItems; ++k) {
-        const size_t i = wbase + (size_t)k * 32 + lane;
-        if (i < n) {
-            if constexpr (SPLAN) {
-                key[k] = reinterpret_cast<const K*>(in_keys)[i];
-                val[k] = 0;
-            } else if constexpr (FIRST) {
-                const R s = xdiv(reinterpret_cast<const R*>(in_keys)[i], t);
-                const bool nz = as_bits(s) == Traits<R>::kSign;
-                key[k] = radix_key<R>(s);
-                val[k] = (uint32_t)i | (nz ? 0x80000000u : 0u);
-            } else {
-                key[k] = reinterpret_cast<const K*>(in_keys)[i];
-                val[k] = in_vals[i];
-            }
-        } else {
-            key[k] = 0;
-            val[k] = 0;
-        }
+    // ---- TMA the tile; a ragged tail (< 16 bytes) is loaded by threads ----
+    const K* gk = reinterpret_cast<const K*>(in_keys) + tile_start;
+    const uint32_t* gv = HAS_VALS ? in_vals + tile_start : nullptr;
+    const bool tma_ok = ((reinterpret_cast<uintptr_t>(gk) & 15) == 0) &&
+                        (!HAS_VALS || (reinterpret_cast<uintptr_t>(gv) & 15) == 0);
+    const uint32_t kbytes = tma_ok ? ((uint32_t)(tile_n * sizeof(K)) & ~15u) : 0u;
+    const uint32_t vbytes = (tma_ok && HAS_VALS) ? ((uint32_t)(tile_n * 4) & ~15u) : 0u;
+    if (tid == 0) {
+        mbar_expect_tx(&sm.bar, kbytes + vbytes);
+        if (kbytes) bulk_g2s(sm.ik, gk, kbytes, &sm.bar);
+        if (vbytes) bulk_g2s(sm.iv, gv, vbytes, &sm.bar);
     }
+    for (int i = (int)(kbytes / sizeof(K)) + tid; i < tile_n; i += kThreads) sm.ik[i] = gk[i];
+    if constexpr (HAS_VALS)
+        for (int i = (int)(vbytes / 4) + tid; i < tile_n; i += kThreads) sm.iv[i] = gv[i];
+    mbar_wait(&sm.bar, 0);
+    __syncthreads();
+    if constexpr (FIRST) {  // raw/t -> radix key, payload = index | (-0 flag)
+        for (int i = tid; i < tile_n; i += kThreads) {
+            const R sv = xdiv(from_bits(sm.ik[i], R(0)), t);
+            const bool nz = as_bits(sv) == Traits<R>::kSign;
+            sm.ik[i] = radix_key<R>(sv);
+            sm.iv[i] = (uint32_t)(tile_start + i) | (nz ? 0x80000000u : 0u);
+        }
+        __syncthreads();
+    }
+    // warp-striped item layout: item k of lane l is tile element w*32*kItems + k*32 + l
+    const int wbase = warp * 32 * kItems;
 
 #if !defined(LX_SORT_LATE)
     // ---- early counts: per-warp digit histogram (order-free smem atomics),
     // published before ranking so successors' look-back overlaps our ranking ----
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
-        const size_t i = wbase + (size_t)k * 32 + lane;
-        if (i < n) atomicAdd(&sm.whist[warp][(int)((key[k] >> shift) & (kRadix - 1))], 1u);
+        const int li = wbase + k * 32 + lane;
+        if (li < tile_n) atomicAdd(&sm.whist[warp][(int)((sm.ik[li] >> shift) & (kRadix - 1))], 1u);
     }
     __syncthreads();
 #endif
@@ -198,26 +213,25 @@ __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict_
         count += c;
     }
     st_relaxed_u64(my_status, status(tile == 0 ? kFlagInc : kFlagAgg, epoch, count));
-#endif
-
-    // ---- stable in-warp ranks: peer mask per key (8 ballots or match.any) and a
-    // running per-warp digit cursor ----
-    uint32_t rank[kItems];
-    const unsigned lt = lanemask_lt();
-#if !defined(LX_SORT_LATE)
     __syncthreads();  // warp-exclusive offsets visible before the cursors start
 #endif
+
+    // ---- stable in-warp ranks: peer mask per key (8 ballots) and a running
+    // per-warp digit cursor ----
+    uint32_t rank[kItems];
+    const unsigned lt = lanemask_lt();
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
         // invalid tail items use digit 255 and are never counted: they follow
         // every valid item of the warp, so they never shift a valid rank
-        const size_t i = wbase + (size_t)k * 32 + lane;
-        const int dk = (int)((key[k] >> shift) & (kRadix - 1));
+        const int li = wbase + k * 32 + lane;
+        const bool valid = li < tile_n;
+        const int dk = valid ? (int)((sm.ik[li] >> shift) & (kRadix - 1)) : kRadix - 1;
 #if defined(LX_SORT_MATCH_ANY)
-        const unsigned peers = __match_any_sync(FULL, i < n ? dk : kRadix);
+        const unsigned peers = __match_any_sync(FULL, valid ? dk : kRadix);
 #else
-        unsigned peers = __ballot_sync(FULL, i < n);
-        if (i >= n) peers = ~peers;
+        unsigned peers = __ballot_sync(FULL, valid);
+        if (!valid) peers = ~peers;
 #pragma unroll
         for (int b = 0; b < kBits; ++b) {
             const bool bit = (dk >> b) & 1;
@@ -229,7 +243,7 @@ __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict_
         uint32_t cnt = 0;
         if (lane == leader) cnt = sm.whist[warp][dk];
         cnt = __shfl_sync(FULL, cnt, leader);
-        if (lane == leader && i < n) sm.whist[warp][dk] = cnt + __popc(peers);
+        if (lane == leader && valid) sm.whist[warp][dk] = cnt + __popc(peers);
         rank[k] = cnt + __popc(peers & lt);
         __syncwarp();
     }
@@ -264,16 +278,11 @@ __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict_
     if (tile > 0) {
         uint32_t j = tile - 1;
         while (true) {
-            const unsigned long long s = ld_relaxed_u64(lookback + (size_t)j * kRadix + d);
-            const uint32_t e = (uint32_t)(s >> 32) & 0x3fffffffu;
-            const unsigned long long f = s & (3ull << 62);
-            if (f == 0 || e != (epoch & 0x3fffffffu)) {  // predecessor not published yet
-#if defined(LX_SORT_BACKOFF)
-                __nanosleep(LX_SORT_BACKOFF);
-#endif
-                continue;
-            }
-            excl += (uint32_t)s;
+            const unsigned long long st = ld_relaxed_u64(lookback + (size_t)j * kRadix + d);
+            const uint32_t e = (uint32_t)(st >> 32) & 0x3fffffffu;
+            const unsigned long long f = st & (3ull << 62);
+            if (f == 0 || e != (epoch & 0x3fffffffu)) continue;  // predecessor not published yet
+            excl += (uint32_t)st;
             if (f == kFlagInc) break;
             --j;
         }
@@ -289,37 +298,38 @@ __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict_
     // ---- scatter into shared memory in digit order ----
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
-        const size_t i = wbase + (size_t)k * 32 + lane;
-        if (i < n) {
-            const int dk = (int)((key[k] >> shift) & (kRadix - 1));
+        const int li = wbase + k * 32 + lane;
+        if (li < tile_n) {
+            const K key = sm.ik[li];
+            const int dk = (int)((key >> shift) & (kRadix - 1));
 #if !defined(LX_SORT_LATE)
             const uint32_t pos = sm.dstart[dk] + rank[k];  // rank includes the warp offset
 #else
             const uint32_t pos = sm.dstart[dk] + sm.whist[warp][dk] + rank[k];
 #endif
-            sm.keys[pos] = key[k];
+            sm.ok[pos] = key;
             if constexpr (SPLAN)
-                out_vals[i] = sm.gbase[dk] + pos;
+                out_vals[tile_start + li] = sm.gbase[dk] + pos;
             else
-                sm.vals[pos] = val[k];
+                sm.ov[pos] = sm.iv[li];
         }
     }
     __syncthreads();
 
     // ---- digit-contiguous global writes ----
     for (int i = tid; i < tile_n; i += kThreads) {
-        const K kk = sm.keys[i];
-        const uint32_t v = SPLAN ? 0u : sm.vals[i];
+        const K kk = sm.ok[i];
         const int dk = (int)((kk >> shift) & (kRadix - 1));
         const uint32_t o = sm.gbase[dk] + (uint32_t)i;
         if constexpr (SPLAN) {
             reinterpret_cast<K*>(out_keys)[o] = kk;
         } else if constexpr (LAST) {
+            const uint32_t v = sm.ov[i];
             reinterpret_cast<R*>(out_keys)[o] = radix_value<R>(kk, (v >> 31) != 0);
             out_vals[o] = v & 0x7fffffffu;
         } else {
             reinterpret_cast<K*>(out_keys)[o] = kk;
-            out_vals[o] = v;
+            out_vals[o] = sm.ov[i];
         }
     }
 }
