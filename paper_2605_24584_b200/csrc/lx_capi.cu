@@ -151,6 +151,12 @@ struct Side {
 // Sides up to this many elements permute directly (the whole vector is
 // L2-resident, 126 MB); larger ones go through the two-pass plan.
 constexpr uint32_t kDirectMax = 1u << 22;
+#ifndef LX_FWD_TPB
+#define LX_FWD_TPB 256
+#endif
+#ifndef LX_BWD_TPB
+#define LX_BWD_TPB 256
+#endif
 constexpr size_t kTmaPad = 64;  // slack after anchor arrays for 16-byte TMA rounding
 
 struct Core {
@@ -480,17 +486,26 @@ lx::ms::MainArgs<R> main_args(const View<R>& v, int rows) {
     return a;
 }
 
+// Main-kernel shape per mode: threads per CTA x items per thread (= one 2048
+// element merge tile).  The backward carries twice the channels, so it runs
+// more threads with fewer items each to stay inside the register file.
+template <bool BWD>
+struct MainShape {
+    static constexpr int TPB = BWD ? LX_BWD_TPB : LX_FWD_TPB;
+    static constexpr int IPT = lx::ms::kTile / TPB;
+};
+
 template <class R, int NG, int NX, bool BWD, bool SEQ = false>
 void launch_main(const char* name, const lx::ms::MainArgs<R>& a, cudaStream_t st) {
     using namespace lx::ms;
-    const size_t smem = sizeof(MainSmem<R, NG, NX>);
+    constexpr int TPB = MainShape<BWD>::TPB, IPT = MainShape<BWD>::IPT;
+    const size_t smem = sizeof(MainSmem<R, NG, NX, TPB / 32>);
     static std::once_flag once;
     std::call_once(once, [&] {
-        cudaFuncSetAttribute(lx_main<R, NG, NX, BWD, SEQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(lx_main<R, NG, NX, BWD, SEQ, TPB, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
     });
-    launch(name, st, [&] {
-        lx_main<R, NG, NX, BWD, SEQ><<<a.T, kThreads, smem, st>>>(a);
-    });
+    launch(name, st, [&] { lx_main<R, NG, NX, BWD, SEQ, TPB, IPT><<<a.T, TPB, smem, st>>>(a); });
 }
 
 template <class R, int NC>
