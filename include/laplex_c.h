@@ -123,6 +123,40 @@ int laplex_sort(int dtype, const void* raw, size_t m, void* values, uint64_t* pe
 int laplex_scan(int dtype, const void* sorted_values, size_t m, const void* payload, void* prefix,
                 void* suffix);
 
+/* ---- range-sharded operator (multi-GPU) ----------------------
+ * A long vector is split over ranks by VALUE: shard(v) = #{splitters < v} with
+ * splitters shared by a and b (equal-value runs never straddle shards).  The
+ * caller (paper_2605_24584_b200/sharded.py) moves data with NCCL; these entry
+ * points are the per-rank device work.  All device pointers, stream-ordered. */
+typedef struct laplex_work_s* laplex_work;
+/* Stable partition of raw/t by shard: counts[s] = elements of shard s
+ * (s = 0..nsplit), perm[j] = local index of the j-th element in shard order. */
+int laplex_shard_partition_dev(int dtype, const void* raw, size_t m, double t, const void* splitters,
+                               int nsplit, uint32_t* perm, uint32_t* counts, void* stream);
+/* dst[r][j] = src[r*ld_src + idx[j]]  /  dst[r*ld_dst + idx[j]] = src[r][j] */
+int laplex_gather_dev(int dtype, const void* src, size_t ld_src, const uint32_t* idx, size_t m, size_t rows,
+                      void* dst, void* stream);
+int laplex_scatter_dev(int dtype, const void* src, const uint32_t* idx, size_t m, size_t rows, void* dst,
+                       size_t ld_dst, void* stream);
+/* Plan of one shard's received anchors; one side may be empty (n + k >= 1). */
+int laplex_shard_plan_create_dev(int dtype, const void* a, size_t n, const void* b, size_t k, double t,
+                                 const void* phi, const void* psi, void* stream, laplex_plan* out);
+/* Entries (Real) of a totals / ext array: 3 + 2 * slots * rows, slots = 2 * channels. */
+int laplex_shard_totals_count(laplex_plan plan, unsigned flags, int backward, size_t rows, size_t* count);
+/* begin: local tile aggregates + carries; writes this shard's totals
+ *   [0] last anchor, [1] first anchor, [2] 1, prefix totals [slot][rows], suffix totals [slot][rows].
+ * end: folds the external carries ext (same layout; [0] prefix anchor, [1]
+ * suffix anchor, [2] flags 1|2 = prefix|suffix present; NULL = none) and
+ * writes the outputs (in this shard's received order); releases work. */
+int laplex_shard_apply_begin(laplex_plan plan, unsigned flags, const void* X, size_t rows, void* totals,
+                             laplex_work* work, void* stream);
+int laplex_shard_apply_end(laplex_work work, const void* ext, void* Y, void* stream);
+int laplex_shard_backward_begin(laplex_plan plan, unsigned flags, const void* X, const void* G, size_t rows,
+                                void* totals, laplex_work* work, void* stream);
+int laplex_shard_backward_end(laplex_work work, const void* ext, void* x_bar, void* a_bar, void* b_bar,
+                              void* phi_bar, void* psi_bar, void* stream);
+int laplex_work_release(laplex_work work);
+
 /* Number of CUDA kernels this library launched on the calling process
  * (instrumentation for the benchmark's gpu_launches count). */
 uint64_t laplex_kernel_launches(void);

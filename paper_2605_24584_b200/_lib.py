@@ -42,6 +42,16 @@ _SIGS = {
     "laplex_gram_dev": (C.c_int, [vp, C.c_uint, vp, vp, vp]),
     "laplex_gram_vjp_weights": (C.c_int, [vp, vp, sz, vp, sz, sz, vp]),
     "laplex_sort": (C.c_int, [C.c_int, vp, sz, vp, vp, vp]),
+    "laplex_shard_partition_dev": (C.c_int, [C.c_int, vp, sz, C.c_double, vp, C.c_int, vp, vp, vp]),
+    "laplex_gather_dev": (C.c_int, [C.c_int, vp, sz, vp, sz, sz, vp, vp]),
+    "laplex_scatter_dev": (C.c_int, [C.c_int, vp, vp, sz, sz, vp, sz, vp]),
+    "laplex_shard_plan_create_dev": (C.c_int, [C.c_int, vp, sz, vp, sz, C.c_double, vp, vp, vp, C.POINTER(vp)]),
+    "laplex_shard_totals_count": (C.c_int, [vp, C.c_uint, C.c_int, sz, C.POINTER(sz)]),
+    "laplex_shard_apply_begin": (C.c_int, [vp, C.c_uint, vp, sz, vp, C.POINTER(vp), vp]),
+    "laplex_shard_apply_end": (C.c_int, [vp, vp, vp, vp]),
+    "laplex_shard_backward_begin": (C.c_int, [vp, C.c_uint, vp, vp, sz, vp, C.POINTER(vp), vp]),
+    "laplex_shard_backward_end": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp]),
+    "laplex_work_release": (C.c_int, [vp]),
     "laplex_scan": (C.c_int, [C.c_int, vp, sz, vp, vp, vp]),
 }
 

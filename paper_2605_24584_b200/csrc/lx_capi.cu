@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <utility>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -22,6 +23,7 @@
 #include "lx_common.cuh"
 #include "lx_gram.cuh"
 #include "lx_scan.cuh"
+#include "lx_shard.cuh"
 #include "lx_sort.cuh"
 
 namespace {
@@ -187,6 +189,8 @@ struct laplex_plan_s {
     bool swapped = false;
     std::atomic<int> refs{1};
 };
+
+struct laplex_work_s;  // defined after the staged helpers
 
 namespace {
 
@@ -370,7 +374,8 @@ template <class R>
 void build_side(Side& sd, const R* raw, uint32_t m, R t, const R* phase, int* bad, cudaStream_t st) {
     sd.m = m;
     sd.vals = DBuf((size_t)m * sizeof(R) + kTmaPad, st);  // TMA reads round up to 16 B
-    sd.perm = DBuf((size_t)m * 4, st);
+    sd.perm = DBuf((size_t)m * 4 + 16, st);
+    if (m == 0) return;  // empty side of a range shard
     radix_sort<R>(raw, m, t, sd.vals.as<R>(), sd.perm.as<uint32_t>(), bad, st);
     if (phase) {
         DBuf ph((size_t)m * sizeof(R), st);
@@ -615,28 +620,81 @@ void scan_carries(const View<R>& v, const Scratch& sc, int rows, unsigned pm, un
                         rows, pm, qm, st);
 }
 
+// ---- staged forward / backward (begin: aggregates + local carries; end:
+// optional external shard carries -> outputs).  The unsharded calls run both
+// halves back to back; the range-sharded operator exchanges the shard totals
+// between them. ----
+struct WorkBase {
+    virtual ~WorkBase() = default;
+    std::shared_ptr<Core> keep;  // the plan outlives the work
+    size_t total_count = 0;      // Real entries of the totals / ext arrays
+};
+
+template <class R>
+void collect_totals(const View<R>& v, const Scratch& sc, int rows, int slots, R* out, cudaStream_t st) {
+    const int per = slots * rows;
+    launch("lx_collect_totals", st, [&] {
+        lx::shard::lx_collect_totals<R><<<(per + 255) / 256, 256, 0, st>>>(
+            sc.cp.as<R>(), sc.cq.as<R>(), v.s_last, v.s_first, v.T, rows, slots, out);
+    });
+}
+
 template <class R, int NX>
-void apply_fwd(const View<R>& v, const R* X, int rows, R* Y, cudaStream_t st) {
-    auto a = main_args(v, rows);
-    Scratch sc(2 * NX, rows, v.T, sizeof(R), st);
-    DBuf xs = sorted_payload<R, NX, false, false, false>(v, rows, X, sc, 0, a.ldxs, st);
-    a.Xs = xs.as<R>();
-    scan_carries<R, NX>(v, sc, rows, 0u, 0u, st);
-    a.cp = sc.cp.as<R>();
-    a.cq = sc.cq.as<R>();
+struct FwdWork : WorkBase {
+    View<R> v;
+    lx::ms::MainArgs<R> a;
+    Scratch sc;
+    DBuf xs;
+    int rows;
+    FwdWork(const View<R>& v_, int rows_, cudaStream_t st) : v(v_), sc(2 * NX, rows_, v_.T, sizeof(R), st), rows(rows_) {}
+};
+
+template <class R, int NX>
+std::unique_ptr<FwdWork<R, NX>> fwd_begin(const View<R>& v, const R* X, int rows, cudaStream_t st) {
+    auto w = std::make_unique<FwdWork<R, NX>>(v, rows, st);
+    w->a = main_args(v, rows);
+    w->xs = sorted_payload<R, NX, false, false, false>(v, rows, X, w->sc, 0, w->a.ldxs, st);
+    w->a.Xs = w->xs.template as<R>();
+    scan_carries<R, NX>(v, w->sc, rows, 0u, 0u, st);
+    w->a.cp = w->sc.cp.template as<R>();
+    w->a.cq = w->sc.cq.template as<R>();
+    w->total_count = 3 + 2 * (size_t)(2 * NX) * rows;
+    return w;
+}
+
+template <class R, int NX>
+void fwd_end(FwdWork<R, NX>& w, const R* ext, R* Y, cudaStream_t st) {
+    const View<R>& v = w.v;
+    auto& a = w.a;
+    a.ext = ext;
     DBuf yst;
     if (v.dst_a) {  // write bucket-staged, then scatter through the rows plan
-        yst = DBuf((size_t)rows * v.n * sizeof(R), st);
+        yst = DBuf((size_t)w.rows * v.n * sizeof(R), st);
         a.y = yst.as<R>();
         a.perm_a = v.pos_a;
     } else {
         a.y = Y;
     }
     a.ldy = v.n;
-    launch_main<R, 0, NX, false>(NX == 2 ? "lx_main_fwd_phased" : "lx_main_fwd", a, st);
-    xs.release();
+    if (v.n) launch_main<R, 0, NX, false>(NX == 2 ? "lx_main_fwd_phased" : "lx_main_fwd", a, st);
+    w.xs.release();
     if (v.dst_a)
-        stage_scatter<R>(v.dst_a, v.n, yst.as<R>(), Y, v.n, rows, nullptr, nullptr, nullptr, nullptr, st);
+        stage_scatter<R>(v.dst_a, v.n, yst.as<R>(), Y, v.n, w.rows, nullptr, nullptr, nullptr, nullptr, st);
+}
+
+}  // namespace
+struct laplex_work_s {
+    std::unique_ptr<WorkBase> impl;
+    int dtype = LAPLEX_F32;
+    bool backward = false;
+    bool phased = false;
+};
+namespace {
+
+template <class R, int NX>
+void apply_fwd(const View<R>& v, const R* X, int rows, R* Y, cudaStream_t st) {
+    auto w = fwd_begin<R, NX>(v, X, rows, st);
+    fwd_end<R, NX>(*w, nullptr, Y, st);
 }
 
 template <class R>
@@ -664,20 +722,41 @@ void apply_trn(const View<R>& v, const R* G, int rows, R* Y, cudaStream_t st) {
 }
 
 template <class R, int NCH>
-void backward_impl(const View<R>& v, const R* X, const R* G, int rows, R* xbar, R* abar, R* bbar, R* phibar,
-                   R* psibar, cudaStream_t st) {
+struct BwdWork : WorkBase {
+    View<R> v;
+    lx::ms::MainArgs<R> a;
+    Scratch sc;
+    DBuf gs, xs;
+    int rows;
+    BwdWork(const View<R>& v_, int rows_, cudaStream_t st)
+        : v(v_), sc(2 * 2 * NCH, rows_, v_.T, sizeof(R), st), rows(rows_) {}
+};
+
+template <class R, int NCH>
+std::unique_ptr<BwdWork<R, NCH>> bwd_begin(const View<R>& v, const R* X, const R* G, int rows, cudaStream_t st) {
     constexpr int NC = 2 * NCH;
-    const size_t rs = sizeof(R);
-    auto a = main_args(v, rows);
-    Scratch sc(2 * NC, rows, v.T, rs, st);
-    DBuf gs = sorted_payload<R, NCH, true, true, true>(v, rows, G, sc, 0, a.ldgs, st);
-    DBuf xs = sorted_payload<R, NCH, false, false, true>(v, rows, X, sc, NCH, a.ldxs, st);
-    a.Gs = gs.as<R>();
-    a.Xs = xs.as<R>();
+    auto w = std::make_unique<BwdWork<R, NCH>>(v, rows, st);
+    auto& a = w->a;
+    a = main_args(v, rows);
+    w->gs = sorted_payload<R, NCH, true, true, true>(v, rows, G, w->sc, 0, a.ldgs, st);
+    w->xs = sorted_payload<R, NCH, false, false, true>(v, rows, X, w->sc, NCH, a.ldxs, st);
+    a.Gs = w->gs.template as<R>();
+    a.Xs = w->xs.template as<R>();
     const unsigned gmask = (1u << NCH) - 1u;
-    scan_carries<R, NC>(v, sc, rows, gmask, gmask << NCH, st);
-    a.cp = sc.cp.as<R>();
-    a.cq = sc.cq.as<R>();
+    scan_carries<R, NC>(v, w->sc, rows, gmask, gmask << NCH, st);
+    a.cp = w->sc.cp.template as<R>();
+    a.cq = w->sc.cq.template as<R>();
+    w->total_count = 3 + 2 * (size_t)(2 * NC) * rows;
+    return w;
+}
+
+template <class R, int NCH>
+void bwd_end(BwdWork<R, NCH>& w, const R* ext, R* xbar, R* abar, R* bbar, R* phibar, R* psibar, cudaStream_t st) {
+    const View<R>& v = w.v;
+    auto& a = w.a;
+    const int rows = w.rows;
+    const size_t rs = sizeof(R);
+    a.ext = ext;
     DBuf sxb, sbb, sqb, sab, spb;  // bucket-staged outputs
     if (v.dst_b) {
         sxb = DBuf((size_t)rows * v.k * rs, st);
@@ -704,14 +783,21 @@ void backward_impl(const View<R>& v, const R* X, const R* G, int rows, R* xbar, 
     }
     a.ldxb = v.k;
     launch_main<R, NCH, NCH, true>(NCH == 2 ? "lx_main_bwd_phased" : "lx_main_bwd", a, st);
-    gs.release();
-    xs.release();
+    w.gs.release();
+    w.xs.release();
     if (v.dst_b)
         stage_scatter<R>(v.dst_b, v.k, sxb.as<R>(), xbar, v.k, rows, sbb.as<R>(), bbar,
                          NCH == 2 ? sqb.as<R>() : nullptr, psibar, st);
     if (v.dst_a)
         stage_scatter<R>(v.dst_a, v.n, sab.as<R>(), abar, v.n, 1, NCH == 2 ? spb.as<R>() : nullptr, phibar, nullptr,
                          nullptr, st);
+}
+
+template <class R, int NCH>
+void backward_impl(const View<R>& v, const R* X, const R* G, int rows, R* xbar, R* abar, R* bbar, R* phibar,
+                   R* psibar, cudaStream_t st) {
+    auto w = bwd_begin<R, NCH>(v, X, G, rows, st);
+    bwd_end<R, NCH>(*w, nullptr, xbar, abar, bbar, phibar, psibar, st);
 }
 
 template <class R>
@@ -1385,4 +1471,232 @@ int laplex_scan(int dtype, const void* sorted_values, size_t m, const void* payl
     });
 }
 
+// ---------------------------------------------------------------------------
+// range-sharded (multi-GPU) building blocks
+// ---------------------------------------------------------------------------
+int laplex_shard_plan_create_dev(int dtype, const void* a, size_t n, const void* b, size_t k, double t,
+                                 const void* phi, const void* psi, void* stream, laplex_plan* out) {
+    return guarded([&] {
+        if (!out) fail(LAPLEX_E_INVALID_ARGUMENT, "out is NULL");
+        *out = nullptr;
+        dtype_check(dtype);
+        if (n + k == 0) fail(LAPLEX_E_EMPTY_INPUT, "shard plan: no anchors on this shard");
+        if (!(t > 0.0) || !std::isfinite(t))
+            fail(LAPLEX_E_NON_FINITE, "LaplexOperator: temperature must be positive and finite");
+        if (n >= 0x80000000ull || k >= 0x80000000ull) fail(LAPLEX_E_INVALID_SIZE, "n and k must be < 2^31");
+        cudaStream_t st = as_stream(stream);
+        if (dtype == LAPLEX_F64)
+            *out = create_plan<double>((const double*)a, (uint32_t)n, (const double*)b, (uint32_t)k, t,
+                                       (const double*)phi, (const double*)psi, st);
+        else
+            *out = create_plan<float>((const float*)a, (uint32_t)n, (const float*)b, (uint32_t)k, t,
+                                      (const float*)phi, (const float*)psi, st);
+    });
+}
+
+int laplex_shard_partition_dev(int dtype, const void* raw, size_t m, double t, const void* splitters, int nsplit,
+                               uint32_t* perm, uint32_t* counts, void* stream) {
+    return guarded([&] {
+        dtype_check(dtype);
+        if (nsplit < 0 || nsplit >= lx::shard::kMaxShards) fail(LAPLEX_E_INVALID_ARGUMENT, "nsplit");
+        cudaStream_t st = as_stream(stream);
+        init_pool();
+        const int nsh = nsplit + 1;
+        if (m == 0) {
+            ck(cudaMemsetAsync(counts, 0, (size_t)nsh * 4, st), "memset");
+            return;
+        }
+        const uint32_t tiles = (uint32_t)((m + lx::shard::kTile - 1) / lx::shard::kTile);
+        DBuf cnt((size_t)tiles * lx::shard::kMaxShards * 4, st);
+        auto run = [&](auto zero) {
+            using R = decltype(zero);
+            const R* rp = (const R*)raw;
+            const R* sp = (const R*)splitters;
+            const R tr = R(t);
+            launch("lx_shard_count", st, [&] {
+                lx::shard::lx_shard_count<R><<<tiles, lx::shard::kThreads, 0, st>>>(rp, m, tr, sp, nsplit,
+                                                                                    cnt.as<uint32_t>());
+            });
+            launch("lx_shard_offsets", st, [&] {
+                lx::shard::lx_shard_offsets<<<1, lx::shard::kMaxShards, 0, st>>>(cnt.as<uint32_t>(), tiles, nsh,
+                                                                                counts);
+            });
+            launch("lx_shard_scatter", st, [&] {
+                lx::shard::lx_shard_scatter<R><<<tiles, lx::shard::kThreads, 0, st>>>(rp, m, tr, sp, nsplit,
+                                                                                      cnt.as<uint32_t>(), perm);
+            });
+        };
+        if (dtype == LAPLEX_F64)
+            run(0.0);
+        else
+            run(0.0f);
+    });
+}
+
+int laplex_gather_dev(int dtype, const void* src, size_t ld_src, const uint32_t* idx, size_t m, size_t rows,
+                      void* dst, void* stream) {
+    return guarded([&] {
+        dtype_check(dtype);
+        if (m == 0 || rows == 0) return;
+        cudaStream_t st = as_stream(stream);
+        auto run = [&](auto zero) {
+            using R = decltype(zero);
+            launch("lx_gather_idx", st, [&] {
+                lx::shard::lx_gather_idx<R><<<grid_for(m * rows), 256, 0, st>>>((const R*)src, ld_src, idx, m,
+                                                                                 (int)rows, (R*)dst);
+            });
+        };
+        if (dtype == LAPLEX_F64)
+            run(0.0);
+        else
+            run(0.0f);
+    });
+}
+
+int laplex_scatter_dev(int dtype, const void* src, const uint32_t* idx, size_t m, size_t rows, void* dst,
+                       size_t ld_dst, void* stream) {
+    return guarded([&] {
+        dtype_check(dtype);
+        if (m == 0 || rows == 0) return;
+        cudaStream_t st = as_stream(stream);
+        auto run = [&](auto zero) {
+            using R = decltype(zero);
+            launch("lx_scatter_idx", st, [&] {
+                lx::shard::lx_scatter_idx<R><<<grid_for(m * rows), 256, 0, st>>>((const R*)src, idx, m, (int)rows,
+                                                                                  (R*)dst, ld_dst);
+            });
+        };
+        if (dtype == LAPLEX_F64)
+            run(0.0);
+        else
+            run(0.0f);
+    });
+}
+
+int laplex_shard_totals_count(laplex_plan plan, unsigned flags, int backward, size_t rows, size_t* count) {
+    return guarded([&] {
+        check_plan(plan);
+        const int ch = (flags & LAPLEX_PHASED) ? 2 : 1;
+        const int nc = backward ? 2 * ch : ch;
+        *count = 3 + 2 * (size_t)(2 * nc) * rows;
+    });
+}
+
+int laplex_shard_apply_begin(laplex_plan plan, unsigned flags, const void* X, size_t rows, void* totals,
+                             laplex_work* work, void* stream) {
+    return guarded([&] {
+        check_plan(plan);
+        Core& c = *plan->core;
+        const bool ph = flags & LAPLEX_PHASED;
+        if (ph != c.phased) fail(ph ? LAPLEX_E_PHASE_ABSENT : LAPLEX_E_PHASE_PRESENT, "shard apply: phase mismatch");
+        if (flags & LAPLEX_TRANSPOSE) fail(LAPLEX_E_INVALID_ARGUMENT, "shard apply: transpose not supported");
+        if (rows == 0 || rows > 0x7fffffff) fail(LAPLEX_E_INVALID_SIZE, "rows");
+        cudaStream_t st = as_stream(stream);
+        auto w = std::make_unique<laplex_work_s>();
+        w->dtype = c.dtype;
+        w->phased = ph;
+        auto run = [&](auto zero) {
+            using R = decltype(zero);
+            View<R> v = view<R>(c, plan->swapped, st);
+            if (ph) {
+                auto f = fwd_begin<R, 2>(v, (const R*)X, (int)rows, st);
+                collect_totals<R>(v, f->sc, (int)rows, 4, (R*)totals, st);
+                w->impl = std::move(f);
+            } else {
+                auto f = fwd_begin<R, 1>(v, (const R*)X, (int)rows, st);
+                collect_totals<R>(v, f->sc, (int)rows, 2, (R*)totals, st);
+                w->impl = std::move(f);
+            }
+            w->impl->keep = plan->core;
+        };
+        if (c.dtype == LAPLEX_F64)
+            run(0.0);
+        else
+            run(0.0f);
+        *work = w.release();
+    });
+}
+
+int laplex_shard_apply_end(laplex_work work, const void* ext, void* Y, void* stream) {
+    return guarded([&] {
+        if (!work || work->backward) fail(LAPLEX_E_INVALID_ARGUMENT, "invalid work handle");
+        cudaStream_t st = as_stream(stream);
+        auto run = [&](auto zero) {
+            using R = decltype(zero);
+            if (work->phased)
+                fwd_end<R, 2>(*static_cast<FwdWork<R, 2>*>(work->impl.get()), (const R*)ext, (R*)Y, st);
+            else
+                fwd_end<R, 1>(*static_cast<FwdWork<R, 1>*>(work->impl.get()), (const R*)ext, (R*)Y, st);
+        };
+        if (work->dtype == LAPLEX_F64)
+            run(0.0);
+        else
+            run(0.0f);
+        delete work;
+    });
+}
+
+int laplex_shard_backward_begin(laplex_plan plan, unsigned flags, const void* X, const void* G, size_t rows,
+                                void* totals, laplex_work* work, void* stream) {
+    return guarded([&] {
+        check_plan(plan);
+        Core& c = *plan->core;
+        const bool ph = flags & LAPLEX_PHASED;
+        if (ph != c.phased) fail(ph ? LAPLEX_E_PHASE_ABSENT : LAPLEX_E_PHASE_PRESENT, "shard backward: phases");
+        if (rows == 0 || rows > 0x7fffffff) fail(LAPLEX_E_INVALID_SIZE, "rows");
+        cudaStream_t st = as_stream(stream);
+        auto w = std::make_unique<laplex_work_s>();
+        w->dtype = c.dtype;
+        w->phased = ph;
+        w->backward = true;
+        auto run = [&](auto zero) {
+            using R = decltype(zero);
+            View<R> v = view<R>(c, plan->swapped, st);
+            if (ph) {
+                auto b = bwd_begin<R, 2>(v, (const R*)X, (const R*)G, (int)rows, st);
+                collect_totals<R>(v, b->sc, (int)rows, 8, (R*)totals, st);
+                w->impl = std::move(b);
+            } else {
+                auto b = bwd_begin<R, 1>(v, (const R*)X, (const R*)G, (int)rows, st);
+                collect_totals<R>(v, b->sc, (int)rows, 4, (R*)totals, st);
+                w->impl = std::move(b);
+            }
+            w->impl->keep = plan->core;
+        };
+        if (c.dtype == LAPLEX_F64)
+            run(0.0);
+        else
+            run(0.0f);
+        *work = w.release();
+    });
+}
+
+int laplex_shard_backward_end(laplex_work work, const void* ext, void* x_bar, void* a_bar, void* b_bar,
+                              void* phi_bar, void* psi_bar, void* stream) {
+    return guarded([&] {
+        if (!work || !work->backward) fail(LAPLEX_E_INVALID_ARGUMENT, "invalid work handle");
+        cudaStream_t st = as_stream(stream);
+        auto run = [&](auto zero) {
+            using R = decltype(zero);
+            if (work->phased)
+                bwd_end<R, 2>(*static_cast<BwdWork<R, 2>*>(work->impl.get()), (const R*)ext, (R*)x_bar, (R*)a_bar,
+                              (R*)b_bar, (R*)phi_bar, (R*)psi_bar, st);
+            else
+                bwd_end<R, 1>(*static_cast<BwdWork<R, 1>*>(work->impl.get()), (const R*)ext, (R*)x_bar, (R*)a_bar,
+                              (R*)b_bar, nullptr, nullptr, st);
+        };
+        if (work->dtype == LAPLEX_F64)
+            run(0.0);
+        else
+            run(0.0f);
+        delete work;
+    });
+}
+
+int laplex_work_release(laplex_work work) {
+    delete work;
+    return LAPLEX_OK;
+}
+
 }  // extern "C"
+

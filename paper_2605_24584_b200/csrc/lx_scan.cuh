@@ -197,6 +197,13 @@ struct MainArgs {
     const R* s_first;  // [T] anchor of each tile's first merged element
     const R* cp;  // inclusive tile carries (lx_carry), [slot][rows][T]
     const R* cq;
+    // external carries from other range shards (multi-GPU): the combined
+    // prefix of all lower shards (anchor = their last element, <= every local
+    // anchor) and suffix of all higher shards; [slot][rows] like one carry tile
+    // device layout: [0] prefix anchor, [1] suffix anchor, [2] flags (1: prefix
+    // present, 2: suffix present), then prefix values [slot][rows] and suffix
+    // values [slot][rows]; null when the operator is not sharded
+    const R* ext;
     R inv_t;
     // final outputs, written at index perm_a[i] / perm_b[j] (caller order, or
     // the bucket-staged position when perm_* holds a plan's pos[] table)
@@ -272,10 +279,17 @@ __global__ void __launch_bounds__(TPB, LX_MAIN_MINB(TPB)) lx_main(MainArgs<R> p)
     const TileDesc<R> dt = p.desc[t], dn = p.desc[t + 1];
     const uint32_t a0 = dt.a0, a1 = dn.a0, b0 = dt.b0, b1 = dn.b0;
     const int na = (int)(a1 - a0), nb = (int)(b1 - b0), len = na + nb;
+    // external shard carries (multi-GPU range sharding)
+    const int ext_flags = p.ext ? (int)p.ext[2] : 0;
+    const bool has_ext_p = ext_flags & 1, has_ext_q = ext_flags & 2;
+    const R ext_pa = has_ext_p ? p.ext[0] : R(0), ext_qa = has_ext_q ? p.ext[1] : R(0);
+    const R* ext_pv = p.ext ? p.ext + 3 : nullptr;
+    const R* ext_qv = p.ext ? p.ext + 3 + (size_t)2 * NC * p.rows : nullptr;
     // neighbouring tiles' edge anchors: the tile carries' reference points
-    const bool hl = t > 0, hr = t + 1 < p.T;
-    const R SL = hl ? p.s_last[t - 1] : R(0);
-    const R SR = hr ? dn.s_first : R(0);
+    // (tile 0 / tile T-1 take the external shard carries when present)
+    const bool hl = t > 0 || has_ext_p, hr = t + 1 < p.T || has_ext_q;
+    const R SL = t > 0 ? p.s_last[t - 1] : ext_pa;
+    const R SR = t + 1 < p.T ? dn.s_first : ext_qa;
     const R s_end = dt.s_last;  // anchor of the tile's last merged element
 
     // ---- prologue: TMA bulk copies ----
@@ -428,14 +442,38 @@ __global__ void __launch_bounds__(TPB, LX_MAIN_MINB(TPB)) lx_main(MainArgs<R> p)
                 if (PAY_B && bytesB) bulk_g2s(sm.payB, p.Xs + (size_t)r * p.ldxs + b0al, bytesB, &sm.barp);
             }
         }
-        // tile carries of this row (issued before the payload wait)
+        // tile carries of this row (issued before the payload wait), combined
+        // with the external shard carries: ext (+) tiles<t  and  tiles>t (+) ext
         R cpv[NC], cps[NC], cqv[NC], cqs[NC];
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
-            cpv[c] = hl ? p.cp[((size_t)(2 * c) * p.rows + r) * T + t - 1] : R(0);
-            cps[c] = (hl && C::pst(c)) ? p.cp[((size_t)(2 * c + 1) * p.rows + r) * T + t - 1] : R(0);
-            cqv[c] = hr ? p.cq[((size_t)(2 * c) * p.rows + r) * T + t + 1] : R(0);
-            cqs[c] = (hr && C::qst(c)) ? p.cq[((size_t)(2 * c + 1) * p.rows + r) * T + t + 1] : R(0);
+            const size_t sl0 = ((size_t)(2 * c) * p.rows + r), sl1 = ((size_t)(2 * c + 1) * p.rows + r);
+            cpv[c] = t > 0 ? p.cp[sl0 * T + t - 1] : R(0);
+            cps[c] = (t > 0 && C::pst(c)) ? p.cp[sl1 * T + t - 1] : R(0);
+            cqv[c] = t + 1 < p.T ? p.cq[sl0 * T + t + 1] : R(0);
+            cqs[c] = (t + 1 < p.T && C::qst(c)) ? p.cq[sl1 * T + t + 1] : R(0);
+            if (has_ext_p) {
+                const R ev = ext_pv[sl0], es = C::pst(c) ? ext_pv[sl1] : R(0);
+                if (t > 0) {  // (ext_anchor, ev, es) then (SL, cpv, cps)
+                    const R e = xexp(xsub(ext_pa, SL));
+                    if (C::pst(c)) cps[c] = xadd(cps[c], ext_pa < SL ? xmul(e, ev) : es);
+                    cpv[c] = xfma(e, ev, cpv[c]);
+                } else {
+                    cpv[c] = ev;
+                    cps[c] = es;
+                }
+            }
+            if (has_ext_q) {
+                const R ev = ext_qv[sl0], es = C::qst(c) ? ext_qv[sl1] : R(0);
+                if (t + 1 < p.T) {  // (SR, cqv, cqs) then (ext_anchor, ev, es)
+                    const R e = xexp(xsub(SR, ext_qa));
+                    if (C::qst(c)) cqs[c] = xadd(cqs[c], SR < ext_qa ? xmul(e, ev) : es);
+                    cqv[c] = xfma(e, ev, cqv[c]);
+                } else {
+                    cqv[c] = ev;
+                    cqs[c] = es;
+                }
+            }
         }
         mbar_wait(&sm.barp, (uint32_t)(r & 1));
         // ---- payloads (from shared memory) ----

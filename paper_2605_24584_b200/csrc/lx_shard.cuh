@@ -1,0 +1,171 @@
+// lx_shard.cuh -- building blocks of the range-sharded (multi-GPU) operator.
+//
+// a single long vector is split into contiguous SORTED ranges,
+// one per GPU.  Splitters are VALUES shared by a and b and an element goes to
+// shard #{splitters < value}, so a run of equal values never straddles two
+// shards (the tie-inclusive co-ranks stay shard-local).  These kernels:
+//   lx_shard_count / lx_shard_offsets / lx_shard_scatter
+//       stable partition of raw/t by shard: counts per shard and the local
+//       index of every element in shard order (what goes into the all-to-all);
+//   lx_collect_totals
+//       per-shard totals of the tile-carry scan (prefix inclusive at the last
+//       tile, suffix inclusive at the first) -- what the all-gather exchanges;
+//   lx_gather_idx / lx_scatter_idx
+//       payload routing by those index lists.
+#pragma once
+
+#include "lx_common.cuh"
+
+namespace lx {
+namespace shard {
+
+constexpr int kThreads = 256;
+constexpr int kItems = 16;
+constexpr int kTile = kThreads * kItems;
+constexpr int kMaxShards = 64;
+
+template <class R>
+__device__ __forceinline__ int shard_of(R v, const R* spl, int nspl) {
+    int s = 0;
+    for (int i = 0; i < nspl; ++i) s += spl[i] < v ? 1 : 0;
+    return s;
+}
+
+// per-tile shard counts: cnt[tile * kMaxShards + s]
+template <class R>
+__global__ void __launch_bounds__(kThreads) lx_shard_count(const R* __restrict__ raw, size_t m, R t,
+                                                          const R* __restrict__ spl, int nspl,
+                                                          uint32_t* __restrict__ cnt) {
+    __shared__ uint32_t sc[kMaxShards];
+    __shared__ R ss[kMaxShards];
+    if (threadIdx.x < kMaxShards) sc[threadIdx.x] = 0;
+    if (threadIdx.x < nspl) ss[threadIdx.x] = spl[threadIdx.x];
+    __syncthreads();
+    const size_t base = (size_t)blockIdx.x * kTile;
+    for (int q = 0; q < kItems; ++q) {
+        const size_t i = base + (size_t)q * kThreads + threadIdx.x;
+        if (i < m) atomicAdd(&sc[shard_of(xdiv(raw[i], t), ss, nspl)], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < kMaxShards) cnt[(size_t)blockIdx.x * kMaxShards + threadIdx.x] = sc[threadIdx.x];
+}
+
+// exclusive offsets: off[tile][s] = sum_{s' < s} total[s'] + sum_{tile' < tile} cnt[tile'][s];
+// counts[s] = total[s].  One block, thread s walks its column.
+__global__ void lx_shard_offsets(uint32_t* __restrict__ cnt, uint32_t tiles, int nsh, uint32_t* __restrict__ counts) {
+    __shared__ uint32_t tot[kMaxShards];
+    const int s = threadIdx.x;
+    uint32_t run = 0;
+    if (s < nsh)
+        for (uint32_t t = 0; t < tiles; ++t) {
+            const uint32_t c = cnt[(size_t)t * kMaxShards + s];
+            cnt[(size_t)t * kMaxShards + s] = run;
+            run += c;
+        }
+    if (s < kMaxShards) tot[s] = s < nsh ? run : 0;
+    __syncthreads();
+    if (s < nsh) {
+        uint32_t base = 0;
+        for (int q = 0; q < s; ++q) base += tot[q];
+        counts[s] = run;
+        for (uint32_t t = 0; t < tiles; ++t) cnt[(size_t)t * kMaxShards + s] += base;
+    }
+}
+
+// stable scatter of local indices into shard order (ranks by ballots over the
+// shard id bits, warp order = input order)
+template <class R>
+__global__ void __launch_bounds__(kThreads) lx_shard_scatter(const R* __restrict__ raw, size_t m, R t,
+                                                            const R* __restrict__ spl, int nspl,
+                                                            const uint32_t* __restrict__ off,
+                                                            uint32_t* __restrict__ perm) {
+    constexpr int W = kThreads / 32;
+    __shared__ uint32_t wc[W][kMaxShards];
+    __shared__ R ss[kMaxShards];
+    for (int i = threadIdx.x; i < W * kMaxShards; i += kThreads) (&wc[0][0])[i] = 0;
+    if (threadIdx.x < nspl) ss[threadIdx.x] = spl[threadIdx.x];
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const size_t base = (size_t)blockIdx.x * kTile + (size_t)warp * 32 * kItems;
+    int sh[kItems];
+    uint32_t rk[kItems];
+    const unsigned lt = lanemask_lt();
+    for (int q = 0; q < kItems; ++q) {
+        const size_t i = base + (size_t)q * 32 + lane;
+        const bool valid = i < m;
+        const int d = valid ? shard_of(xdiv(raw[i], t), ss, nspl) : kMaxShards - 1;
+        unsigned peers = __ballot_sync(FULL, valid);
+        if (!valid) peers = ~peers;
+        for (int b = 0; b < 6; ++b) {
+            const bool bit = (d >> b) & 1;
+            const unsigned mk = __ballot_sync(FULL, bit);
+            peers &= bit ? mk : ~mk;
+        }
+        const int leader = __ffs(peers) - 1;
+        uint32_t c = 0;
+        if (lane == leader) c = wc[warp][d];
+        c = __shfl_sync(FULL, c, leader);
+        if (lane == leader && valid) wc[warp][d] = c + __popc(peers);
+        sh[q] = d;
+        rk[q] = c + __popc(peers & lt);
+        __syncwarp();
+    }
+    __syncthreads();
+    // warp-exclusive offsets per shard
+    if (threadIdx.x < kMaxShards) {
+        uint32_t run = 0;
+        for (int w = 0; w < W; ++w) {
+            const uint32_t c = wc[w][threadIdx.x];
+            wc[w][threadIdx.x] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    for (int q = 0; q < kItems; ++q) {
+        const size_t i = base + (size_t)q * 32 + lane;
+        if (i < m) perm[off[(size_t)blockIdx.x * kMaxShards + sh[q]] + wc[warp][sh[q]] + rk[q]] = (uint32_t)i;
+    }
+}
+
+// totals layout (R): [0] prefix anchor (last merged element), [1] suffix anchor
+// (first merged element), [2] 1 if the shard has elements, then prefix totals
+// [slot][rows] and suffix totals [slot][rows] (slots = 2 * channels).
+template <class R>
+__global__ void lx_collect_totals(const R* __restrict__ cp, const R* __restrict__ cq, const R* __restrict__ s_last,
+                                  const R* __restrict__ s_first, uint32_t T, int rows, int slots,
+                                  R* __restrict__ out) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    const int per = slots * rows;
+    if (e == 0) {
+        out[0] = s_last[T - 1];
+        out[1] = s_first[0];
+        out[2] = R(1);
+    }
+    if (e < per) {
+        out[3 + e] = cp[(size_t)e * T + T - 1];
+        out[3 + per + e] = cq[(size_t)e * T + 0];
+    }
+}
+
+template <class R>
+__global__ void lx_gather_idx(const R* __restrict__ src, size_t ld_src, const uint32_t* __restrict__ idx, size_t m,
+                              int rows, R* __restrict__ dst) {
+    const size_t total = m * rows;
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+        const size_t r = e / m, j = e - r * m;
+        dst[e] = src[r * ld_src + idx[j]];
+    }
+}
+
+template <class R>
+__global__ void lx_scatter_idx(const R* __restrict__ src, const uint32_t* __restrict__ idx, size_t m, int rows,
+                               R* __restrict__ dst, size_t ld_dst) {
+    const size_t total = m * rows;
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+        const size_t r = e / m, j = e - r * m;
+        dst[r * ld_dst + idx[j]] = src[e];
+    }
+}
+
+}  // namespace shard
+}  // namespace lx
