@@ -311,6 +311,114 @@ def run_ours(args, rank, world, dist):
         print(json.dumps(line), flush=True)
 
 
+def run_sharded(args, rank, world, dist, comm_factory):
+    """N > 1: one long vector (n = k = 2^log2n in total) range-sharded over the
+    ranks; each rank starts from its contiguous slice of a, b, x, g."""
+    import torch
+
+    import paper_2605_24584_b200 as L
+    from paper_2605_24584_b200.sharded import GpuBackend, ShardedOperator
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not args.sim:
+        torch.cuda.set_device(local)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    n = k = 1 << args.log2n
+    nl, kl = n // world, k // world
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(42 + rank)
+    a = torch.empty(nl, device=dev).uniform_(-100, 100, generator=gen)
+    b = torch.empty(kl, device=dev).uniform_(-100, 100, generator=gen)
+    x = torch.empty(kl, device=dev).uniform_(-1, 1, generator=gen)
+    g = torch.empty(nl, device=dev).uniform_(-1, 1, generator=gen)
+    comm = comm_factory()
+    be = GpuBackend()
+
+    def step():
+        op = ShardedOperator(a, b, 1.0, comm, be)
+        y = op.apply(x)
+        xb, ab, bb = op.backward(x, g)
+        return op, (y, xb, ab, bb)
+
+    def barrier():
+        torch.cuda.synchronize()
+        comm.all_gather(torch.zeros(1, device=dev))
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    launches0 = L.kernel_launches()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local if not args.sim else 0, args.clock_interval) as clk:
+        barrier()
+        ev0.record()
+        for _ in range(args.steps):
+            _, outs = step()
+        ev1.record()
+        barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    ms = max(float(v.item()) for v in comm.all_gather(torch.tensor([ms], device=dev)))
+    launches = L.kernel_launches() - launches0
+    y, xb, ab, bb = outs
+    # e2e: the same sharded step from pinned host slices, outputs read back
+    e2e = None
+    if args.e2e:
+        pin = dict(pin_memory=True)
+        hs = [v.cpu().pin_memory() for v in (a, b, x, g)]
+        ho = [torch.empty(v.numel(), dtype=v.dtype, **pin) for v in (y, xb, ab, bb)]
+        dv = [torch.empty_like(v) for v in (a, b, x, g)]
+
+        def e2e_step():
+            for d_, h_ in zip(dv, hs):
+                d_.copy_(h_, non_blocking=True)
+            op = ShardedOperator(dv[0], dv[1], 1.0, comm, be)
+            yy = op.apply(dv[2])
+            outs2 = (yy,) + tuple(op.backward(dv[2], dv[3]))
+            for h_, o_ in zip(ho, outs2):
+                h_.copy_(o_.reshape(-1), non_blocking=True)
+            torch.cuda.synchronize()
+        e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        barrier()
+        sec = (time.perf_counter() - t0) / args.e2e_steps
+        sec = max(float(v.item()) for v in comm.all_gather(torch.tensor([sec], device=dev)))
+        e2e = {"value": n / sec, "unit": UNIT, "ms_per_step": 1000 * sec,
+               "h2d_bytes_per_step": 4 * (n + k + k + n), "d2h_bytes_per_step": 4 * (n + k + n + k),
+               "path": "sharded.ShardedOperator from pinned host slices (H2D) to host outputs (D2H), all ranks"}
+    s = torch.stack(comm.all_gather(torch.stack([ab.double().sum() + bb.double().sum(),
+                                                 ab.double().abs().sum() + bb.double().abs().sum()])))
+    cons = float(s[:, 0].sum().abs() / s[:, 1].sum())
+    if rank == 0:
+        hbm, peak_kind = peaks()
+        value = n / (ms / 1000)
+        step_bytes = step_model_bytes(n, k)
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic: anchors U(-100,100), x and g U(-1,1), t=1; rank r holds the r-th contiguous slice",
+            "config": {"workload": f"C5 LAPLEX fwd+bwd incl. plan build, n=k=2^{args.log2n} total, batch 1",
+                       "n": n, "k": k, "batch": 1, "temperature": 1.0,
+                       "parallelism": f"range-sharded x{world}: value splitters + NCCL all-to-all (a, b, x, g, "
+                                      f"outputs) + all-gather of shard totals" + (" [SIMULATED in-process]" if args.sim else ""),
+                       "l2": "inputs larger than L2"},
+            "gpu_launches": launches,
+            "roofline": None,
+            "step_roofline": {"model": "SURVEY 8(d) fwd+bwd incl. plan: 100n+96k+8n+12k bytes (whole job)",
+                              "bytes": step_bytes, "achieved": round(step_bytes / (ms / 1000) / 1e9, 1),
+                              "peak": hbm * world, "unit": "GB/s",
+                              "frac": round(step_bytes / (ms / 1000) / 1e9 / (hbm * world), 4)},
+            "check": {"conservation_rel": cons},
+            "clocks": clk.summary(),
+            "e2e": e2e,
+        }), flush=True)
+
+
 def run_e2e(args, torch, lib, n, k):
     """Same step through the host-buffer C-ABI: pinned host in, host out."""
     import paper_2605_24584_b200 as L  # noqa: F401
@@ -363,6 +471,8 @@ def main():
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--sim", type=int, default=0,
+                    help="simulate N range shards with threads on one GPU (functional check only)")
     ap.add_argument("--clock-interval", type=float, default=1.0,
                     help="seconds between nvidia-smi samples during the timed region")
     args = ap.parse_args()
@@ -372,16 +482,26 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    dist = None
+    if args.sim > 1:  # N shards as threads on one GPU (functional path check)
+        from paper_2605_24584_b200.sharded import SimComm, SimWorld
+        w = SimWorld(args.sim)
+        ths = [threading.Thread(target=run_sharded, args=(args, r, args.sim, None, lambda r=r: SimComm(w, r)))
+               for r in range(args.sim)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        return
     if world > 1:
         import torch
         import torch.distributed as tdist
+        from paper_2605_24584_b200.sharded import TorchComm
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
         tdist.init_process_group("nccl")
-        dist = tdist
-    run_ours(args, rank, world, dist)
-    if dist is not None:
-        dist.destroy_process_group()
+        run_sharded(args, rank, world, tdist, lambda: TorchComm())
+        tdist.destroy_process_group()
+        return
+    run_ours(args, rank, world, None)
 
 
 if __name__ == "__main__":
