@@ -42,10 +42,12 @@ def kernel_model_bytes(name, n, k, rows=1):
     return {
         "lx_sort_hist": 4 * m2,                       # read raw keys once
         "lx_sort_pass": (12 + 16 + 16 + 16) * m2,     # pass1 r4 w8; passes 2-4 r8 w8
-        # tile aggregates: fwd reads Bh, pos_b, x-stage; bwd reads both sides
-        "lx_tileagg": (12 * k + rows * 0) + (12 * n + 12 * k),
-        # fwd: A, Bh, pos_b, x-stage in; pos_a in, y-stage out
-        "lx_main_fwd": 4 * n + 4 * k + 4 * k + rows * (4 * k + 4 * n) + 4 * n,
+        # payload gather into sorted order + tile aggregates: per payload element read
+        # the sorted anchor, the source index and the (staged) payload, write the
+        # sorted payload.  fwd: x on cols; bwd: g on rows, x on cols
+        "lx_gather_agg": 16 * rows * (k + n + k),
+        # fwd: A, Bh, sorted x in; output index of rows in, y (stage) out
+        "lx_main_fwd": 4 * n + 4 * k + rows * 4 * k + 4 * n + rows * 4 * n,
         # bwd: A, Bh, pos_a, pos_b, g-stage, x-stage in; x_bar, b_bar, a_bar stage out
         "lx_main_bwd": 8 * n + 8 * k + rows * (4 * n + 4 * k + 4 * k) + 4 * n + 4 * k,
         # permutation plan build: read perm, write pos (sequential) and dst (bucket streams)
