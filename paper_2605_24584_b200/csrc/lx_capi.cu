@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <utility>
 #include <mutex>
@@ -22,6 +23,7 @@
 #include "../../include/laplex_c.h"
 #include "lx_common.cuh"
 #include "lx_gram.cuh"
+#include "lx_main.cuh"
 #include "lx_scan.cuh"
 #include "lx_shard.cuh"
 #include "lx_sort.cuh"
@@ -422,17 +424,45 @@ void stage_scatter(const uint32_t* dst, uint32_t m, const R* s1, R* o1, size_t l
     });
 }
 
+// any non-finite entry of v[0, m) sets *bad (host-pointer API validation,
+// run on the device after the upload instead of a host pass over the input)
 template <class R>
 __global__ void finite_check(const R* __restrict__ v, size_t m, int* __restrict__ bad) {
+    constexpr int kV = 16 / sizeof(R);
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    const size_t i0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // v is a pool allocation (256-byte aligned): 16-byte vectors, then the tail
+    const size_t nv = m / kV;
     int b = 0;
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (size_t)gridDim.x * blockDim.x)
-        if (!isfinite(v[i])) b = 1;
-    if (b) atomicOr(bad, 1);
+    for (size_t i = i0; i < nv; i += stride) {
+        if constexpr (kV == 4) {
+            const float4 q = reinterpret_cast<const float4*>(v)[i];
+            b |= !isfinite(q.x) | !isfinite(q.y) | !isfinite(q.z) | !isfinite(q.w);
+        } else {
+            const double2 q = reinterpret_cast<const double2*>(v)[i];
+            b |= !isfinite(q.x) | !isfinite(q.y);
+        }
+    }
+    for (size_t i = nv * kV + i0; i < m; i += stride) b |= !isfinite(v[i]);
+    if (__syncthreads_or(b) && threadIdx.x == 0) atomicOr(bad, 1);
 }
 
 template <class R>
+void launch_finite(const R* v, size_t m, int* bad, cudaStream_t st) {
+    if (!m) return;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const size_t blocks = std::min<size_t>((m + 1023) / 1024, (size_t)sms * 8);
+    launch("finite_check", st, [&] { finite_check<R><<<(unsigned)blocks, 256, 0, st>>>(v, m, bad); });
+}
+
+// ready[s]: optional event the build of side s waits for (host-pointer API:
+// side 1 is still uploading while side 0 sorts).  Non-finite anchors (found by
+// the histogram pass) and phases raise NonFinite after the one synchronisation,
+// in the reference's check order (operator.hpp:88-101).
+template <class R>
 laplex_plan create_plan(const R* a, uint32_t n, const R* b, uint32_t k, double t, const R* phi, const R* psi,
-                        cudaStream_t st) {
+                        cudaStream_t st, const cudaEvent_t* ready = nullptr) {
     init_pool();
     auto core = std::make_shared<Core>();
     core->dtype = sizeof(R) == 8 ? LAPLEX_F64 : LAPLEX_F32;
@@ -440,24 +470,23 @@ laplex_plan create_plan(const R* a, uint32_t n, const R* b, uint32_t k, double t
     core->t = t;
     core->phased = phi != nullptr;
     ck(cudaEventCreateWithFlags(&core->last, cudaEventDisableTiming), "cudaEventCreate");
-    DBuf bad(sizeof(int) * 2, st);
-    ck(cudaMemsetAsync(bad.p, 0, sizeof(int) * 2, st), "memset");
-    build_side<R>(core->side[0], a, n, R(t), phi, bad.as<int>(), st);
-    build_side<R>(core->side[1], b, k, R(t), psi, bad.as<int>(), st);
+    DBuf bad(sizeof(int) * 4, st);
+    ck(cudaMemsetAsync(bad.p, 0, sizeof(int) * 4, st), "memset");
+    if (ready) ck(cudaStreamWaitEvent(st, ready[0], 0), "cudaStreamWaitEvent");
+    build_side<R>(core->side[0], a, n, R(t), phi, bad.as<int>() + 0, st);
+    if (ready) ck(cudaStreamWaitEvent(st, ready[1], 0), "cudaStreamWaitEvent");
+    build_side<R>(core->side[1], b, k, R(t), psi, bad.as<int>() + 1, st);
     if (phi) {
-        launch("finite_check", st, [&] {
-            finite_check<R><<<64, 256, 0, st>>>(phi, n, bad.as<int>() + 1);
-        });
-        launch("finite_check", st, [&] {
-            finite_check<R><<<64, 256, 0, st>>>(psi, k, bad.as<int>() + 1);
-        });
+        launch_finite<R>(phi, n, bad.as<int>() + 2, st);
+        launch_finite<R>(psi, k, bad.as<int>() + 2, st);
     }
     build_partition<R>(*core, 0, st);
-    int hbad[2] = {0, 0};
+    int hbad[4] = {0, 0, 0, 0};
     ck(cudaMemcpyAsync(hbad, bad.p, sizeof(hbad), cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
     ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
-    if (hbad[0]) fail(LAPLEX_E_NON_FINITE, "LaplexOperator: non-finite anchor");
-    if (hbad[1]) fail(LAPLEX_E_NON_FINITE, "LaplexOperator: non-finite phase");
+    if (hbad[0]) fail(LAPLEX_E_NON_FINITE, "LaplexOperator row anchors: non-finite entry");
+    if (hbad[1]) fail(LAPLEX_E_NON_FINITE, "LaplexOperator col anchors: non-finite entry");
+    if (hbad[2]) fail(LAPLEX_E_NON_FINITE, "LaplexOperator phases: non-finite entry");
     ck(cudaEventRecord(core->last, st), "cudaEventRecord");
     auto* p = new laplex_plan_s;
     p->core = core;
@@ -504,13 +533,23 @@ template <class R, int NG, int NX, bool BWD, bool SEQ = false>
 void launch_main(const char* name, const lx::ms::MainArgs<R>& a, cudaStream_t st) {
     using namespace lx::ms;
     constexpr int TPB = MainShape<BWD>::TPB, IPT = MainShape<BWD>::IPT;
-    const size_t smem = sizeof(MainSmem<R, NG, NX, TPB / 32>);
+    auto kern = lx_main<R, NG, NX, BWD, SEQ, TPB, IPT>;
+    const size_t smem = sizeof(MainShared<R, NG + NX, TPB / 32, BWD ? (NG == 2 ? 2 : 1) : 0>);
+    static int per_sm = 0, sms = 0;
     static std::once_flag once;
     std::call_once(once, [&] {
-        cudaFuncSetAttribute(lx_main<R, NG, NX, BWD, SEQ, TPB, IPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TPB, smem);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        if (per_sm < 1) per_sm = 1;
     });
-    launch(name, st, [&] { lx_main<R, NG, NX, BWD, SEQ, TPB, IPT><<<a.T, TPB, smem, st>>>(a); });
+    // persistent: one CTA per resident slot, tiles claimed in order
+    const uint32_t grid = std::max<uint32_t>(1u, std::min<uint32_t>(a.T, (uint32_t)(sms * per_sm)));
+    DBuf ctr(4, st);
+    ck(cudaMemsetAsync(ctr.p, 0, 4, st), "memset");
+    lx::ms::MainArgs<R> b = a;
+    b.tile_ctr = ctr.as<uint32_t>();
+    launch(name, st, [&] { kern<<<grid, TPB, smem, st>>>(b); });
 }
 
 template <class R, int NC>
@@ -733,13 +772,15 @@ struct BwdWork : WorkBase {
 };
 
 template <class R, int NCH>
-std::unique_ptr<BwdWork<R, NCH>> bwd_begin(const View<R>& v, const R* X, const R* G, int rows, cudaStream_t st) {
+std::unique_ptr<BwdWork<R, NCH>> bwd_begin(const View<R>& v, const R* X, const R* G, int rows, cudaStream_t st,
+                                           const std::function<void()>& before_g = {}) {
     constexpr int NC = 2 * NCH;
     auto w = std::make_unique<BwdWork<R, NCH>>(v, rows, st);
     auto& a = w->a;
     a = main_args(v, rows);
-    w->gs = sorted_payload<R, NCH, true, true, true>(v, rows, G, w->sc, 0, a.ldgs, st);
     w->xs = sorted_payload<R, NCH, false, false, true>(v, rows, X, w->sc, NCH, a.ldxs, st);
+    if (before_g) before_g();  // host API: g may still be uploading
+    w->gs = sorted_payload<R, NCH, true, true, true>(v, rows, G, w->sc, 0, a.ldgs, st);
     a.Gs = w->gs.template as<R>();
     a.Xs = w->xs.template as<R>();
     const unsigned gmask = (1u << NCH) - 1u;
@@ -795,8 +836,8 @@ void bwd_end(BwdWork<R, NCH>& w, const R* ext, R* xbar, R* abar, R* bbar, R* phi
 
 template <class R, int NCH>
 void backward_impl(const View<R>& v, const R* X, const R* G, int rows, R* xbar, R* abar, R* bbar, R* phibar,
-                   R* psibar, cudaStream_t st) {
-    auto w = bwd_begin<R, NCH>(v, X, G, rows, st);
+                   R* psibar, cudaStream_t st, const std::function<void()>& before_g) {
+    auto w = bwd_begin<R, NCH>(v, X, G, rows, st, before_g);
     bwd_end<R, NCH>(*w, nullptr, xbar, abar, bbar, phibar, psibar, st);
 }
 
@@ -821,21 +862,22 @@ void do_apply(laplex_plan_s* p, unsigned flags, const R* X, size_t rows, R* Y, c
 
 template <class R>
 void do_backward(laplex_plan_s* p, unsigned flags, const R* X, const R* G, size_t rows, R* xbar, R* abar, R* bbar,
-                 R* phibar, R* psibar, cudaStream_t st) {
+                 R* phibar, R* psibar, cudaStream_t st, const std::function<void()>& before_g = {}) {
     Core& c = *p->core;
     const bool ph = flags & LAPLEX_PHASED;
     if (ph && !c.phased) fail(LAPLEX_E_PHASE_ABSENT, "phased_matvec_vjp: operator has no phases");
     if (!ph && c.phased) fail(LAPLEX_E_PHASE_PRESENT, "matvec_vjp: use phased_matvec_vjp");
     View<R> v = view<R>(c, p->swapped, st);
     if (rows == 0) {
+        if (before_g) before_g();
         ck(cudaMemsetAsync(abar, 0, (size_t)v.n * sizeof(R), st), "memset");
         ck(cudaMemsetAsync(bbar, 0, (size_t)v.k * sizeof(R), st), "memset");
         return;
     }
     if (ph)
-        backward_impl<R, 2>(v, X, G, (int)rows, xbar, abar, bbar, phibar, psibar, st);
+        backward_impl<R, 2>(v, X, G, (int)rows, xbar, abar, bbar, phibar, psibar, st, before_g);
     else
-        backward_impl<R, 1>(v, X, G, (int)rows, xbar, abar, bbar, nullptr, nullptr, st);
+        backward_impl<R, 1>(v, X, G, (int)rows, xbar, abar, bbar, nullptr, nullptr, st, before_g);
     touch(c, st);
 }
 
@@ -1024,13 +1066,61 @@ bool host_finite(const R* v, size_t m) {
     return true;
 }
 
+// Host -> device upload of one host-pointer argument.  The copy runs on the
+// calling thread's upload stream, so the compute stream can start on an
+// earlier argument while this one is in flight; the buffer belongs to (and is
+// freed on) the compute stream, which must wait() before reading it.
+cudaStream_t upload_stream() {
+    thread_local cudaStream_t s = [] {
+        cudaStream_t x = nullptr;
+        ck(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking), "cudaStreamCreate");
+        return x;
+    }();
+    return s;
+}
+
 template <class R>
 struct HostUp {
     DBuf d;
+    cudaEvent_t done = nullptr;
     HostUp(const void* h, size_t count, cudaStream_t st) : d(count * sizeof(R), st) {
-        if (count) ck(cudaMemcpyAsync(d.p, h, count * sizeof(R), cudaMemcpyHostToDevice, st), "H2D");
+        if (!count) return;
+        cudaStream_t up = upload_stream();
+        cudaEvent_t alloc;
+        ck(cudaEventCreateWithFlags(&alloc, cudaEventDisableTiming), "cudaEventCreate");
+        ck(cudaEventRecord(alloc, st), "cudaEventRecord");  // the allocation is ordered on st
+        ck(cudaStreamWaitEvent(up, alloc, 0), "cudaStreamWaitEvent");
+        cudaEventDestroy(alloc);
+        ck(cudaMemcpyAsync(d.p, h, count * sizeof(R), cudaMemcpyHostToDevice, up), "H2D");
+        ck(cudaEventCreateWithFlags(&done, cudaEventDisableTiming), "cudaEventCreate");
+        ck(cudaEventRecord(done, up), "cudaEventRecord");
+    }
+    HostUp(const HostUp&) = delete;
+    HostUp& operator=(const HostUp&) = delete;
+    ~HostUp() {
+        if (done) cudaEventDestroy(done);
+    }
+    void wait(cudaStream_t st) const {
+        if (done) ck(cudaStreamWaitEvent(st, done, 0), "cudaStreamWaitEvent");
     }
     R* get() const { return d.as<R>(); }
+};
+
+// Device flags of the host-pointer API's finiteness checks (one int each).
+struct Flags {
+    DBuf d;
+    int n;
+    Flags(int n_, cudaStream_t st) : d(sizeof(int) * n_, st), n(n_) {
+        ck(cudaMemsetAsync(d.p, 0, sizeof(int) * n_, st), "memset");
+    }
+    int* at(int i) const { return d.as<int>() + i; }
+    // synchronises st; returns the host copy
+    std::vector<int> read(cudaStream_t st) const {
+        std::vector<int> h(n);
+        ck(cudaMemcpyAsync(h.data(), d.p, sizeof(int) * n, cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        return h;
+    }
 };
 
 cudaStream_t host_stream() { return cudaStreamPerThread; }
@@ -1045,22 +1135,50 @@ int dtype_check(int dtype) {
     return dtype;
 }
 
-template <class R>
-void validate_create(const R* a, size_t n, const R* b, size_t k, double t, const R* phi, const R* psi) {
-    // order of operator.hpp:88-101
-    if (n == 0 || k == 0) fail(LAPLEX_E_EMPTY_INPUT, "LaplexOperator: empty anchor set");
-    if (!host_finite(a, n)) fail(LAPLEX_E_NON_FINITE, "LaplexOperator row anchors: non-finite entry");
-    if (!host_finite(b, k)) fail(LAPLEX_E_NON_FINITE, "LaplexOperator col anchors: non-finite entry");
-    const R tr = R(t);
-    if (!(tr > R(0)) || !std::isfinite(tr))
-        fail(LAPLEX_E_NON_FINITE, "LaplexOperator: temperature must be positive and finite");
-    if ((phi == nullptr) != (psi == nullptr))
-        fail(LAPLEX_E_DIMENSION_MISMATCH, "LaplexOperator: phases must be given for both sides");
-    if (phi) {
-        if (!host_finite(phi, n)) fail(LAPLEX_E_NON_FINITE, "LaplexOperator row phases: non-finite entry");
-        if (!host_finite(psi, k)) fail(LAPLEX_E_NON_FINITE, "LaplexOperator col phases: non-finite entry");
+// LaplexOperator checks that need no data, in reference order
+// (operator.hpp:88-101); anchor / phase finiteness is checked on the device.
+struct CreateChecks {
+    int code = 0;
+    const char* msg = nullptr;
+};
+CreateChecks create_checks(double t, bool phi, bool psi) {
+    CreateChecks c;
+    const float tf = (float)t;
+    if (!(t > 0.0) || !std::isfinite(t) || !(tf > 0.0f) || !std::isfinite(tf)) {
+        c.code = LAPLEX_E_NON_FINITE;
+        c.msg = "LaplexOperator: temperature must be positive and finite";
+    } else if (phi != psi) {
+        c.code = LAPLEX_E_DIMENSION_MISMATCH;
+        c.msg = "LaplexOperator: phases must be given for both sides";
     }
+    return c;
+}
+
+template <class R>
+laplex_plan create_from_host(const void* a, size_t n, const void* b, size_t k, double t, const void* phi,
+                             const void* psi, cudaStream_t st) {
+    if (n == 0 || k == 0) fail(LAPLEX_E_EMPTY_INPUT, "LaplexOperator: empty anchor set");
     if (n >= 0x80000000ull || k >= 0x80000000ull) fail(LAPLEX_E_INVALID_SIZE, "n and k must be < 2^31");
+    const CreateChecks cc = create_checks(sizeof(R) == 4 ? (double)(float)t : t, phi != nullptr, psi != nullptr);
+    // upload order a, phi, b, psi: side 0 sorts while side 1 is in flight
+    HostUp<R> da(a, n, st);
+    HostUp<R> dp(phi, (phi && !cc.code) ? n : 0, st);
+    HostUp<R> db(b, k, st);
+    HostUp<R> dq(psi, (psi && !cc.code) ? k : 0, st);
+    if (cc.code) {  // the anchors' finiteness is reported before these
+        Flags f(2, st);
+        da.wait(st);
+        launch_finite<R>(da.get(), n, f.at(0), st);
+        db.wait(st);
+        launch_finite<R>(db.get(), k, f.at(1), st);
+        const auto h = f.read(st);
+        if (h[0]) fail(LAPLEX_E_NON_FINITE, "LaplexOperator row anchors: non-finite entry");
+        if (h[1]) fail(LAPLEX_E_NON_FINITE, "LaplexOperator col anchors: non-finite entry");
+        fail(cc.code, cc.msg);
+    }
+    const cudaEvent_t ready[2] = {phi ? dp.done : da.done, psi ? dq.done : db.done};
+    return create_plan<R>(da.get(), (uint32_t)n, db.get(), (uint32_t)k, t, phi ? dp.get() : nullptr,
+                          psi ? dq.get() : nullptr, st, ready);
 }
 
 }  // namespace
@@ -1132,18 +1250,10 @@ int laplex_plan_create(int dtype, const void* a, size_t n, const void* b, size_t
         dtype_check(dtype);
         cudaStream_t st = host_stream();
         init_pool();
-        if (dtype == LAPLEX_F64) {
-            validate_create<double>((const double*)a, n, (const double*)b, k, t, (const double*)phi,
-                                    (const double*)psi);
-            HostUp<double> da(a, n, st), db(b, k, st), dp(phi, phi ? n : 0, st), dq(psi, psi ? k : 0, st);
-            *out = create_plan<double>(da.get(), (uint32_t)n, db.get(), (uint32_t)k, t, phi ? dp.get() : nullptr,
-                                       psi ? dq.get() : nullptr, st);
-        } else {
-            validate_create<float>((const float*)a, n, (const float*)b, k, t, (const float*)phi, (const float*)psi);
-            HostUp<float> da(a, n, st), db(b, k, st), dp(phi, phi ? n : 0, st), dq(psi, psi ? k : 0, st);
-            *out = create_plan<float>(da.get(), (uint32_t)n, db.get(), (uint32_t)k, t, phi ? dp.get() : nullptr,
-                                      psi ? dq.get() : nullptr, st);
-        }
+        if (dtype == LAPLEX_F64)
+            *out = create_from_host<double>(a, n, b, k, t, phi, psi, st);
+        else
+            *out = create_from_host<float>(a, n, b, k, t, phi, psi, st);
     });
 }
 
@@ -1275,21 +1385,22 @@ int laplex_apply(laplex_plan plan, unsigned flags, const void* X, size_t rows, s
         const size_t in_len = trn ? n : k, out_len = trn ? k : n;
         if (cols != in_len) fail(LAPLEX_E_DIMENSION_MISMATCH, "matvec: x length");
         cudaStream_t st = host_stream();
-        const size_t rs = rsize(c.dtype);
-        if (c.dtype == LAPLEX_F64) {
-            if (!host_finite((const double*)X, rows * cols)) fail(LAPLEX_E_NON_FINITE, "matvec x: non-finite entry");
-            HostUp<double> dx(X, rows * cols, st);
-            DBuf dy(rows * out_len * rs, st);
-            do_apply<double>(plan, flags, dx.get(), rows, dy.as<double>(), st);
-            d2h<double>(Y, dy, rows * out_len, st);
-        } else {
-            if (!host_finite((const float*)X, rows * cols)) fail(LAPLEX_E_NON_FINITE, "matvec x: non-finite entry");
-            HostUp<float> dx(X, rows * cols, st);
-            DBuf dy(rows * out_len * rs, st);
-            do_apply<float>(plan, flags, dx.get(), rows, dy.as<float>(), st);
-            d2h<float>(Y, dy, rows * out_len, st);
-        }
-        ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        auto run = [&](auto zero) {
+            using R = decltype(zero);
+            HostUp<R> dx(X, rows * cols, st);
+            DBuf dy(rows * out_len * sizeof(R), st);
+            Flags f(1, st);
+            dx.wait(st);
+            launch_finite<R>(dx.get(), rows * cols, f.at(0), st);
+            do_apply<R>(plan, flags, dx.get(), rows, dy.as<R>(), st);
+            if (f.read(st)[0]) fail(LAPLEX_E_NON_FINITE, "matvec x: non-finite entry");
+            d2h<R>(Y, dy, rows * out_len, st);
+            ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        };
+        if (c.dtype == LAPLEX_F64)
+            run(0.0);
+        else
+            run(0.0f);
     });
 }
 
@@ -1324,12 +1435,21 @@ int laplex_backward(laplex_plan plan, unsigned flags, const void* X, size_t rows
         const size_t rs = rsize(c.dtype);
         auto run = [&](auto zero) {
             using R = decltype(zero);
-            if (!host_finite((const R*)X, rows * xcols)) fail(LAPLEX_E_NON_FINITE, "matvec_vjp x: non-finite entry");
-            if (!host_finite((const R*)G, rows * gcols)) fail(LAPLEX_E_NON_FINITE, "matvec_vjp g: non-finite entry");
-            HostUp<R> dx(X, rows * k, st), dg(G, rows * n, st);
+            // x first: its gather runs while g is still uploading
+            HostUp<R> dx(X, rows * k, st);
+            HostUp<R> dg(G, rows * n, st);
             DBuf xb(rows * k * rs, st), ab(n * rs, st), bb(k * rs, st), pb(ph ? n * rs : 0, st), qb(ph ? k * rs : 0, st);
+            Flags f(2, st);
+            dx.wait(st);
+            launch_finite<R>(dx.get(), rows * k, f.at(0), st);
             do_backward<R>(plan, flags, dx.get(), dg.get(), rows, xb.as<R>(), ab.as<R>(), bb.as<R>(), pb.as<R>(),
-                           qb.as<R>(), st);
+                           qb.as<R>(), st, [&] {
+                               dg.wait(st);
+                               launch_finite<R>(dg.get(), rows * n, f.at(1), st);
+                           });
+            const auto h = f.read(st);
+            if (h[0]) fail(LAPLEX_E_NON_FINITE, "matvec_vjp x: non-finite entry");
+            if (h[1]) fail(LAPLEX_E_NON_FINITE, "matvec_vjp g: non-finite entry");
             d2h<R>(x_bar, xb, rows * k, st);
             d2h<R>(a_bar, ab, n, st);
             d2h<R>(b_bar, bb, k, st);

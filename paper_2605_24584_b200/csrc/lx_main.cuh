@@ -1,0 +1,715 @@
+// lx_main.cuh -- the main merged-tile scan pass (forward, transpose, backward,
+// single-sequence scans) as a persistent, double-buffered sm_100a kernel.
+//
+// Reference algorithm being replaced (paths under /root/reference/proj):
+//   matvec branch A/B           include/laplex/operator.hpp:319-369
+//   prefix/suffix_decay_scan    include/laplex/scan.hpp:50-73
+//   row/col split sums (VJP)    include/laplex/gradients.hpp:33-103,110-135
+//
+// One CTA per SM slot walks the merge tiles t = blockIdx.x, +gridDim.x, ...
+// Each tile's inputs (the two anchor ranges, the output-index ranges and the
+// row-0 payload ranges) arrive by TMA bulk copy into one of two shared-memory
+// stages; the copy for the CTA's next tile is issued before the current tile
+// is computed, so the loads overlap the scan.
+//
+// Per tile and batch row (merged order, rows first on ties; see lx_scan.cuh):
+//   1. merge the two anchor ranges (merge path), IPT consecutive merged
+//      elements per thread; anchors, kinds and payloads go to registers;
+//   2. thread-local totals of the prefix and suffix recurrences (+ strict);
+//   3. warp Kogge-Stone over the thread totals, block totals over warps in
+//      every warp (one barrier), tile carries and shard carries folded in:
+//      each thread gets its exclusive carry from the left and from the right;
+//   4. the thread re-runs its IPT-element recurrences seeded with those
+//      carries (suffix first, recording what the outputs need, then prefix)
+//      and writes each output into a shared-memory staging row indexed by
+//      the element's side-local index;
+//   5. the staged outputs are stored side by side (one side at a time, no
+//      divergence) to perm / plan position.
+// Numerics: every carry that crosses a thread is applied as one exp of an
+// anchor difference; within a thread's IPT consecutive elements carries are
+// products of per-step decays (the exception DESIGN.md section 4 allows).
+#pragma once
+
+#include "lx_scan.cuh"
+
+namespace lx {
+namespace ms {
+
+template <class R>
+struct MainStage {
+    static constexpr int kPad = 16 / sizeof(R);
+    unsigned long long bar;   // anchors + output indices
+    unsigned long long barp;  // payloads (one completion per batch row)
+    uint32_t t;  // tile index staged here (>= T: no more tiles)
+    uint32_t a0, b0;
+    int na, nb;
+    R s_last, SL, SR;  // tile's last anchor, previous tile's last, next tile's first
+    alignas(16) R anch[kTile + 4 * kPad];   // A range at [offA], B range at [baseB + offB]
+    alignas(16) R pay[kTile + 4 * kPad];    // row payloads, same layout
+    alignas(16) uint32_t oidx[kTile + 16];  // output index ranges: A at [offIA], B at [baseIB + offIB]
+};
+
+template <class R, int NC, int NW, int NACC>
+struct MainShared {
+    MainStage<R> st[2];
+    // backward: a_bar at [li], b_bar at [na + li] (and phi_bar / psi_bar),
+    // accumulated over the batch rows by the element's owning thread
+    R acc[NACC > 0 ? NACC : 1][kTile];
+    R wsl[NW], wsf[NW];                 // warp last / first anchors (per tile)
+    R pv[NC][NW], pw[NC][NW];           // warp prefix totals (inclusive, strict)
+    R qv[NC][NW], qw[NC][NW];           // warp suffix totals
+};
+
+// Geometry of one staged tile, derived from its header.
+template <class R>
+struct TileGeom {
+    uint32_t a0, b0;
+    int na, nb;
+    int offA, baseB, offIA, baseIB;  // element offsets inside anch/pay and oidx
+    uint32_t bytesA, bytesB, ibytesA, ibytesB;
+    uint32_t a0al, b0al, a0i, b0i;
+    __device__ __forceinline__ void init(uint32_t a0_, uint32_t b0_, int na_, int nb_, bool outA, bool outB) {
+        constexpr int kPad = 16 / sizeof(R);
+        a0 = a0_;
+        b0 = b0_;
+        na = na_;
+        nb = nb_;
+        a0al = a0 & ~uint32_t(kPad - 1);
+        b0al = b0 & ~uint32_t(kPad - 1);
+        offA = (int)(a0 - a0al);
+        const int offB = (int)(b0 - b0al);
+        bytesA = na ? (uint32_t)(((offA + na + kPad - 1) / kPad) * 16) : 0u;
+        bytesB = nb ? (uint32_t)(((offB + nb + kPad - 1) / kPad) * 16) : 0u;
+        baseB = (int)(bytesA / sizeof(R)) + offB;
+        a0i = a0 & ~3u;
+        b0i = b0 & ~3u;
+        offIA = (int)(a0 - a0i);
+        const int offIB = (int)(b0 - b0i);
+        ibytesA = (outA && na) ? (uint32_t)(((offIA + na + 3) / 4) * 16) : 0u;
+        ibytesB = (outB && nb) ? (uint32_t)(((offIB + nb + 3) / 4) * 16) : 0u;
+        baseIB = (int)(ibytesA / 4) + offIB;
+    }
+};
+
+// Thread 0: stage tile t (anchors, output indices, row-0 payloads) by TMA.
+template <class R, bool SEQ, bool PAY_A, bool PAY_B, bool OUT_A, bool OUT_B>
+__device__ __forceinline__ void issue_tile(MainStage<R>& S, const MainArgs<R>& p, uint32_t t, const TileDesc<R>& dt,
+                                           const TileDesc<R>& dn, R SL) {
+    S.t = t;
+    if (t >= p.T) return;
+    TileGeom<R> g;
+    g.init(dt.a0, dt.b0, (int)(dn.a0 - dt.a0), (int)(dn.b0 - dt.b0), OUT_A, OUT_B);
+    S.a0 = dt.a0;
+    S.b0 = dt.b0;
+    S.na = g.na;
+    S.nb = g.nb;
+    S.s_last = dt.s_last;
+    S.SL = SL;
+    S.SR = dn.s_first;
+    mbar_expect_tx(&S.bar, g.bytesA + g.bytesB + g.ibytesA + g.ibytesB);
+    if (g.bytesA) bulk_g2s(S.anch, p.A + g.a0al, g.bytesA, &S.bar);
+    if (g.bytesB) bulk_g2s(S.anch + (g.bytesA / sizeof(R)), p.B + g.b0al, g.bytesB, &S.bar);
+    if (g.ibytesA) bulk_g2s(S.oidx, p.perm_a + g.a0i, g.ibytesA, &S.bar);
+    if (g.ibytesB) bulk_g2s(S.oidx + g.ibytesA / 4, p.perm_b + g.b0i, g.ibytesB, &S.bar);
+    const R* srcA = SEQ ? p.Xs : p.Gs;
+    mbar_expect_tx(&S.barp, (PAY_A ? g.bytesA : 0u) + (PAY_B ? g.bytesB : 0u));
+    if (PAY_A && g.bytesA) bulk_g2s(S.pay, srcA + g.a0al, g.bytesA, &S.barp);
+    if (PAY_B && g.bytesB) bulk_g2s(S.pay + (g.bytesA / sizeof(R)), p.Xs + g.b0al, g.bytesB, &S.barp);
+}
+
+// Channel layout: g channels first (c < NG), then x channels.  Strict prefix
+// variants for g channels and strict suffix variants for x channels, in the
+// backward (BWD) configuration only.  SEQ: one x channel carried by rows.
+template <class R, int NG, int NX, bool BWD, bool SEQ, int TPB, int IPT>
+#ifndef LX_MAIN_CTAS
+#define LX_MAIN_CTAS 768
+#endif
+#ifndef LX_BWD_CTAS
+#define LX_BWD_CTAS 512
+#endif
+__global__ void __launch_bounds__(TPB, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS : LX_MAIN_CTAS) / TPB : 1) lx_main(MainArgs<R> p) {
+    static_assert(TPB * IPT == kTile, "a CTA covers one merge tile");
+    constexpr int NW = TPB / 32;
+    static_assert(NW <= 32 && (NW & (NW - 1)) == 0, "warps per CTA: power of two");
+    constexpr int LOGW = NW <= 1 ? 0 : NW <= 2 ? 1 : NW <= 4 ? 2 : NW <= 8 ? 3 : NW <= 16 ? 4 : 5;
+    using C = Ch<NG, NX, BWD>;
+    constexpr int NC = C::NC;
+    constexpr bool PHASED = (NG == 2 || NX == 2);
+    constexpr int NP = PHASED ? 2 : 1;  // modulated payload channels per element
+    constexpr bool PAY_A = SEQ || NG > 0;
+    constexpr bool PAY_B = !SEQ && NX > 0;
+    constexpr bool OUT_A = !SEQ && (BWD || NX > 0);  // row-side outputs
+    constexpr bool OUT_B = !SEQ && NG > 0;           // col-side outputs
+    // suffix values recorded per element for the outputs
+    constexpr int KS = SEQ ? 1 : (!BWD ? (NG > 0 ? NG : NX) : (PHASED ? 4 : 1));
+    constexpr int NACC = BWD ? (PHASED ? 2 : 1) : 0;
+    using SM = MainShared<R, NC, NW, NACC>;
+    extern __shared__ __align__(16) unsigned char smem_main[];
+    SM& sm = *reinterpret_cast<SM*>(smem_main);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t T = p.T, G = gridDim.x;
+    const int rows = p.rows;
+    const int ext_flags = p.ext ? (int)p.ext[2] : 0;
+    const bool has_ext_p = ext_flags & 1, has_ext_q = ext_flags & 2;
+    const R ext_pa = has_ext_p ? p.ext[0] : R(0), ext_qa = has_ext_q ? p.ext[1] : R(0);
+    const R* ext_pv = p.ext ? p.ext + 3 : nullptr;
+    const R* ext_qv = p.ext ? p.ext + 3 + (size_t)2 * NC * rows : nullptr;
+    const R* cphi = p.cphi;
+    const R* sphi = p.sphi;
+    const R* cpsi = p.cpsi;
+    const R* spsi = p.spsi;
+
+    // ---- tile schedule ----
+    // Tiles are claimed in increasing order from a global counter, so the
+    // tiles in flight stay a compact window of the merged sequence (the
+    // staged output writes of neighbouring tiles then combine in L2).  Thread
+    // 0 runs the claim two tiles ahead: claim (iteration i) -> descriptor
+    // loads (i+1) -> TMA issue (i+2), so none of the latencies is exposed.
+    uint32_t tn1 = 0, tn2 = 0;  // thread 0: next tile (descriptors loaded), the one after (claimed)
+    TileDesc<R> nd0, nd1;
+    R nsl = R(0);
+    auto load_desc = [&](uint32_t tt) {
+        if (tt < T) {
+            nd0 = p.desc[tt];
+            nd1 = p.desc[tt + 1];
+            nsl = tt > 0 ? p.s_last[tt - 1] : R(0);
+        }
+    };
+    if (tid == 0) {
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&sm.st[s].bar, 1);
+            mbar_init(&sm.st[s].barp, 1);
+        }
+        fence_mbar_init();
+        const uint32_t t0 = atomicAdd(p.tile_ctr, 1u);
+        load_desc(t0);
+        issue_tile<R, SEQ, PAY_A, PAY_B, OUT_A, OUT_B>(sm.st[0], p, t0, nd0, nd1, nsl);
+        tn1 = atomicAdd(p.tile_ctr, 1u);
+        load_desc(tn1);
+        tn2 = atomicAdd(p.tile_ctr, 1u);
+    }
+    __syncthreads();
+
+    for (int it = 0;; ++it) {
+        const int sidx = it & 1;
+        MainStage<R>& S = sm.st[sidx];
+        const uint32_t t = S.t;
+        if (t >= T) break;
+        // ---- stage the CTA's next tile into the other buffer ----
+        if (tid == 0) {
+            issue_tile<R, SEQ, PAY_A, PAY_B, OUT_A, OUT_B>(sm.st[sidx ^ 1], p, tn1, nd0, nd1, nsl);
+            if (tn1 < T) {
+                tn1 = tn2;
+                load_desc(tn1);
+                if (tn1 < T) tn2 = atomicAdd(p.tile_ctr, 1u);
+            }
+        }
+        TileGeom<R> g;
+        g.init(S.a0, S.b0, S.na, S.nb, OUT_A, OUT_B);
+        const int na = g.na, nb = g.nb, len = na + nb;
+        const R s_end = S.s_last;
+        const bool hl = t > 0 || has_ext_p, hr = t + 1 < T || has_ext_q;
+        const R SL = t > 0 ? S.SL : ext_pa;
+        const R SR = t + 1 < T ? S.SR : ext_qa;
+        const uint32_t use = (uint32_t)(it >> 1);  // completions of this stage's barriers so far
+        mbar_wait(&S.bar, use & 1u);
+        const R* sA = S.anch + g.offA;
+        const R* sB = S.anch + g.baseB;
+        const R* pA = S.pay + g.offA;
+        const R* pB = S.pay + g.baseB;
+        const uint32_t* iA = S.oidx + g.offIA;
+        const uint32_t* iB = S.oidx + g.baseIB;
+
+        // ---- merge: anchors and kinds of this thread's IPT elements ----
+        R s[IPT];
+        unsigned rowm = 0;  // bit q: element q is a row
+        int ia0, ib0, nval;
+        {
+            const int dd = min(tid * IPT, len);
+            nval = min(IPT, len - dd);
+            int ia = merge_path<true, R, int>(sA, na, sB, nb, dd);
+            int ib = dd - ia;
+            ia0 = ia;
+            ib0 = ib;
+            const R kInf = R(__int_as_float(0x7f800000));
+            R av = ia < na ? sA[ia] : kInf, bv = ib < nb ? sB[ib] : kInf;
+            // branch-free: one compare, one shared load per element (an
+            // exhausted side reads as +inf; anchors are finite)
+#pragma unroll
+            for (int q = 0; q < IPT; ++q) {
+                const bool takeA = av <= bv;
+                s[q] = takeA ? av : bv;
+                rowm |= (unsigned)takeA << q;
+                ia += takeA;
+                ib += !takeA;
+                const int ni = takeA ? ia : ib;
+                const int lim = takeA ? na : nb;
+                const R* base = takeA ? sA : sB;
+                const R nx = ni < lim ? base[ni] : kInf;
+                av = takeA ? nx : av;
+                bv = takeA ? bv : nx;
+            }
+#pragma unroll
+            for (int q = 0; q < IPT; ++q)
+                if (q >= nval) s[q] = s_end;
+        }
+        const unsigned valm = (1u << nval) - 1u;
+
+        // ---- row-independent geometry: every exp is taken from an anchor difference ----
+        R E[IPT];  // E[q] = exp(s[q-1] - s[q])
+        E[0] = R(0);
+#pragma unroll
+        for (int q = 1; q < IPT; ++q) E[q] = xexp(xsub(s[q - 1], s[q]));
+        unsigned ltE = 0;  // bit q: s[q-1] < s[q]
+#pragma unroll
+        for (int q = 1; q < IPT; ++q)
+            if (s[q - 1] < s[q]) ltE |= 1u << q;
+        const R sl = s[IPT - 1], sf = s[0];
+        if (lane == 31) sm.wsl[warp] = sl;
+        if (lane == 0) sm.wsf[warp] = sf;
+        const R S1 = shfl_up(sl, 1);     // previous lane's last anchor
+        const R S1q = shfl_down(sf, 1);  // next lane's first anchor
+
+        const bool first_t = tid == 0, last_t = tid == TPB - 1;
+
+        for (int r = 0; r < rows; ++r) {
+            // tile carries of this row, combined with the external shard carries:
+            // ext (+) tiles<t  and  tiles>t (+) ext
+            R cpv[NC], cps[NC], cqv[NC], cqs[NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const size_t sl0 = ((size_t)(2 * c) * rows + r), sl1 = ((size_t)(2 * c + 1) * rows + r);
+                cpv[c] = t > 0 ? p.cp[sl0 * T + t - 1] : R(0);
+                cps[c] = (t > 0 && C::pst(c)) ? p.cp[sl1 * T + t - 1] : R(0);
+                cqv[c] = t + 1 < T ? p.cq[sl0 * T + t + 1] : R(0);
+                cqs[c] = (t + 1 < T && C::qst(c)) ? p.cq[sl1 * T + t + 1] : R(0);
+                if (has_ext_p) {
+                    const R ev = ext_pv[sl0], es = C::pst(c) ? ext_pv[sl1] : R(0);
+                    if (t > 0) {  // (ext_anchor, ev, es) then (SL, cpv, cps)
+                        const R e = xexp(xsub(ext_pa, SL));
+                        if (C::pst(c)) cps[c] = xadd(cps[c], ext_pa < SL ? xmul(e, ev) : es);
+                        cpv[c] = xfma(e, ev, cpv[c]);
+                    } else {
+                        cpv[c] = ev;
+                        cps[c] = es;
+                    }
+                }
+                if (has_ext_q) {
+                    const R ev = ext_qv[sl0], es = C::qst(c) ? ext_qv[sl1] : R(0);
+                    if (t + 1 < T) {  // (SR, cqv, cqs) then (ext_anchor, ev, es)
+                        const R e = xexp(xsub(SR, ext_qa));
+                        if (C::qst(c)) cqs[c] = xadd(cqs[c], SR < ext_qa ? xmul(e, ev) : es);
+                        cqv[c] = xfma(e, ev, cqv[c]);
+                    } else {
+                        cqv[c] = ev;
+                        cqs[c] = es;
+                    }
+                }
+            }
+            mbar_wait(&S.barp, (use * (uint32_t)rows + (uint32_t)r) & 1u);
+            // ---- payloads: modulated channel values of each element ----
+            R pay[NP][IPT];
+            R raw[PHASED ? IPT : 1];
+            {
+                int ia = ia0, ib = ib0;
+#pragma unroll
+                for (int q = 0; q < IPT; ++q) {
+                    const bool isr = (rowm >> q) & 1, val = (valm >> q) & 1;
+                    const int li = isr ? ia : ib;
+                    ia += isr;
+                    ib += !isr;
+                    R v = R(0);
+                    if constexpr (PAY_A && PAY_B) {
+                        v = val ? (isr ? pA : pB)[li] : R(0);
+                    } else if constexpr (PAY_A) {
+                        v = (val && isr) ? pA[li] : R(0);
+                    } else {
+                        v = (val && !isr) ? pB[li] : R(0);
+                    }
+                    R m0 = R(1), m1 = R(0);
+                    if constexpr (NG == 2) {
+                        if (val && isr) {
+                            m0 = cphi[g.a0 + li];
+                            m1 = sphi[g.a0 + li];
+                        }
+                    }
+                    if constexpr (NX == 2) {
+                        if (val && !isr) {
+                            m0 = cpsi[g.b0 + li];
+                            m1 = spsi[g.b0 + li];
+                        }
+                    }
+                    if constexpr (PHASED) {
+                        raw[q] = v;
+                        pay[0][q] = xmul(m0, v);
+                        pay[1][q] = xmul(m1, v);
+                    } else {
+                        pay[0][q] = v;
+                    }
+                }
+            }
+            // payload of channel c at element q
+            auto chp = [&](int c, int q) -> R {
+                const bool isr = (rowm >> q) & 1;
+                if constexpr (SEQ) {
+                    return pay[0][q];
+                } else {
+                    if (c < NG) return isr ? pay[NG == 2 ? c : 0][q] : R(0);
+                    return isr ? R(0) : pay[NX == 2 ? c - NG : 0][q];
+                }
+            };
+
+            // ---- 2. thread-local totals ----
+            R v[NC], w[NC], vq[NC], wq[NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                R a = chp(c, 0), b = R(0);
+#pragma unroll
+                for (int q = 1; q < IPT; ++q) {
+                    if (C::pst(c)) b = ((ltE >> q) & 1) ? xmul(E[q], a) : b;
+                    a = xfma(E[q], a, chp(c, q));
+                }
+                v[c] = a;
+                w[c] = b;
+                R u = chp(c, IPT - 1), z = R(0);
+#pragma unroll
+                for (int q = IPT - 2; q >= 0; --q) {
+                    if (C::qst(c)) z = ((ltE >> (q + 1)) & 1) ? xmul(E[q + 1], u) : z;
+                    u = xfma(E[q + 1], u, chp(c, q));
+                }
+                vq[c] = u;
+                wq[c] = z;
+            }
+            // ---- 3a. warp Kogge-Stone (prefix from lower lanes, suffix from upper) ----
+            // (geometry recomputed per batch row: short live ranges beat reuse)
+            R eP[5], eQ[5];
+            unsigned ltP = 0, ltQ = 0;
+#pragma unroll
+            for (int j = 0; j < 5; ++j) {
+                const int off = 1 << j;
+                const R so = shfl_up(sl, off);
+                const R sq = shfl_down(sf, off);
+                eP[j] = lane >= off ? xexp(xsub(so, sl)) : R(0);
+                if (lane >= off && so < sl) ltP |= 1u << j;
+                eQ[j] = lane + off < 32 ? xexp(xsub(sf, sq)) : R(0);
+                if (lane + off < 32 && sf < sq) ltQ |= 1u << j;
+            }
+#pragma unroll
+            for (int j = 0; j < 5; ++j) {
+                const int off = 1 << j;
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    const R vo = shfl_up(v[c], off);
+                    if (C::pst(c)) {
+                        const R wo = shfl_up(w[c], off);
+                        if (lane >= off) w[c] = xadd(w[c], ((ltP >> j) & 1) ? xmul(eP[j], vo) : wo);
+                    }
+                    if (lane >= off) v[c] = xfma(eP[j], vo, v[c]);
+                    const R uo = shfl_down(vq[c], off);
+                    if (C::qst(c)) {
+                        const R zo = shfl_down(wq[c], off);
+                        if (lane + off < 32) wq[c] = xadd(wq[c], ((ltQ >> j) & 1) ? xmul(eQ[j], uo) : zo);
+                    }
+                    if (lane + off < 32) vq[c] = xfma(eQ[j], uo, vq[c]);
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                if (lane == 31) {
+                    sm.pv[c][warp] = v[c];
+                    sm.pw[c][warp] = w[c];
+                }
+                if (lane == 0) {
+                    sm.qv[c][warp] = vq[c];
+                    sm.qw[c][warp] = wq[c];
+                }
+            }
+            __syncthreads();  // (A) warp totals; every merge of this tile is done
+            if (tid == 0 && r + 1 < rows) {  // next batch row's payloads into this stage
+                const R* srcA = SEQ ? p.Xs : p.Gs;
+                const size_t ldA = SEQ ? p.ldxs : p.ldgs;
+                mbar_expect_tx(&S.barp, (PAY_A ? g.bytesA : 0u) + (PAY_B ? g.bytesB : 0u));
+                if (PAY_A && g.bytesA) bulk_g2s(S.pay, srcA + (size_t)(r + 1) * ldA + g.a0al, g.bytesA, &S.barp);
+                if (PAY_B && g.bytesB)
+                    bulk_g2s(S.pay + (g.bytesA / sizeof(R)), p.Xs + (size_t)(r + 1) * p.ldxs + g.b0al, g.bytesB,
+                             &S.barp);
+            }
+            // block-level geometry (warp anchors stay in shared memory for the whole tile)
+            R eBP[LOGW > 0 ? LOGW : 1], eBQ[LOGW > 0 ? LOGW : 1];
+            unsigned ltBP = 0, ltBQ = 0;
+            {
+                const R wl = lane < NW ? sm.wsl[lane] : sm.wsl[NW - 1];
+                const R wf = lane < NW ? sm.wsf[lane] : sm.wsf[NW - 1];
+#pragma unroll
+                for (int j = 0; j < LOGW; ++j) {
+                    const int off = 1 << j;
+                    const R so = shfl_up(wl, off);
+                    const R sq = shfl_down(wf, off);
+                    eBP[j] = lane >= off ? xexp(xsub(so, wl)) : R(0);
+                    if (lane >= off && so < wl) ltBP |= 1u << j;
+                    eBQ[j] = lane + off < NW ? xexp(xsub(wf, sq)) : R(0);
+                    if (lane + off < NW && wf < sq) ltBQ |= 1u << j;
+                }
+            }
+            // thread-exclusive anchors: the first thread's left neighbour is the
+            // previous tile's last element (SL), the last thread's right
+            // neighbour is the next tile's first element (SR)
+            const R SW = warp > 0 ? sm.wsl[warp - 1] : sf;       // previous warp's last anchor
+            const R SWq = warp < NW - 1 ? sm.wsf[warp + 1] : sl;  // next warp's first anchor
+            const R eTW = (lane > 0 && warp > 0) ? xexp(xsub(SW, S1)) : R(0);
+            const bool ltTW = SW < S1;
+            const R eTWq = (lane < 31 && warp < NW - 1) ? xexp(xsub(S1q, SWq)) : R(0);
+            const bool ltTWq = S1q < SWq;
+            const R SE = first_t ? SL : (lane > 0 ? S1 : SW);
+            const R SEq = last_t ? SR : (lane < 31 ? S1q : SWq);
+            const bool hasP = first_t ? hl : true;
+            const bool hasQ = last_t ? hr : true;
+            const R eTL = (!first_t && hl) ? xexp(xsub(SL, SE)) : R(0);
+            const bool ltTL = SL < SE;
+            const R eTR = (!last_t && hr) ? xexp(xsub(SEq, SR)) : R(0);
+            const bool ltTR = SEq < SR;
+            const R eL0 = hasP ? xexp(xsub(SE, sf)) : R(0);
+            const bool ltL0 = SE < sf;
+            const R eRq = hasQ ? xexp(xsub(sl, SEq)) : R(0);
+            const bool ltRq = sl < SEq;
+            // ---- 3b. block totals over warps (every warp), exclusive per warp ----
+            R XV[NC], XW[NC], YV[NC], YW[NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                R bv = lane < NW ? sm.pv[c][lane] : R(0);
+                R bw = lane < NW ? sm.pw[c][lane] : R(0);
+                R cv = lane < NW ? sm.qv[c][lane] : R(0);
+                R cw = lane < NW ? sm.qw[c][lane] : R(0);
+#pragma unroll
+                for (int j = 0; j < LOGW; ++j) {
+                    const int off = 1 << j;
+                    const R vo = shfl_up(bv, off);
+                    const R wo = shfl_up(bw, off);
+                    const R vqo = shfl_down(cv, off);
+                    const R wqo = shfl_down(cw, off);
+                    if (lane >= off) {
+                        if (C::pst(c)) bw = xadd(bw, ((ltBP >> j) & 1) ? xmul(eBP[j], vo) : wo);
+                        bv = xfma(eBP[j], vo, bv);
+                    }
+                    if (lane + off < NW) {
+                        if (C::qst(c)) cw = xadd(cw, ((ltBQ >> j) & 1) ? xmul(eBQ[j], vqo) : wqo);
+                        cv = xfma(eBQ[j], vqo, cv);
+                    }
+                }
+                const int lp = warp > 0 ? warp - 1 : 0, lq = warp < NW - 1 ? warp + 1 : NW - 1;
+                XV[c] = __shfl_sync(FULL, bv, lp);
+                XW[c] = __shfl_sync(FULL, bw, lp);
+                YV[c] = __shfl_sync(FULL, cv, lq);
+                YW[c] = __shfl_sync(FULL, cw, lq);
+            }
+            // ---- 3c. thread-exclusive carries (+ tile carries) ----
+            R VE[NC], WE[NC], VEq[NC], WEq[NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const R V1 = shfl_up(v[c], 1), W1 = shfl_up(w[c], 1);
+                const R V1q = shfl_down(vq[c], 1), W1q = shfl_down(wq[c], 1);
+                R a = R(0), b = R(0), aq = R(0), bq = R(0);
+                if (first_t) {
+                    a = cpv[c];
+                    b = cps[c];
+                } else {
+                    if (lane > 0) {
+                        a = V1;
+                        b = W1;
+                        if (warp > 0) {
+                            if (C::pst(c)) b = xadd(W1, ltTW ? xmul(eTW, XV[c]) : XW[c]);
+                            a = xfma(eTW, XV[c], V1);
+                        }
+                    } else {
+                        a = XV[c];
+                        b = XW[c];
+                    }
+                    if (hl) {  // previous tiles, anchored at SL <= SE
+                        if (C::pst(c)) b = xadd(b, ltTL ? xmul(eTL, cpv[c]) : cps[c]);
+                        a = xfma(eTL, cpv[c], a);
+                    }
+                }
+                if (last_t) {
+                    aq = cqv[c];
+                    bq = cqs[c];
+                } else {
+                    if (lane < 31) {
+                        aq = V1q;
+                        bq = W1q;
+                        if (warp < NW - 1) {
+                            if (C::qst(c)) bq = xadd(W1q, ltTWq ? xmul(eTWq, YV[c]) : YW[c]);
+                            aq = xfma(eTWq, YV[c], V1q);
+                        }
+                    } else {
+                        aq = YV[c];
+                        bq = YW[c];
+                    }
+                    if (hr) {  // following tiles, anchored at SR >= SEq
+                        if (C::qst(c)) bq = xadd(bq, ltTR ? xmul(eTR, cqv[c]) : cqs[c]);
+                        aq = xfma(eTR, cqv[c], aq);
+                    }
+                }
+                VE[c] = a;
+                WE[c] = b;
+                VEq[c] = aq;
+                WEq[c] = bq;
+            }
+
+            // ---- 4a. suffix re-scan seeded with the right carry; record what outputs need ----
+            R os[KS][IPT];
+            {
+                R u[NC], z[NC];
+#pragma unroll
+                for (int q = IPT - 1; q >= 0; --q) {
+                    const R e = q == IPT - 1 ? eRq : E[q + 1];
+                    const bool lt = q == IPT - 1 ? ltRq : (bool)((ltE >> (q + 1)) & 1);
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) {
+                        const R prevu = q == IPT - 1 ? VEq[c] : u[c];
+                        if (C::qst(c)) z[c] = lt ? xmul(e, prevu) : (q == IPT - 1 ? WEq[c] : z[c]);
+                        u[c] = xfma(e, prevu, chp(c, q));
+                    }
+                    const bool isr = (rowm >> q) & 1;
+                    if constexpr (SEQ) {
+                        os[0][q] = u[0];
+                    } else if constexpr (!BWD) {
+                        if constexpr (NG > 0) {
+#pragma unroll
+                            for (int c = 0; c < NG; ++c) os[c][q] = u[c];
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < NX; ++c) os[c][q] = u[c];
+                        }
+                    } else if constexpr (!PHASED) {
+                        os[0][q] = isr ? z[1] : u[0];  // rows: strict suffix of x; cols: suffix of g
+                    } else {
+                        // rows: Q and strict Q of the two x channels; cols: Q of the two g channels
+                        os[0][q] = isr ? u[2] : u[0];
+                        os[1][q] = isr ? u[3] : u[1];
+                        os[2][q] = z[2];
+                        os[3][q] = z[3];
+                    }
+                }
+            }
+            // ---- 4b. prefix re-scan seeded with the left carry; outputs ----
+            R* stg = S.anch;  // staging row (anchors are no longer needed after (A))
+            {
+                R a[NC], b[NC];
+                int ia = ia0, ib = ib0;
+#pragma unroll
+                for (int q = 0; q < IPT; ++q) {
+                    const R e = q == 0 ? eL0 : E[q];
+                    const bool lt = q == 0 ? ltL0 : (bool)((ltE >> q) & 1);
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) {
+                        const R preva = q == 0 ? VE[c] : a[c];
+                        if (C::pst(c)) b[c] = lt ? xmul(e, preva) : (q == 0 ? WE[c] : b[c]);
+                        a[c] = xfma(e, preva, chp(c, q));
+                    }
+                    if (!((valm >> q) & 1)) continue;
+                    const bool isr = (rowm >> q) & 1;
+                    // backward accumulators of this element (shared memory, summed over rows)
+                    R* acp1 = &sm.acc[0][isr ? ia : na + ib];
+                    R* acp2 = &sm.acc[NACC > 1 ? 1 : 0][isr ? ia : na + ib];
+                    R acc1 = R(0), acc2 = R(0);
+                    if constexpr (BWD) {
+                        if (r > 0) {
+                            acc1 = *acp1;
+                            if constexpr (PHASED) acc2 = *acp2;
+                        }
+                    }
+                    if constexpr (SEQ) {
+                        const uint32_t i = g.a0 + ia;
+                        p.pre[(size_t)r * p.n + i] = a[0];
+                        p.suf[(size_t)r * p.n + i] = os[0][q];
+                        ++ia;
+                    } else if (isr) {
+                        const int li = ia++;
+                        if constexpr (!BWD && NX > 0) {
+                            R out = xadd(a[0], os[0][q]);
+                            if constexpr (NX == 2) {
+                                const uint32_t i = g.a0 + li;
+                                out = xadd(xmul(cphi[i], out), xmul(sphi[i], xadd(a[1], os[1][q])));
+                            }
+                            stg[li] = out;
+                        } else if constexpr (BWD) {
+                            if constexpr (!PHASED) {
+                                const R gg = pay[0][q];
+                                acc1 = xfma(xmul(gg, p.inv_t), xsub(os[0][q], a[1]), acc1);
+                            } else {
+                                const uint32_t i = g.a0 + li;
+                                const R gg = raw[q];
+                                const R m0 = cphi[i], m1 = sphi[i];
+                                const R in0 = xsub(os[2][q], a[NG]);  // sum_{b>a} - sum_{b<a}
+                                const R in1 = xsub(os[3][q], a[NG + 1]);
+                                acc1 = xfma(xmul(xmul(m0, gg), p.inv_t), in0, acc1);
+                                acc1 = xfma(xmul(xmul(m1, gg), p.inv_t), in1, acc1);
+                                const R p0 = xadd(a[NG], os[0][q]), p1 = xadd(a[NG + 1], os[1][q]);
+                                acc2 = xfma(gg, xadd(xmul(-m1, p0), xmul(m0, p1)), acc2);
+                            }
+                        }
+                    } else {
+                        const int li = ib++;
+                        if constexpr (NG > 0) {
+                            const R xb0 = xadd(a[0], os[0][q]);  // x_bar: identical in transpose and VJP
+                            if constexpr (!BWD) {
+                                stg[li] = xb0;
+                            } else if constexpr (!PHASED) {
+                                stg[li] = xb0;
+                                const R x = pay[0][q];
+                                acc1 = xfma(xmul(x, p.inv_t), xsub(os[0][q], b[0]), acc1);
+                            } else {
+                                const uint32_t j = g.b0 + li;
+                                const R x = raw[q];
+                                const R m0 = cpsi[j], m1 = spsi[j];
+                                const R xb1 = xadd(a[1], os[1][q]);
+                                stg[li] = xadd(xmul(m0, xb0), xmul(m1, xb1));
+                                acc2 = xfma(x, xadd(xmul(-m1, xb0), xmul(m0, xb1)), acc2);
+                                acc1 = xfma(xmul(xmul(m0, x), p.inv_t), xsub(os[0][q], b[0]), acc1);
+                                acc1 = xfma(xmul(xmul(m1, x), p.inv_t), xsub(os[1][q], b[1]), acc1);
+                            }
+                        }
+                    }
+                    if constexpr (BWD) {
+                        *acp1 = acc1;
+                        if constexpr (PHASED) *acp2 = acc2;
+                    }
+                }
+            }
+            // ---- 5. staged per-row outputs -> perm / plan position ----
+            if constexpr (!SEQ && ((!BWD && NX > 0) || NG > 0)) {
+                __syncthreads();  // (B) staging row complete
+                if constexpr (!BWD && NX > 0) {
+                    R* y = p.y + (size_t)r * p.ldy;
+                    for (int li = tid; li < na; li += TPB) y[iA[li]] = stg[li];
+                } else if constexpr (!BWD) {
+                    R* y = p.y + (size_t)r * p.ldy;
+                    for (int li = tid; li < nb; li += TPB) y[iB[li]] = stg[li];
+                } else {
+                    R* xb = p.xbar + (size_t)r * p.ldxb;
+                    for (int li = tid; li < nb; li += TPB) xb[iB[li]] = stg[li];
+                }
+            }
+            __syncthreads();  // (C) staging row and warp totals free for the next row / tile
+        }
+        if constexpr (BWD) {  // anchor cotangents summed over rows (complete after (C))
+            const uint32_t* iA = S.oidx + g.offIA;
+            const uint32_t* iB = S.oidx + g.baseIB;
+            for (int li = tid; li < na; li += TPB) {
+                const uint32_t u = iA[li];
+                p.abar[u] = sm.acc[0][li];
+                if constexpr (PHASED) p.phibar[u] = sm.acc[NACC - 1][li];
+            }
+            for (int li = tid; li < nb; li += TPB) {
+                const uint32_t u = iB[li];
+                p.bbar[u] = sm.acc[0][na + li];
+                if constexpr (PHASED) p.psibar[u] = sm.acc[NACC - 1][na + li];
+            }
+            __syncthreads();
+        }
+    }
+}
+
+}  // namespace ms
+}  // namespace lx

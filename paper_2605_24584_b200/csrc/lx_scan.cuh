@@ -174,6 +174,7 @@ struct MainArgs {
     const R* B;
     const uint32_t* perm_b;
     const uint32_t* part;  // T+1 row offsets of the merged tiles
+    uint32_t* tile_ctr;    // zeroed tile counter (lx_main's in-order tile schedule)
     const TileDesc<R>* desc;  // T+1 tile descriptors
     uint32_t n, k, T;
     int rows;
@@ -228,536 +229,6 @@ struct Ch {
     static __host__ __device__ constexpr bool pst(int c) { return BWD && c < NG; }
     static __host__ __device__ constexpr bool qst(int c) { return BWD && c >= NG; }
 };
-
-template <class R, int NG, int NX, int NWARP>
-struct MainSmem {
-    static constexpr int NC = NG + NX;
-    static constexpr int kPad = 16 / sizeof(R);  // TMA bulk copies start 16-byte aligned
-    unsigned long long bar;   // anchors + output index ranges
-    unsigned long long barp;  // payloads (phase = row & 1)
-    R wsl[NWARP];  // warp last anchors
-    R wsf[NWARP];  // warp first anchors
-    R pv[NC][NWARP], pw[NC][NWARP];    // warp prefix totals (inclusive, strict)
-    R qv[NC][NWARP], qw[NC][NWARP];    // warp suffix totals
-    R xpv[NC][NWARP], xpw[NC][NWARP];  // warp exclusive prefix
-    R xqv[NC][NWARP], xqw[NC][NWARP];  // warp exclusive suffix
-    alignas(16) R sA[kTile + 2 * kPad];       // tile rows (TMA destination)
-    alignas(16) R sB[kTile + 2 * kPad];       // tile cols
-    alignas(16) R payA[kTile + 2 * kPad];     // g of the tile rows (sorted order)
-    alignas(16) R payB[kTile + 2 * kPad];     // x of the tile cols
-    alignas(16) uint32_t oA[kTile + 8];       // output index (perm / plan pos) of the tile rows
-    alignas(16) uint32_t oB[kTile + 8];       // ... of the tile cols
-};
-
-// SEQ: single sorted sequence (k = 0, part[t] = t*kTile): every element is a
-// "row" carrying its own payload X[r][i] (sorted order) and receiving both the
-// inclusive prefix (pre) and inclusive suffix (suf) -- the free functions
-// prefix_decay_scan / suffix_decay_scan of scan.hpp:50-73.
-//
-// Per tile: the tile descriptor gives the row/col ranges; the anchor ranges,
-// the output-index ranges and the row's payload ranges (already gathered into
-// sorted order by lx_gather_agg) arrive by TMA bulk copy (cp.async.bulk +
-// mbarrier).  The tile carries (lx_carry) are folded into each thread's
-// exclusive carry once per thread, so every item is finished by a single
-// exp(anchor difference) per direction and the outputs are plain P + Q sums.
-template <class R, int NG, int NX, bool BWD, bool SEQ, int TPB, int IPT>
-#ifndef LX_MAIN_MINB
-#define LX_MAIN_MINB(tpb) (2048 / (tpb) / 4)
-#endif
-__global__ void __launch_bounds__(TPB, LX_MAIN_MINB(TPB)) lx_main(MainArgs<R> p) {
-    static_assert(TPB * IPT == kTile, "a CTA covers one merge tile");
-    constexpr int kWarpsT = TPB / 32;
-    using C = Ch<NG, NX, BWD>;
-    constexpr int NC = C::NC;
-    using SM = MainSmem<R, NG, NX, kWarpsT>;
-    constexpr int kPad = SM::kPad;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    SM& sm = *reinterpret_cast<SM*>(smem_raw);
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t t = blockIdx.x;
-    const TileDesc<R> dt = p.desc[t], dn = p.desc[t + 1];
-    const uint32_t a0 = dt.a0, a1 = dn.a0, b0 = dt.b0, b1 = dn.b0;
-    const int na = (int)(a1 - a0), nb = (int)(b1 - b0), len = na + nb;
-    // external shard carries (multi-GPU range sharding)
-    const int ext_flags = p.ext ? (int)p.ext[2] : 0;
-    const bool has_ext_p = ext_flags & 1, has_ext_q = ext_flags & 2;
-    const R ext_pa = has_ext_p ? p.ext[0] : R(0), ext_qa = has_ext_q ? p.ext[1] : R(0);
-    const R* ext_pv = p.ext ? p.ext + 3 : nullptr;
-    const R* ext_qv = p.ext ? p.ext + 3 + (size_t)2 * NC * p.rows : nullptr;
-    // neighbouring tiles' edge anchors: the tile carries' reference points
-    // (tile 0 / tile T-1 take the external shard carries when present)
-    const bool hl = t > 0 || has_ext_p, hr = t + 1 < p.T || has_ext_q;
-    const R SL = t > 0 ? p.s_last[t - 1] : ext_pa;
-    const R SR = t + 1 < p.T ? dn.s_first : ext_qa;
-    const R s_end = dt.s_last;  // anchor of the tile's last merged element
-
-    // ---- prologue: TMA bulk copies ----
-    constexpr bool PAY_A = SEQ || NG > 0;
-    constexpr bool PAY_B = !SEQ && NX > 0;
-    constexpr bool OUT_A = !SEQ && (BWD || NX > 0);  // row-side outputs
-    constexpr bool OUT_B = !SEQ && NG > 0;           // col-side outputs
-    const uint32_t a0al = a0 & ~uint32_t(kPad - 1), b0al = b0 & ~uint32_t(kPad - 1);
-    const int offA = (int)(a0 - a0al), offB = (int)(b0 - b0al);
-    const uint32_t bytesA = na ? (uint32_t)(((offA + na + kPad - 1) / kPad) * 16) : 0u;
-    const uint32_t bytesB = nb ? (uint32_t)(((offB + nb + kPad - 1) / kPad) * 16) : 0u;
-    const uint32_t a0i = a0 & ~3u, b0i = b0 & ~3u;  // u32 index ranges: 4-element alignment
-    const int offIA = (int)(a0 - a0i), offIB = (int)(b0 - b0i);
-    const uint32_t ibytesA = (OUT_A && na) ? (uint32_t)(((offIA + na + 3) / 4) * 16) : 0u;
-    const uint32_t ibytesB = (OUT_B && nb) ? (uint32_t)(((offIB + nb + 3) / 4) * 16) : 0u;
-    const R* srcA = SEQ ? p.Xs : p.Gs;
-    const size_t ldA = SEQ ? p.ldxs : p.ldgs;
-    if (tid == 0) {
-        mbar_init(&sm.bar, 1);
-        mbar_init(&sm.barp, 1);
-        fence_mbar_init();
-        mbar_expect_tx(&sm.bar, bytesA + bytesB + ibytesA + ibytesB);
-        if (bytesA) bulk_g2s(sm.sA, p.A + a0al, bytesA, &sm.bar);
-        if (bytesB) bulk_g2s(sm.sB, p.B + b0al, bytesB, &sm.bar);
-        if (ibytesA) bulk_g2s(sm.oA, p.perm_a + a0i, ibytesA, &sm.bar);
-        if (ibytesB) bulk_g2s(sm.oB, p.perm_b + b0i, ibytesB, &sm.bar);
-        mbar_expect_tx(&sm.barp, (PAY_A ? bytesA : 0u) + (PAY_B ? bytesB : 0u));
-        if (PAY_A && bytesA) bulk_g2s(sm.payA, srcA + a0al, bytesA, &sm.barp);
-        if (PAY_B && bytesB) bulk_g2s(sm.payB, p.Xs + b0al, bytesB, &sm.barp);
-    }
-    __syncthreads();  // barrier init visible before anyone waits
-    mbar_wait(&sm.bar, 0);
-    const R* sA = sm.sA + offA;
-    const R* sB = sm.sB + offB;
-    const R* pA = sm.payA + offA;
-    const R* pB = sm.payB + offB;
-    const uint32_t* iA = sm.oA + offIA;
-    const uint32_t* iB = sm.oB + offIB;
-
-    // ---- per-thread merge: anchors, kind, local index ----
-    R s[IPT];
-    uint32_t code[IPT];  // bit31 row element, bit30 valid, low bits local index
-    {
-        const int dd = min(tid * IPT, len);
-        int ia = merge_path<true, R, int>(sA, na, sB, nb, dd);
-        int ib = dd - ia;
-#pragma unroll
-        for (int q = 0; q < IPT; ++q) {
-            if (dd + q < len) {
-                const bool takeA = ib >= nb || (ia < na && sA[ia] <= sB[ib]);
-                if (takeA) {
-                    s[q] = sA[ia];
-                    code[q] = 0xC0000000u | (uint32_t)ia;
-                    ++ia;
-                } else {
-                    s[q] = sB[ib];
-                    code[q] = 0x40000000u | (uint32_t)ib;
-                    ++ib;
-                }
-            } else {
-                s[q] = s_end;
-                code[q] = 0;
-            }
-        }
-    }
-
-    // ---- row-independent geometry: all exps are taken from anchor differences ----
-    R E[IPT];  // E[q] = exp(s[q-1] - s[q])
-    E[0] = R(0);
-#pragma unroll
-    for (int q = 1; q < IPT; ++q) E[q] = xexp(xsub(s[q - 1], s[q]));
-    const R sl = s[IPT - 1], sf = s[0];
-    R eP[5], eQ[5];
-    unsigned ltP = 0, ltQ = 0;
-#pragma unroll
-    for (int j = 0; j < 5; ++j) {
-        const int off = 1 << j;
-        const R so = shfl_up(sl, off);
-        const R sq = shfl_down(sf, off);
-        eP[j] = lane >= off ? xexp(xsub(so, sl)) : R(0);
-        if (lane >= off && so < sl) ltP |= 1u << j;
-        eQ[j] = lane + off < 32 ? xexp(xsub(sf, sq)) : R(0);
-        if (lane + off < 32 && sf < sq) ltQ |= 1u << j;
-    }
-    if (lane == 31) sm.wsl[warp] = sl;
-    if (lane == 0) sm.wsf[warp] = sf;
-    const R S1 = shfl_up(sl, 1);     // previous lane's last anchor
-    const R S1q = shfl_down(sf, 1);  // next lane's first anchor
-    __syncthreads();
-    // warp-0 geometry for the scan over warp totals
-    R eBP[5], eBQ[5];
-    unsigned ltBP = 0, ltBQ = 0;
-    if (warp == 0) {
-        const R wl = lane < kWarpsT ? sm.wsl[lane] : sm.wsl[kWarpsT - 1];
-        const R wf = lane < kWarpsT ? sm.wsf[lane] : sm.wsf[kWarpsT - 1];
-#pragma unroll
-        for (int j = 0; j < 5; ++j) {
-            const int off = 1 << j;
-            const R so = shfl_up(wl, off);
-            const R sq = shfl_down(wf, off);
-            eBP[j] = lane >= off ? xexp(xsub(so, wl)) : R(0);
-            if (lane >= off && so < wl) ltBP |= 1u << j;
-            eBQ[j] = lane + off < 32 ? xexp(xsub(wf, sq)) : R(0);
-            if (lane + off < 32 && wf < sq) ltBQ |= 1u << j;
-        }
-    }
-    // Thread-exclusive anchors.  The first thread's left neighbour is the
-    // previous tile's last element (SL), the last thread's right neighbour is
-    // the next tile's first element (SR): the tile carries enter there.
-    const bool first_t = tid == 0, last_t = tid == TPB - 1;
-    const R SW = warp > 0 ? sm.wsl[warp - 1] : sf;            // prev warp's last anchor
-    const R SWq = warp < kWarpsT - 1 ? sm.wsf[warp + 1] : sl;  // next warp's first anchor
-    const R eTW = (lane > 0 && warp > 0) ? xexp(xsub(SW, S1)) : R(0);
-    const bool ltTW = SW < S1;
-    const R eTWq = (lane < 31 && warp < kWarpsT - 1) ? xexp(xsub(S1q, SWq)) : R(0);
-    const bool ltTWq = S1q < SWq;
-    const R SE = first_t ? SL : (lane > 0 ? S1 : SW);
-    const R SEq = last_t ? SR : (lane < 31 ? S1q : SWq);
-    const bool hasP = first_t ? hl : true, hasQ = last_t ? hr : true;
-    // tile carry folded into a non-first thread's exclusive carry
-    const R eTL = (!first_t && hl) ? xexp(xsub(SL, SE)) : R(0);
-    const bool ltTL = SL < SE;
-    const R eTR = (!last_t && hr) ? xexp(xsub(SEq, SR)) : R(0);
-    const bool ltTR = SEq < SR;
-    R eI[IPT], eIq[IPT];
-    unsigned ltI = 0, ltIq = 0;
-#pragma unroll
-    for (int q = 0; q < IPT; ++q) {
-        eI[q] = hasP ? xexp(xsub(SE, s[q])) : R(0);
-        if (SE < s[q]) ltI |= 1u << q;
-        eIq[q] = hasQ ? xexp(xsub(s[q], SEq)) : R(0);
-        if (s[q] < SEq) ltIq |= 1u << q;
-    }
-
-    const R* cphi = p.cphi;
-    const R* sphi = p.sphi;
-    const R* cpsi = p.cpsi;
-    const R* spsi = p.spsi;
-    const size_t T = p.T;
-    R acc1[IPT], acc2[IPT];  // backward: a_bar/b_bar and phi_bar/psi_bar over rows
-#pragma unroll
-    for (int q = 0; q < IPT; ++q) acc1[q] = acc2[q] = R(0);
-
-    for (int r = 0; r < p.rows; ++r) {
-        if (r > 0) {
-            __syncthreads();  // previous row's payload reads are done
-            if (tid == 0) {
-                mbar_expect_tx(&sm.barp, (PAY_A ? bytesA : 0u) + (PAY_B ? bytesB : 0u));
-                if (PAY_A && bytesA) bulk_g2s(sm.payA, srcA + (size_t)r * ldA + a0al, bytesA, &sm.barp);
-                if (PAY_B && bytesB) bulk_g2s(sm.payB, p.Xs + (size_t)r * p.ldxs + b0al, bytesB, &sm.barp);
-            }
-        }
-        // tile carries of this row (issued before the payload wait), combined
-        // with the external shard carries: ext (+) tiles<t  and  tiles>t (+) ext
-        R cpv[NC], cps[NC], cqv[NC], cqs[NC];
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            const size_t sl0 = ((size_t)(2 * c) * p.rows + r), sl1 = ((size_t)(2 * c + 1) * p.rows + r);
-            cpv[c] = t > 0 ? p.cp[sl0 * T + t - 1] : R(0);
-            cps[c] = (t > 0 && C::pst(c)) ? p.cp[sl1 * T + t - 1] : R(0);
-            cqv[c] = t + 1 < p.T ? p.cq[sl0 * T + t + 1] : R(0);
-            cqs[c] = (t + 1 < p.T && C::qst(c)) ? p.cq[sl1 * T + t + 1] : R(0);
-            if (has_ext_p) {
-                const R ev = ext_pv[sl0], es = C::pst(c) ? ext_pv[sl1] : R(0);
-                if (t > 0) {  // (ext_anchor, ev, es) then (SL, cpv, cps)
-                    const R e = xexp(xsub(ext_pa, SL));
-                    if (C::pst(c)) cps[c] = xadd(cps[c], ext_pa < SL ? xmul(e, ev) : es);
-                    cpv[c] = xfma(e, ev, cpv[c]);
-                } else {
-                    cpv[c] = ev;
-                    cps[c] = es;
-                }
-            }
-            if (has_ext_q) {
-                const R ev = ext_qv[sl0], es = C::qst(c) ? ext_qv[sl1] : R(0);
-                if (t + 1 < p.T) {  // (SR, cqv, cqs) then (ext_anchor, ev, es)
-                    const R e = xexp(xsub(SR, ext_qa));
-                    if (C::qst(c)) cqs[c] = xadd(cqs[c], SR < ext_qa ? xmul(e, ev) : es);
-                    cqv[c] = xfma(e, ev, cqv[c]);
-                } else {
-                    cqv[c] = ev;
-                    cqs[c] = es;
-                }
-            }
-        }
-        mbar_wait(&sm.barp, (uint32_t)(r & 1));
-        // ---- payloads (from shared memory) ----
-        R pay[NC][IPT];
-#pragma unroll
-        for (int q = 0; q < IPT; ++q) {
-#pragma unroll
-            for (int c = 0; c < NC; ++c) pay[c][q] = R(0);
-            const uint32_t cd = code[q];
-            if (!(cd & 0x40000000u)) continue;
-            const uint32_t li = cd & 0x3fffffffu;
-            if (cd & 0x80000000u) {
-                if constexpr (SEQ) {
-                    pay[0][q] = pA[li];
-                } else if constexpr (NG > 0) {
-                    const R g = pA[li];
-                    if constexpr (NG == 2) {
-                        pay[0][q] = xmul(cphi[a0 + li], g);
-                        pay[1][q] = xmul(sphi[a0 + li], g);
-                    } else {
-                        pay[0][q] = g;
-                    }
-                }
-            } else {
-                if constexpr (NX > 0) {
-                    const R x = pB[li];
-                    if constexpr (NX == 2) {
-                        pay[NG][q] = xmul(cpsi[b0 + li], x);
-                        pay[NG + 1][q] = xmul(spsi[b0 + li], x);
-                    } else {
-                        pay[NG][q] = x;
-                    }
-                }
-            }
-        }
-
-        // ---- prefix: thread-serial, warp Kogge-Stone ----
-        R pi[NC][IPT], ps[NC][IPT];
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            pi[c][0] = pay[c][0];
-            ps[c][0] = R(0);
-#pragma unroll
-            for (int q = 1; q < IPT; ++q) {
-                if (C::pst(c)) ps[c][q] = (s[q - 1] < s[q]) ? xmul(E[q], pi[c][q - 1]) : ps[c][q - 1];
-                pi[c][q] = xfma(E[q], pi[c][q - 1], pay[c][q]);
-            }
-        }
-        R v[NC], w[NC];
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            v[c] = pi[c][IPT - 1];
-            w[c] = C::pst(c) ? ps[c][IPT - 1] : R(0);
-        }
-#pragma unroll
-        for (int j = 0; j < 5; ++j) {
-            const int off = 1 << j;
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                const R vo = shfl_up(v[c], off);
-                if (C::pst(c)) {
-                    const R wo = shfl_up(w[c], off);
-                    if (lane >= off) w[c] = xadd(w[c], ((ltP >> j) & 1) ? xmul(eP[j], vo) : wo);
-                }
-                if (lane >= off) v[c] = xfma(eP[j], vo, v[c]);
-            }
-        }
-        // ---- suffix: thread-serial, warp Kogge-Stone ----
-        R qi[NC][IPT], qs[NC][IPT];
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            qi[c][IPT - 1] = pay[c][IPT - 1];
-            qs[c][IPT - 1] = R(0);
-#pragma unroll
-            for (int q = IPT - 2; q >= 0; --q) {
-                if (C::qst(c)) qs[c][q] = (s[q] < s[q + 1]) ? xmul(E[q + 1], qi[c][q + 1]) : qs[c][q + 1];
-                qi[c][q] = xfma(E[q + 1], qi[c][q + 1], pay[c][q]);
-            }
-        }
-        R vq[NC], wq[NC];
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            vq[c] = qi[c][0];
-            wq[c] = C::qst(c) ? qs[c][0] : R(0);
-        }
-#pragma unroll
-        for (int j = 0; j < 5; ++j) {
-            const int off = 1 << j;
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                const R vo = shfl_down(vq[c], off);
-                if (C::qst(c)) {
-                    const R wo = shfl_down(wq[c], off);
-                    if (lane + off < 32) wq[c] = xadd(wq[c], ((ltQ >> j) & 1) ? xmul(eQ[j], vo) : wo);
-                }
-                if (lane + off < 32) vq[c] = xfma(eQ[j], vo, vq[c]);
-            }
-        }
-        // ---- warp totals -> block scan in warp 0 ----
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            if (lane == 31) {
-                sm.pv[c][warp] = v[c];
-                sm.pw[c][warp] = w[c];
-            }
-            if (lane == 0) {
-                sm.qv[c][warp] = vq[c];
-                sm.qw[c][warp] = wq[c];
-            }
-        }
-        __syncthreads();
-        if (warp == 0) {
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                R bv = lane < kWarpsT ? sm.pv[c][lane] : R(0);
-                R bw = lane < kWarpsT ? sm.pw[c][lane] : R(0);
-                R cv = lane < kWarpsT ? sm.qv[c][lane] : R(0);
-                R cw = lane < kWarpsT ? sm.qw[c][lane] : R(0);
-#pragma unroll
-                for (int j = 0; j < 5; ++j) {
-                    const int off = 1 << j;
-                    const R vo = shfl_up(bv, off);
-                    const R wo = shfl_up(bw, off);
-                    const R vqo = shfl_down(cv, off);
-                    const R wqo = shfl_down(cw, off);
-                    if (lane >= off) {
-                        if (C::pst(c)) bw = xadd(bw, ((ltBP >> j) & 1) ? xmul(eBP[j], vo) : wo);
-                        bv = xfma(eBP[j], vo, bv);
-                    }
-                    if (lane + off < 32) {
-                        if (C::qst(c)) cw = xadd(cw, ((ltBQ >> j) & 1) ? xmul(eBQ[j], vqo) : wqo);
-                        cv = xfma(eBQ[j], vqo, cv);
-                    }
-                }
-                // exclusive per warp (prefix from lane-1, suffix from lane+1)
-                const R xv = shfl_up(bv, 1), xw = shfl_up(bw, 1);
-                const R yv = shfl_down(cv, 1), yw = shfl_down(cw, 1);
-                if (lane < kWarpsT) {
-                    sm.xpv[c][lane] = xv;
-                    sm.xpw[c][lane] = xw;
-                    sm.xqv[c][lane] = yv;
-                    sm.xqw[c][lane] = yw;
-                }
-            }
-        }
-        // lane-exclusive values within the warp
-        R V1[NC], W1[NC], V1q[NC], W1q[NC];
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            V1[c] = shfl_up(v[c], 1);
-            W1[c] = shfl_up(w[c], 1);
-            V1q[c] = shfl_down(vq[c], 1);
-            W1q[c] = shfl_down(wq[c], 1);
-        }
-        __syncthreads();
-
-        // ---- thread-exclusive carries (+ tile carries), folded into the items ----
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            R VE = R(0), WE = R(0), VEq = R(0), WEq = R(0);
-            if (first_t) {
-                VE = cpv[c];
-                WE = cps[c];
-            } else {
-                if (lane > 0) {
-                    VE = V1[c];
-                    WE = W1[c];
-                    if (warp > 0) {
-                        const R VW = sm.xpv[c][warp], WW = sm.xpw[c][warp];
-                        if (C::pst(c)) WE = xadd(W1[c], ltTW ? xmul(eTW, VW) : WW);
-                        VE = xfma(eTW, VW, V1[c]);
-                    }
-                } else {
-                    VE = sm.xpv[c][warp];
-                    WE = sm.xpw[c][warp];
-                }
-                if (hl) {  // previous tiles, anchored at SL <= SE
-                    if (C::pst(c)) WE = xadd(WE, ltTL ? xmul(eTL, cpv[c]) : cps[c]);
-                    VE = xfma(eTL, cpv[c], VE);
-                }
-            }
-            if (last_t) {
-                VEq = cqv[c];
-                WEq = cqs[c];
-            } else {
-                if (lane < 31) {
-                    VEq = V1q[c];
-                    WEq = W1q[c];
-                    if (warp < kWarpsT - 1) {
-                        const R VW = sm.xqv[c][warp], WW = sm.xqw[c][warp];
-                        if (C::qst(c)) WEq = xadd(W1q[c], ltTWq ? xmul(eTWq, VW) : WW);
-                        VEq = xfma(eTWq, VW, V1q[c]);
-                    }
-                } else {
-                    VEq = sm.xqv[c][warp];
-                    WEq = sm.xqw[c][warp];
-                }
-                if (hr) {  // following tiles, anchored at SR >= SEq
-                    if (C::qst(c)) WEq = xadd(WEq, ltTR ? xmul(eTR, cqv[c]) : cqs[c]);
-                    VEq = xfma(eTR, cqv[c], VEq);
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < IPT; ++q) {
-                if (C::pst(c)) ps[c][q] = xadd(ps[c][q], ((ltI >> q) & 1) ? xmul(eI[q], VE) : WE);
-                pi[c][q] = xfma(eI[q], VE, pi[c][q]);
-                if (C::qst(c)) qs[c][q] = xadd(qs[c][q], ((ltIq >> q) & 1) ? xmul(eIq[q], VEq) : WEq);
-                qi[c][q] = xfma(eIq[q], VEq, qi[c][q]);
-            }
-        }
-
-        // ---- outputs: complete prefix/suffix sums per item ----
-#pragma unroll
-        for (int q = 0; q < IPT; ++q) {
-            const uint32_t cd = code[q];
-            if (!(cd & 0x40000000u)) continue;
-            const uint32_t li = cd & 0x3fffffffu;
-            if (cd & 0x80000000u) {  // ---- row element ----
-                const uint32_t i = a0 + li;
-                if constexpr (SEQ) {
-                    p.pre[(size_t)r * p.n + i] = pi[0][q];
-                    p.suf[(size_t)r * p.n + i] = qi[0][q];
-                } else if constexpr (!BWD && NX > 0) {
-                    R out = xadd(pi[NG][q], qi[NG][q]);
-                    if constexpr (NX == 2)
-                        out = xadd(xmul(cphi[i], out), xmul(sphi[i], xadd(pi[NG + 1][q], qi[NG + 1][q])));
-                    p.y[(size_t)r * p.ldy + iA[li]] = out;
-                } else if constexpr (BWD) {
-                    const R g = pA[li];
-                    if constexpr (NX == 2) {
-                        const R m0 = cphi[i], m1 = sphi[i];
-                        const R in0 = xsub(qs[NG][q], pi[NG][q]);      // sum_{b>a} - sum_{b<a}
-                        const R in1 = xsub(qs[NG + 1][q], pi[NG + 1][q]);
-                        acc1[q] = xfma(xmul(xmul(m0, g), p.inv_t), in0, acc1[q]);
-                        acc1[q] = xfma(xmul(xmul(m1, g), p.inv_t), in1, acc1[q]);
-                        const R p0 = xadd(pi[NG][q], qi[NG][q]), p1 = xadd(pi[NG + 1][q], qi[NG + 1][q]);
-                        acc2[q] = xfma(g, xadd(xmul(-m1, p0), xmul(m0, p1)), acc2[q]);
-                    } else {
-                        acc1[q] = xfma(xmul(g, p.inv_t), xsub(qs[NG][q], pi[NG][q]), acc1[q]);
-                    }
-                }
-            } else {  // ---- column element ----
-                if constexpr (NG > 0) {
-                    const uint32_t j = b0 + li;
-                    const uint32_t u = iB[li];
-                    const R xb0 = xadd(pi[0][q], qi[0][q]);  // x_bar: identical in transpose and VJP
-                    if constexpr (!BWD) {
-                        p.y[(size_t)r * p.ldy + u] = xb0;
-                    } else {
-                        const R x = pB[li];
-                        if constexpr (NG == 2) {
-                            const R m0 = cpsi[j], m1 = spsi[j];
-                            const R xb1 = xadd(pi[1][q], qi[1][q]);
-                            p.xbar[(size_t)r * p.ldxb + u] = xadd(xmul(m0, xb0), xmul(m1, xb1));
-                            acc2[q] = xfma(x, xadd(xmul(-m1, xb0), xmul(m0, xb1)), acc2[q]);
-                            acc1[q] = xfma(xmul(xmul(m0, x), p.inv_t), xsub(qi[0][q], ps[0][q]), acc1[q]);
-                            acc1[q] = xfma(xmul(xmul(m1, x), p.inv_t), xsub(qi[1][q], ps[1][q]), acc1[q]);
-                        } else {
-                            p.xbar[(size_t)r * p.ldxb + u] = xb0;
-                            acc1[q] = xfma(xmul(x, p.inv_t), xsub(qi[0][q], ps[0][q]), acc1[q]);
-                        }
-                    }
-                }
-            }
-        }
-    }
-    if constexpr (BWD) {  // anchor cotangents summed over rows
-#pragma unroll
-        for (int q = 0; q < IPT; ++q) {
-            const uint32_t cd = code[q];
-            if (!(cd & 0x40000000u)) continue;
-            const uint32_t li = cd & 0x3fffffffu;
-            if (cd & 0x80000000u) {
-                const uint32_t u = iA[li];
-                p.abar[u] = acc1[q];
-                if constexpr (NG == 2) p.phibar[u] = acc2[q];
-            } else {
-                const uint32_t u = iB[li];
-                p.bbar[u] = acc1[q];
-                if constexpr (NG == 2) p.psibar[u] = acc2[q];
-            }
-        }
-    }
-}
 
 // ---------------------------------------------------------------------------
 // gather + tile aggregates (one pass per payload side).  For every merge tile
