@@ -10,7 +10,8 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liblaplex_b200.so")
+# LAPLEX_LIB: load an alternative in-tree build (diagnostic sweeps, tools/)
+LIB_PATH = os.environ.get("LAPLEX_LIB") or os.path.join(HERE, "liblaplex_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "laplex_c.h")
 
 _lib = None

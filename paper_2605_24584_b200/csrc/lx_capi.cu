@@ -346,12 +346,17 @@ __global__ void cos_sin_kernel(const R* __restrict__ ph, uint32_t m, R* __restri
     }
 }
 
+// ≤256 caller-index buckets of 2^shift elements (permutation plans, store grouping)
+int bucket_shift(uint32_t m) {
+    int bits = 0;
+    while ((1ull << bits) < m) ++bits;
+    return bits > 8 ? bits - 8 : 0;
+}
+
 void build_splan(Side& sd, cudaStream_t st) {
     using namespace lx::sort;
     const uint32_t m = sd.m;
-    int bits = 0;
-    while ((1ull << bits) < m) ++bits;
-    const int shift = bits > 8 ? bits - 8 : 0;
+    const int shift = bucket_shift(m);
     const uint32_t tiles = (m + kTile - 1) / kTile;
     sd.spos = DBuf((size_t)m * 4, st);
     sd.sdst = DBuf((size_t)m * 4, st);
@@ -517,6 +522,8 @@ lx::ms::MainArgs<R> main_args(const View<R>& v, int rows) {
     a.cpsi = v.cpsi;
     a.spsi = v.spsi;
     a.inv_t = v.inv_t;
+    a.gshift_a = bucket_shift(v.n);
+    a.gshift_b = bucket_shift(v.k);
     return a;
 }
 
@@ -539,7 +546,7 @@ void launch_main(const char* name, const lx::ms::MainArgs<R>& a, cudaStream_t st
     static std::once_flag once;
     std::call_once(once, [&] {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TPB, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TPB + 32, smem);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
         if (per_sm < 1) per_sm = 1;
     });
@@ -549,7 +556,7 @@ void launch_main(const char* name, const lx::ms::MainArgs<R>& a, cudaStream_t st
     ck(cudaMemsetAsync(ctr.p, 0, 4, st), "memset");
     lx::ms::MainArgs<R> b = a;
     b.tile_ctr = ctr.as<uint32_t>();
-    launch(name, st, [&] { kern<<<grid, TPB, smem, st>>>(b); });
+    launch(name, st, [&] { kern<<<grid, TPB + 32, smem, st>>>(b); });  // + producer warp
 }
 
 template <class R, int NC>

@@ -122,6 +122,9 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 // 1-D TMA bulk copy global -> shared (16-byte aligned, size % 16 == 0), completes on bar
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(

@@ -35,11 +35,13 @@
 namespace lx {
 namespace ms {
 
-template <class R>
+template <class R, int NC>
 struct MainStage {
     static constexpr int kPad = 16 / sizeof(R);
-    unsigned long long bar;   // anchors + output indices
-    unsigned long long barp;  // payloads (one completion per batch row)
+    unsigned long long bar;    // "full": header, anchors + output indices (producer -> consumers)
+    unsigned long long barp;   // payloads (one completion per batch row)
+    unsigned long long empty;  // consumers -> producer: the stage may be refilled
+    R c0[4][NC];               // row-0 tile carries: prefix, strict prefix, suffix, strict suffix
     uint32_t t;  // tile index staged here (>= T: no more tiles)
     uint32_t a0, b0;
     int na, nb;
@@ -49,9 +51,18 @@ struct MainStage {
     alignas(16) uint32_t oidx[kTile + 16];  // output index ranges: A at [offIA], B at [baseIB + offIB]
 };
 
+constexpr int kMainStages = 2;
+
+constexpr int kGroupBuckets = 256;
+
 template <class R, int NC, int NW, int NACC>
 struct MainShared {
-    MainStage<R> st[2];
+    MainStage<R, NC> st[kMainStages];
+    // store grouping of the current tile: gmap[side][k] = side-local index of
+    // the k-th element in output-bucket order; gcnt = bucket counters
+    uint16_t gmap[2][kTile];
+    uint32_t gcnt[2][kGroupBuckets];
+    uint32_t gwarp[2][NW];
     // backward: a_bar at [li], b_bar at [na + li] (and phi_bar / psi_bar),
     // accumulated over the batch rows by the element's owning thread
     R acc[NACC > 0 ? NACC : 1][kTile];
@@ -92,11 +103,26 @@ struct TileGeom {
 };
 
 // Thread 0: stage tile t (anchors, output indices, row-0 payloads) by TMA.
-template <class R, bool SEQ, bool PAY_A, bool PAY_B, bool OUT_A, bool OUT_B>
-__device__ __forceinline__ void issue_tile(MainStage<R>& S, const MainArgs<R>& p, uint32_t t, const TileDesc<R>& dt,
-                                           const TileDesc<R>& dn, R SL) {
+// Producer lane: stage tile t (header, row-0 carries, anchors, output
+// indices, row-0 payloads) and arm the stage's barriers.  t >= T stages the
+// end-of-work sentinel (header only).
+template <class R, int NC, bool SEQ, bool PAY_A, bool PAY_B, bool OUT_A, bool OUT_B, class CH>
+__device__ __forceinline__ void issue_tile(MainStage<R, NC>& S, const MainArgs<R>& p, uint32_t t,
+                                           const TileDesc<R>& dt, const TileDesc<R>& dn, R SL) {
     S.t = t;
-    if (t >= p.T) return;
+    if (t >= p.T) {
+        mbar_expect_tx(&S.bar, 0u);
+        return;
+    }
+    const size_t T = p.T, rows = p.rows;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const size_t sl0 = (size_t)(2 * c) * rows, sl1 = (size_t)(2 * c + 1) * rows;
+        S.c0[0][c] = t > 0 ? p.cp[sl0 * T + t - 1] : R(0);
+        S.c0[1][c] = (t > 0 && CH::pst(c)) ? p.cp[sl1 * T + t - 1] : R(0);
+        S.c0[2][c] = t + 1 < T ? p.cq[sl0 * T + t + 1] : R(0);
+        S.c0[3][c] = (t + 1 < T && CH::qst(c)) ? p.cq[sl1 * T + t + 1] : R(0);
+    }
     TileGeom<R> g;
     g.init(dt.a0, dt.b0, (int)(dn.a0 - dt.a0), (int)(dn.b0 - dt.b0), OUT_A, OUT_B);
     S.a0 = dt.a0;
@@ -120,6 +146,73 @@ __device__ __forceinline__ void issue_tile(MainStage<R>& S, const MainArgs<R>& p
 // Channel layout: g channels first (c < NG), then x channels.  Strict prefix
 // variants for g channels and strict suffix variants for x channels, in the
 // backward (BWD) configuration only.  SEQ: one x channel carried by rows.
+// diagnostics only (LX_DIAG_CONTIG): write outputs at the sorted position
+// instead of perm / plan position, to isolate the cost of the scattered stores
+#ifdef LX_DIAG_CONTIG
+#define LXO(perm_pos, sorted_pos) (sorted_pos)
+#else
+#define LXO(perm_pos, sorted_pos) (perm_pos)
+#endif
+
+// barrier among the TPB consumer threads (named barrier 1; the producer warp is not part of it)
+template <int TPB>
+__device__ __forceinline__ void cbar() {
+    asm volatile("bar.sync 1, %0;" ::"n"(TPB) : "memory");
+}
+
+// Store grouping.  The outputs of a tile go to perm / plan positions that are
+// spread over up to 256 caller-index buckets (2 MB pages apart at 2^30); a
+// warp storing 32 consecutive sorted elements would touch ~32 pages per
+// instruction.  Instead the tile's elements of each side are ranked by bucket
+// (counting sort in shared memory; order inside a bucket is irrelevant since
+// every element carries its exact position), and stores walk that order:
+// one or two runs per warp instruction.  gcnt must be zero on entry and is
+// zero again on exit.  NS sides (0: rows via idx0, 1: cols via idx1).
+template <int TPB, int NW, bool SA, bool SB>
+__device__ __forceinline__ void group_tile(uint16_t (&gmap)[2][kTile], uint32_t (&gcnt)[2][kGroupBuckets],
+                                           uint32_t (&gwarp)[2][NW], const uint32_t* idx0, int n0, int sh0,
+                                           const uint32_t* idx1, int n1, int sh1, int tid) {
+    static_assert(TPB == kGroupBuckets, "one bucket per consumer thread");
+    const int lane = tid & 31, warp = tid >> 5;
+    if (SA)
+        for (int li = tid; li < n0; li += TPB) atomicAdd(&gcnt[0][idx0[li] >> sh0], 1u);
+    if (SB)
+        for (int li = tid; li < n1; li += TPB) atomicAdd(&gcnt[1][idx1[li] >> sh1], 1u);
+    cbar<TPB>();
+    uint32_t c0 = SA ? gcnt[0][tid] : 0u, c1 = SB ? gcnt[1][tid] : 0u;
+    uint32_t x0 = c0, x1 = c1;  // inclusive warp scans
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y0 = __shfl_up_sync(FULL, x0, o), y1 = __shfl_up_sync(FULL, x1, o);
+        if (lane >= o) {
+            x0 += y0;
+            x1 += y1;
+        }
+    }
+    if (lane == 31) {
+        gwarp[0][warp] = x0;
+        gwarp[1][warp] = x1;
+    }
+    cbar<TPB>();
+    uint32_t b0 = 0, b1 = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w)
+        if (w < warp) {
+            b0 += gwarp[0][w];
+            b1 += gwarp[1][w];
+        }
+    if (SA) gcnt[0][tid] = b0 + x0 - c0;  // exclusive offsets
+    if (SB) gcnt[1][tid] = b1 + x1 - c1;
+    cbar<TPB>();
+    if (SA)
+        for (int li = tid; li < n0; li += TPB) gmap[0][atomicAdd(&gcnt[0][idx0[li] >> sh0], 1u)] = (uint16_t)li;
+    if (SB)
+        for (int li = tid; li < n1; li += TPB) gmap[1][atomicAdd(&gcnt[1][idx1[li] >> sh1], 1u)] = (uint16_t)li;
+    cbar<TPB>();
+    if (SA) gcnt[0][tid] = 0u;  // ready for the next tile (read again only after later barriers)
+    if (SB) gcnt[1][tid] = 0u;
+}
+
 template <class R, int NG, int NX, bool BWD, bool SEQ, int TPB, int IPT>
 #ifndef LX_MAIN_CTAS
 #define LX_MAIN_CTAS 768
@@ -127,7 +220,7 @@ template <class R, int NG, int NX, bool BWD, bool SEQ, int TPB, int IPT>
 #ifndef LX_BWD_CTAS
 #define LX_BWD_CTAS 512
 #endif
-__global__ void __launch_bounds__(TPB, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS : LX_MAIN_CTAS) / TPB : 1) lx_main(MainArgs<R> p) {
+__global__ void __launch_bounds__(TPB + 32, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS : LX_MAIN_CTAS) / TPB : 1) lx_main(MainArgs<R> p) {
     static_assert(TPB * IPT == kTile, "a CTA covers one merge tile");
     constexpr int NW = TPB / 32;
     static_assert(NW <= 32 && (NW & (NW - 1)) == 0, "warps per CTA: power of two");
@@ -148,7 +241,7 @@ __global__ void __launch_bounds__(TPB, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS : LX_
     SM& sm = *reinterpret_cast<SM*>(smem_main);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t T = p.T, G = gridDim.x;
+    const uint32_t T = p.T;
     const int rows = p.rows;
     const int ext_flags = p.ext ? (int)p.ext[2] : 0;
     const bool has_ext_p = ext_flags & 1, has_ext_q = ext_flags & 2;
@@ -160,51 +253,56 @@ __global__ void __launch_bounds__(TPB, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS : LX_
     const R* cpsi = p.cpsi;
     const R* spsi = p.spsi;
 
-    // ---- tile schedule ----
+    // ---- tile schedule: one producer warp, TPB consumer threads ----
     // Tiles are claimed in increasing order from a global counter, so the
     // tiles in flight stay a compact window of the merged sequence (the
-    // staged output writes of neighbouring tiles then combine in L2).  Thread
-    // 0 runs the claim two tiles ahead: claim (iteration i) -> descriptor
-    // loads (i+1) -> TMA issue (i+2), so none of the latencies is exposed.
-    uint32_t tn1 = 0, tn2 = 0;  // thread 0: next tile (descriptors loaded), the one after (claimed)
-    TileDesc<R> nd0, nd1;
-    R nsl = R(0);
-    auto load_desc = [&](uint32_t tt) {
-        if (tt < T) {
-            nd0 = p.desc[tt];
-            nd1 = p.desc[tt + 1];
-            nsl = tt > 0 ? p.s_last[tt - 1] : R(0);
-        }
-    };
+    // staged output writes of neighbouring tiles then combine in L2).  Lane 0
+    // of the producer warp claims a tile, loads its descriptors, waits for a
+    // free stage and stages the tile by TMA; its latencies never stall the
+    // consumers, which synchronise among themselves on named barrier 1.
+    for (int i = tid; i < 2 * kGroupBuckets; i += blockDim.x) (&sm.gcnt[0][0])[i] = 0u;
     if (tid == 0) {
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < kMainStages; ++s) {
             mbar_init(&sm.st[s].bar, 1);
             mbar_init(&sm.st[s].barp, 1);
+            mbar_init(&sm.st[s].empty, 1);
         }
         fence_mbar_init();
-        const uint32_t t0 = atomicAdd(p.tile_ctr, 1u);
-        load_desc(t0);
-        issue_tile<R, SEQ, PAY_A, PAY_B, OUT_A, OUT_B>(sm.st[0], p, t0, nd0, nd1, nsl);
-        tn1 = atomicAdd(p.tile_ctr, 1u);
-        load_desc(tn1);
-        tn2 = atomicAdd(p.tile_ctr, 1u);
     }
     __syncthreads();
-
-    for (int it = 0;; ++it) {
-        const int sidx = it & 1;
-        MainStage<R>& S = sm.st[sidx];
-        const uint32_t t = S.t;
-        if (t >= T) break;
-        // ---- stage the CTA's next tile into the other buffer ----
-        if (tid == 0) {
-            issue_tile<R, SEQ, PAY_A, PAY_B, OUT_A, OUT_B>(sm.st[sidx ^ 1], p, tn1, nd0, nd1, nsl);
-            if (tn1 < T) {
-                tn1 = tn2;
-                load_desc(tn1);
-                if (tn1 < T) tn2 = atomicAdd(p.tile_ctr, 1u);
+    if (warp == NW) {
+        if (lane == 0) {
+            auto claim = [&](uint32_t& tt, TileDesc<R>& d0, TileDesc<R>& d1, R& sl) {
+                tt = atomicAdd(p.tile_ctr, 1u);
+                if (tt < T) {
+                    d0 = p.desc[tt];
+                    d1 = p.desc[tt + 1];
+                    sl = tt > 0 ? p.s_last[tt - 1] : R(0);
+                }
+            };
+            uint32_t tc;
+            TileDesc<R> d0, d1;
+            R sl = R(0);
+            claim(tc, d0, d1, sl);
+            for (int it = 0;; ++it) {
+                const int s = it % kMainStages;
+                const uint32_t use = (uint32_t)(it / kMainStages);
+                if (it >= kMainStages) mbar_wait(&sm.st[s].empty, (use - 1u) & 1u);
+                issue_tile<R, NC, SEQ, PAY_A, PAY_B, OUT_A, OUT_B, C>(sm.st[s], p, tc, d0, d1, sl);
+                if (tc >= T) break;
+                claim(tc, d0, d1, sl);
             }
         }
+        return;
+    }
+
+    for (int it = 0;; ++it) {
+        const int sidx = it % kMainStages;
+        auto& S = sm.st[sidx];
+        const uint32_t use = (uint32_t)(it / kMainStages);  // completions of this stage's barriers so far
+        mbar_wait(&S.bar, use & 1u);
+        const uint32_t t = S.t;
+        if (t >= T) break;
         TileGeom<R> g;
         g.init(S.a0, S.b0, S.na, S.nb, OUT_A, OUT_B);
         const int na = g.na, nb = g.nb, len = na + nb;
@@ -212,14 +310,14 @@ __global__ void __launch_bounds__(TPB, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS : LX_
         const bool hl = t > 0 || has_ext_p, hr = t + 1 < T || has_ext_q;
         const R SL = t > 0 ? S.SL : ext_pa;
         const R SR = t + 1 < T ? S.SR : ext_qa;
-        const uint32_t use = (uint32_t)(it >> 1);  // completions of this stage's barriers so far
-        mbar_wait(&S.bar, use & 1u);
         const R* sA = S.anch + g.offA;
         const R* sB = S.anch + g.baseB;
         const R* pA = S.pay + g.offA;
         const R* pB = S.pay + g.baseB;
         const uint32_t* iA = S.oidx + g.offIA;
         const uint32_t* iB = S.oidx + g.baseIB;
+        if constexpr (OUT_A || OUT_B)
+            group_tile<TPB, NW, OUT_A, OUT_B>(sm.gmap, sm.gcnt, sm.gwarp, iA, na, p.gshift_a, iB, nb, p.gshift_b, tid);
 
         // ---- merge: anchors and kinds of this thread's IPT elements ----
         R s[IPT];
@@ -280,10 +378,17 @@ __global__ void __launch_bounds__(TPB, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS : LX_
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
                 const size_t sl0 = ((size_t)(2 * c) * rows + r), sl1 = ((size_t)(2 * c + 1) * rows + r);
-                cpv[c] = t > 0 ? p.cp[sl0 * T + t - 1] : R(0);
-                cps[c] = (t > 0 && C::pst(c)) ? p.cp[sl1 * T + t - 1] : R(0);
-                cqv[c] = t + 1 < T ? p.cq[sl0 * T + t + 1] : R(0);
-                cqs[c] = (t + 1 < T && C::qst(c)) ? p.cq[sl1 * T + t + 1] : R(0);
+                if (r == 0) {  // staged by the producer
+                    cpv[c] = S.c0[0][c];
+                    cps[c] = S.c0[1][c];
+                    cqv[c] = S.c0[2][c];
+                    cqs[c] = S.c0[3][c];
+                } else {
+                    cpv[c] = t > 0 ? p.cp[sl0 * T + t - 1] : R(0);
+                    cps[c] = (t > 0 && C::pst(c)) ? p.cp[sl1 * T + t - 1] : R(0);
+                    cqv[c] = t + 1 < T ? p.cq[sl0 * T + t + 1] : R(0);
+                    cqs[c] = (t + 1 < T && C::qst(c)) ? p.cq[sl1 * T + t + 1] : R(0);
+                }
                 if (has_ext_p) {
                     const R ev = ext_pv[sl0], es = C::pst(c) ? ext_pv[sl1] : R(0);
                     if (t > 0) {  // (ext_anchor, ev, es) then (SL, cpv, cps)
@@ -425,7 +530,7 @@ __global__ void __launch_bounds__(TPB, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS : LX_
                     sm.qw[c][warp] = wq[c];
                 }
             }
-            __syncthreads();  // (A) warp totals; every merge of this tile is done
+            cbar<TPB>();  // (A) warp totals; every merge of this tile is done
             if (tid == 0 && r + 1 < rows) {  // next batch row's payloads into this stage
                 const R* srcA = SEQ ? p.Xs : p.Gs;
                 const size_t ldA = SEQ ? p.ldxs : p.ldgs;
@@ -679,35 +784,47 @@ __global__ void __launch_bounds__(TPB, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS : LX_
             }
             // ---- 5. staged per-row outputs -> perm / plan position ----
             if constexpr (!SEQ && ((!BWD && NX > 0) || NG > 0)) {
-                __syncthreads();  // (B) staging row complete
+                cbar<TPB>();  // (B) staging row complete
                 if constexpr (!BWD && NX > 0) {
                     R* y = p.y + (size_t)r * p.ldy;
-                    for (int li = tid; li < na; li += TPB) y[iA[li]] = stg[li];
+                    for (int k = tid; k < na; k += TPB) {
+                        const int li = sm.gmap[0][k];
+                        y[LXO(iA[li], g.a0 + li)] = stg[li];
+                    }
                 } else if constexpr (!BWD) {
                     R* y = p.y + (size_t)r * p.ldy;
-                    for (int li = tid; li < nb; li += TPB) y[iB[li]] = stg[li];
+                    for (int k = tid; k < nb; k += TPB) {
+                        const int li = sm.gmap[1][k];
+                        y[LXO(iB[li], g.b0 + li)] = stg[li];
+                    }
                 } else {
                     R* xb = p.xbar + (size_t)r * p.ldxb;
-                    for (int li = tid; li < nb; li += TPB) xb[iB[li]] = stg[li];
+                    for (int k = tid; k < nb; k += TPB) {
+                        const int li = sm.gmap[1][k];
+                        xb[LXO(iB[li], g.b0 + li)] = stg[li];
+                    }
                 }
             }
-            __syncthreads();  // (C) staging row and warp totals free for the next row / tile
+            cbar<TPB>();  // (C) staging row and warp totals free for the next row / tile
         }
         if constexpr (BWD) {  // anchor cotangents summed over rows (complete after (C))
             const uint32_t* iA = S.oidx + g.offIA;
             const uint32_t* iB = S.oidx + g.baseIB;
-            for (int li = tid; li < na; li += TPB) {
-                const uint32_t u = iA[li];
+            for (int k = tid; k < na; k += TPB) {
+                const int li = sm.gmap[0][k];
+                const uint32_t u = LXO(iA[li], g.a0 + li);
                 p.abar[u] = sm.acc[0][li];
                 if constexpr (PHASED) p.phibar[u] = sm.acc[NACC - 1][li];
             }
-            for (int li = tid; li < nb; li += TPB) {
-                const uint32_t u = iB[li];
+            for (int k = tid; k < nb; k += TPB) {
+                const int li = sm.gmap[1][k];
+                const uint32_t u = LXO(iB[li], g.b0 + li);
                 p.bbar[u] = sm.acc[0][na + li];
                 if constexpr (PHASED) p.psibar[u] = sm.acc[NACC - 1][na + li];
             }
-            __syncthreads();
+            cbar<TPB>();
         }
+        if (tid == 0) mbar_arrive(&S.empty);  // the stage may be refilled
     }
 }
 

@@ -175,6 +175,7 @@ struct MainArgs {
     const uint32_t* perm_b;
     const uint32_t* part;  // T+1 row offsets of the merged tiles
     uint32_t* tile_ctr;    // zeroed tile counter (lx_main's in-order tile schedule)
+    int gshift_a, gshift_b;  // output-position bucket = position >> gshift (store grouping)
     const TileDesc<R>* desc;  // T+1 tile descriptors
     uint32_t n, k, T;
     int rows;
