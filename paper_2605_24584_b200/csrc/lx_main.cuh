@@ -53,8 +53,6 @@ struct MainStage {
 
 constexpr int kMainStages = 2;
 
-constexpr int kGroupBuckets = 256;
-
 template <class R, int NC, int NW, int NACC>
 struct MainShared {
     MainStage<R, NC> st[kMainStages];
@@ -153,65 +151,6 @@ __device__ __forceinline__ void issue_tile(MainStage<R, NC>& S, const MainArgs<R
 #else
 #define LXO(perm_pos, sorted_pos) (perm_pos)
 #endif
-
-// barrier among the TPB consumer threads (named barrier 1; the producer warp is not part of it)
-template <int TPB>
-__device__ __forceinline__ void cbar() {
-    asm volatile("bar.sync 1, %0;" ::"n"(TPB) : "memory");
-}
-
-// Store grouping.  The outputs of a tile go to perm / plan positions that are
-// spread over up to 256 caller-index buckets (2 MB pages apart at 2^30); a
-// warp storing 32 consecutive sorted elements would touch ~32 pages per
-// instruction.  Instead the tile's elements of each side are ranked by bucket
-// (counting sort in shared memory; order inside a bucket is irrelevant since
-// every element carries its exact position), and stores walk that order:
-// one or two runs per warp instruction.  gcnt must be zero on entry and is
-// zero again on exit.  NS sides (0: rows via idx0, 1: cols via idx1).
-template <int TPB, int NW, bool SA, bool SB>
-__device__ __forceinline__ void group_tile(uint16_t (&gmap)[2][kTile], uint32_t (&gcnt)[2][kGroupBuckets],
-                                           uint32_t (&gwarp)[2][NW], const uint32_t* idx0, int n0, int sh0,
-                                           const uint32_t* idx1, int n1, int sh1, int tid) {
-    static_assert(TPB == kGroupBuckets, "one bucket per consumer thread");
-    const int lane = tid & 31, warp = tid >> 5;
-    if (SA)
-        for (int li = tid; li < n0; li += TPB) atomicAdd(&gcnt[0][idx0[li] >> sh0], 1u);
-    if (SB)
-        for (int li = tid; li < n1; li += TPB) atomicAdd(&gcnt[1][idx1[li] >> sh1], 1u);
-    cbar<TPB>();
-    uint32_t c0 = SA ? gcnt[0][tid] : 0u, c1 = SB ? gcnt[1][tid] : 0u;
-    uint32_t x0 = c0, x1 = c1;  // inclusive warp scans
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y0 = __shfl_up_sync(FULL, x0, o), y1 = __shfl_up_sync(FULL, x1, o);
-        if (lane >= o) {
-            x0 += y0;
-            x1 += y1;
-        }
-    }
-    if (lane == 31) {
-        gwarp[0][warp] = x0;
-        gwarp[1][warp] = x1;
-    }
-    cbar<TPB>();
-    uint32_t b0 = 0, b1 = 0;
-#pragma unroll
-    for (int w = 0; w < NW; ++w)
-        if (w < warp) {
-            b0 += gwarp[0][w];
-            b1 += gwarp[1][w];
-        }
-    if (SA) gcnt[0][tid] = b0 + x0 - c0;  // exclusive offsets
-    if (SB) gcnt[1][tid] = b1 + x1 - c1;
-    cbar<TPB>();
-    if (SA)
-        for (int li = tid; li < n0; li += TPB) gmap[0][atomicAdd(&gcnt[0][idx0[li] >> sh0], 1u)] = (uint16_t)li;
-    if (SB)
-        for (int li = tid; li < n1; li += TPB) gmap[1][atomicAdd(&gcnt[1][idx1[li] >> sh1], 1u)] = (uint16_t)li;
-    cbar<TPB>();
-    if (SA) gcnt[0][tid] = 0u;  // ready for the next tile (read again only after later barriers)
-    if (SB) gcnt[1][tid] = 0u;
-}
 
 template <class R, int NG, int NX, bool BWD, bool SEQ, int TPB, int IPT>
 #ifndef LX_MAIN_CTAS
@@ -317,7 +256,7 @@ __global__ void __launch_bounds__(TPB + 32, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS 
         const uint32_t* iA = S.oidx + g.offIA;
         const uint32_t* iB = S.oidx + g.baseIB;
         if constexpr (OUT_A || OUT_B)
-            group_tile<TPB, NW, OUT_A, OUT_B>(sm.gmap, sm.gcnt, sm.gwarp, iA, na, p.gshift_a, iB, nb, p.gshift_b, tid);
+            group_tile<TPB, NW, OUT_A, OUT_B, 1>(sm.gmap, sm.gcnt, sm.gwarp, iA, na, p.gshift_a, iB, nb, p.gshift_b, tid);
 
         // ---- merge: anchors and kinds of this thread's IPT elements ----
         R s[IPT];
