@@ -24,6 +24,12 @@
 
 #include "lx_common.cuh"
 
+// digit counts published after ranking (measured faster on B200 than the
+// early-count variant: 64.8 vs 66.4 ms for the 8 passes at 2^30)
+#if !defined(LX_SORT_EARLY) && !defined(LX_SORT_LATE)
+#define LX_SORT_LATE
+#endif
+
 namespace lx {
 namespace sort {
 
