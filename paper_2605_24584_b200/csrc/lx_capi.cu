@@ -655,7 +655,8 @@ DBuf sorted_payload(const View<R>& v, int rows, const R* user, const Scratch& sc
         g.idx = perm;
     }
     launch("lx_gather_agg", st, [&] {
-        lx::ms::lx_gather_agg<R, NCH, SIDE_A, GFORM, STRICT><<<v.T, lx::ms::kAggThreads, 0, st>>>(g);
+        const uint32_t grid = (v.T + lx::ms::kAggTiles - 1) / lx::ms::kAggTiles;
+        lx::ms::lx_gather_agg<R, NCH, SIDE_A, GFORM, STRICT><<<grid, lx::ms::kAggThreads, 0, st>>>(g);
     });
     return out;
 }

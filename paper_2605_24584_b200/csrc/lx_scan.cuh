@@ -334,99 +334,135 @@ struct GatherAggArgs {
 
 // SIDE_A: the tile range is the rows range; GFORM: g-channel formulas (prefix
 // strict) vs x-channel formulas (suffix strict).
+// One CTA covers kAggTiles consecutive merge tiles (about kTile elements of
+// this side), so every thread has ~kTile/kAggThreads useful loads in flight
+// per round trip (the chain is descriptors -> indices/anchors -> payload).
+#ifndef LX_AGG_TILES
+#define LX_AGG_TILES 4
+#endif
+constexpr int kAggTiles = LX_AGG_TILES;
+
 template <class R, int NCH, bool SIDE_A, bool GFORM, bool STRICT>
 __global__ void __launch_bounds__(kAggThreads) lx_gather_agg(GatherAggArgs<R> g) {
     constexpr int NW = kAggThreads / 32;
-    const uint32_t t = blockIdx.x;
+    constexpr int NT = kAggTiles;
+    constexpr int kGI = kTile * NT / 2 / kAggThreads;  // slots for ~the side's share of NT tiles
+    constexpr int kSpan = kGI * kAggThreads;
+    const uint32_t t0 = blockIdx.x * NT;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const TileDesc<R> dt = g.desc[t];
-    const TileDesc<R> dn = g.desc[t + 1];
-    const uint32_t s0 = SIDE_A ? dt.a0 : dt.b0;
-    const uint32_t s1 = SIDE_A ? dn.a0 : dn.b0;
-    const int ns = (int)(s1 - s0);
-    const R S_first = dt.s_first, S_last = dt.s_last;
+    const uint32_t T = g.T;
+    const int nt = (int)min((uint32_t)NT, T - t0);  // tiles of this CTA
+    uint32_t sb[NT + 1];                             // side offsets of the tiles (+ end)
+    R Sf[NT], Sl[NT];
+#pragma unroll
+    for (int j = 0; j <= NT; ++j) {
+        const TileDesc<R> d = g.desc[min(t0 + j, T)];
+        sb[j] = SIDE_A ? d.a0 : d.b0;
+        if (j < NT) {
+            Sf[j] = d.s_first;
+            Sl[j] = d.s_last;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+        if (j >= nt) sb[j + 1] = sb[j];
+    const uint32_t s0 = sb[0];
+    const int ns = (int)(sb[NT] - s0);
     const uint32_t* __restrict__ idx = g.idx;
     const R* __restrict__ src = g.src;
     const R* __restrict__ V = g.V;
     R* __restrict__ out = g.out;
-    __shared__ R red[4 * NCH][NW];
-    const size_t T = g.T;
+    __shared__ R red[NT][4 * NCH][NW];
     for (int r = 0; r < g.rows; ++r) {
-        R pi[NCH], ps[NCH], qi[NCH], qs[NCH];
+        R pi[NT][NCH], ps[NT][NCH], qi[NT][NCH], qs[NT][NCH];
 #pragma unroll
-        for (int c = 0; c < NCH; ++c) pi[c] = ps[c] = qi[c] = qs[c] = R(0);
-        // all loads of the thread's (up to) kGI elements are issued before use
-        constexpr int kGI = kTile / kAggThreads;
-        uint32_t ix[kGI];
-        R v[kGI], sv[kGI];
+        for (int j = 0; j < NT; ++j)
 #pragma unroll
-        for (int q = 0; q < kGI; ++q) {
-            const int i = tid + q * kAggThreads;
-            const uint32_t e = s0 + (uint32_t)i;
-            ix[q] = i < ns ? (idx ? idx[e] : e) : 0u;
-            sv[q] = i < ns ? V[e] : R(0);
-        }
+            for (int c = 0; c < NCH; ++c) pi[j][c] = ps[j][c] = qi[j][c] = qs[j][c] = R(0);
+        for (int base = 0; base < ns; base += kSpan) {  // one round unless the side dominates
+            // all loads of the thread's (up to) kGI elements are issued before use
+            uint32_t ix[kGI];
+            R v[kGI], sv[kGI];
 #pragma unroll
-        for (int q = 0; q < kGI; ++q) {
-            const int i = tid + q * kAggThreads;
-            v[q] = i < ns ? src[(size_t)r * g.ld_src + ix[q]] : R(0);
-        }
-#pragma unroll
-        for (int q = 0; q < kGI; ++q) {
-            const int i = tid + q * kAggThreads;
-            if (i >= ns) continue;
-            const uint32_t e = s0 + (uint32_t)i;
-            out[(size_t)r * g.ld_out + e] = v[q];
-            const R s = sv[q];
-            const R e1 = xexp(xsub(s, S_last)), e2 = xexp(xsub(S_first, s));
-            R pay[NCH];
-            if constexpr (NCH == 2) {
-                pay[0] = xmul(g.cph[e], v[q]);
-                pay[1] = xmul(g.sph[e], v[q]);
-            } else {
-                pay[0] = v[q];
+            for (int q = 0; q < kGI; ++q) {
+                const int i = base + tid + q * kAggThreads;
+                const uint32_t e = s0 + (uint32_t)i;
+                ix[q] = i < ns ? (idx ? idx[e] : e) : 0u;
+                sv[q] = i < ns ? V[e] : R(0);
             }
 #pragma unroll
-            for (int c = 0; c < NCH; ++c) {
-                if constexpr (GFORM) {
-                    const R pe = xmul(e1, pay[c]);
-                    pi[c] = xadd(pi[c], pe);
-                    if (STRICT && s < S_last) ps[c] = xadd(ps[c], pe);
-                    qi[c] = xfma(e2, pay[c], qi[c]);
-                } else {
-                    pi[c] = xfma(e1, pay[c], pi[c]);
-                    const R qe = xmul(e2, pay[c]);
-                    qi[c] = xadd(qi[c], qe);
-                    if (STRICT && S_first < s) qs[c] = xadd(qs[c], qe);
+            for (int q = 0; q < kGI; ++q) {
+                const int i = base + tid + q * kAggThreads;
+                v[q] = i < ns ? src[(size_t)r * g.ld_src + ix[q]] : R(0);
+            }
+#pragma unroll
+            for (int q = 0; q < kGI; ++q) {
+                const int i = base + tid + q * kAggThreads;
+                if (i >= ns) continue;
+                const uint32_t e = s0 + (uint32_t)i;
+                out[(size_t)r * g.ld_out + e] = v[q];
+                const R s = sv[q];
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                    if (e < sb[j] || e >= sb[j + 1]) continue;  // element of tile t0 + j
+                    const R S_first = Sf[j], S_last = Sl[j];
+                    const R e1 = xexp(xsub(s, S_last)), e2 = xexp(xsub(S_first, s));
+                    R pay[NCH];
+                    if constexpr (NCH == 2) {
+                        pay[0] = xmul(g.cph[e], v[q]);
+                        pay[1] = xmul(g.sph[e], v[q]);
+                    } else {
+                        pay[0] = v[q];
+                    }
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c) {
+                        if constexpr (GFORM) {
+                            const R pe = xmul(e1, pay[c]);
+                            pi[j][c] = xadd(pi[j][c], pe);
+                            if (STRICT && s < S_last) ps[j][c] = xadd(ps[j][c], pe);
+                            qi[j][c] = xfma(e2, pay[c], qi[j][c]);
+                        } else {
+                            pi[j][c] = xfma(e1, pay[c], pi[j][c]);
+                            const R qe = xmul(e2, pay[c]);
+                            qi[j][c] = xadd(qi[j][c], qe);
+                            if (STRICT && S_first < s) qs[j][c] = xadd(qs[j][c], qe);
+                        }
+                    }
                 }
             }
         }
 #pragma unroll
-        for (int c = 0; c < NCH; ++c) {
+        for (int j = 0; j < NT; ++j)
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                pi[c] = xadd(pi[c], __shfl_xor_sync(FULL, pi[c], off));
-                ps[c] = xadd(ps[c], __shfl_xor_sync(FULL, ps[c], off));
-                qi[c] = xadd(qi[c], __shfl_xor_sync(FULL, qi[c], off));
-                qs[c] = xadd(qs[c], __shfl_xor_sync(FULL, qs[c], off));
+            for (int c = 0; c < NCH; ++c) {
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    pi[j][c] = xadd(pi[j][c], __shfl_xor_sync(FULL, pi[j][c], off));
+                    ps[j][c] = xadd(ps[j][c], __shfl_xor_sync(FULL, ps[j][c], off));
+                    qi[j][c] = xadd(qi[j][c], __shfl_xor_sync(FULL, qi[j][c], off));
+                    qs[j][c] = xadd(qs[j][c], __shfl_xor_sync(FULL, qs[j][c], off));
+                }
+                if (lane == 0) {
+                    red[j][4 * c + 0][warp] = pi[j][c];
+                    red[j][4 * c + 1][warp] = ps[j][c];
+                    red[j][4 * c + 2][warp] = qi[j][c];
+                    red[j][4 * c + 3][warp] = qs[j][c];
+                }
             }
-            if (lane == 0) {
-                red[4 * c + 0][warp] = pi[c];
-                red[4 * c + 1][warp] = ps[c];
-                red[4 * c + 2][warp] = qi[c];
-                red[4 * c + 3][warp] = qs[c];
-            }
-        }
         __syncthreads();
-        if (tid < 4 * NCH) {
-            R v = red[tid][0];
+        if (tid < NT * 4 * NCH) {
+            const int j = tid / (4 * NCH), k = tid % (4 * NCH);
+            if (j < nt) {
+                R a = red[j][k][0];
 #pragma unroll
-            for (int w = 1; w < NW; ++w) v = xadd(v, red[tid][w]);
-            const int c = g.cbase + (tid >> 2), kind = tid & 3;
-            if (kind == 0) g.aggp[((size_t)(2 * c) * g.rows + r) * T + t] = v;
-            if (kind == 1 && STRICT && GFORM) g.aggp[((size_t)(2 * c + 1) * g.rows + r) * T + t] = v;
-            if (kind == 2) g.aggq[((size_t)(2 * c) * g.rows + r) * T + t] = v;
-            if (kind == 3 && STRICT && !GFORM) g.aggq[((size_t)(2 * c + 1) * g.rows + r) * T + t] = v;
+                for (int w = 1; w < NW; ++w) a = xadd(a, red[j][k][w]);
+                const int c = g.cbase + (k >> 2), kind = k & 3;
+                const size_t TT = T, t = t0 + j;
+                if (kind == 0) g.aggp[((size_t)(2 * c) * g.rows + r) * TT + t] = a;
+                if (kind == 1 && STRICT && GFORM) g.aggp[((size_t)(2 * c + 1) * g.rows + r) * TT + t] = a;
+                if (kind == 2) g.aggq[((size_t)(2 * c) * g.rows + r) * TT + t] = a;
+                if (kind == 3 && STRICT && !GFORM) g.aggq[((size_t)(2 * c + 1) * g.rows + r) * TT + t] = a;
+            }
         }
         __syncthreads();
     }

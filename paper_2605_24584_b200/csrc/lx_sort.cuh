@@ -345,7 +345,10 @@ __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict_
 // the resident blocks always sit in one or two caller-index buckets and the
 // random side of each pass stays inside an L2-resident window.
 constexpr int kPermThreads = 256;
-constexpr int kPermItems = 8;
+#ifndef LX_PERM_ITEMS
+#define LX_PERM_ITEMS 8
+#endif
+constexpr int kPermItems = LX_PERM_ITEMS;
 constexpr int kPermChunk = kPermThreads * kPermItems;
 
 // gather (caller order -> sorted order), first half: stage[r][q] = src[r][dst[q]];
