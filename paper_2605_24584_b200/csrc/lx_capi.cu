@@ -172,6 +172,7 @@ struct Core {
     std::mutex mu;
     DBuf part[2];  // merge-path tiles with side 0 (resp. 1) as the "A" operand, A-first
     DBuf desc[2], sfirst[2], slast[2];  // per-tile descriptors and edge anchors
+    DBuf gmap[2][2];  // per orientation: store order of the A / B side in every tile (lx_group_plan)
     uint32_t T[2] = {0, 0};
     DBuf ranks[4];  // [side*2 + strict]
     bool has_ranks[4] = {false, false, false, false};
@@ -220,7 +221,15 @@ struct View {
     uint32_t T;
     R inv_t;
     const uint32_t *pos_a, *dst_a, *pos_b, *dst_b;  // null = direct permutation
+    const uint16_t *gm_a, *gm_b;                      // per-tile store order (lx_group_plan)
 };
+
+// ≤256 caller-index buckets of 2^shift elements (permutation plans, store grouping)
+int bucket_shift(uint32_t m) {
+    int bits = 0;
+    while ((1ull << bits) < m) ++bits;
+    return bits > 8 ? bits - 8 : 0;
+}
 
 uint32_t tiles_for(uint64_t total) { return (uint32_t)((total + lx::ms::kTile - 1) / lx::ms::kTile); }
 
@@ -243,6 +252,17 @@ void build_partition(Core& c, int which, cudaStream_t st) {
             c.desc[which].as<lx::ms::TileDesc<R>>(), c.sfirst[which].as<R>(), c.slast[which].as<R>());
     });
     c.T[which] = T;
+    // per-tile store order of both sides (output positions: plan pos or perm)
+    const uint32_t* pa = a.staged ? a.spos.as<uint32_t>() : a.perm.as<uint32_t>();
+    const uint32_t* pb = b.staged ? b.spos.as<uint32_t>() : b.perm.as<uint32_t>();
+    c.gmap[which][0] = DBuf(((size_t)a.m + 16) * 2, st);
+    c.gmap[which][1] = DBuf(((size_t)b.m + 16) * 2, st);
+    if (T)
+        launch("lx_group_plan", st, [&] {
+            lx::ms::lx_group_plan<R><<<T, lx::ms::kGroupBuckets, 0, st>>>(
+                c.desc[which].as<lx::ms::TileDesc<R>>(), T, pa, bucket_shift(a.m), pb, bucket_shift(b.m),
+                c.gmap[which][0].as<uint16_t>(), c.gmap[which][1].as<uint16_t>());
+        });
 }
 
 template <class R>
@@ -275,6 +295,8 @@ View<R> view(Core& c, bool swapped, cudaStream_t st) {
     v.dst_a = a.staged ? a.sdst.as<uint32_t>() : nullptr;
     v.pos_b = b.staged ? b.spos.as<uint32_t>() : nullptr;
     v.dst_b = b.staged ? b.sdst.as<uint32_t>() : nullptr;
+    v.gm_a = c.gmap[ia][0].as<uint16_t>();
+    v.gm_b = c.gmap[ia][1].as<uint16_t>();
     return v;
 }
 
@@ -344,13 +366,6 @@ __global__ void cos_sin_kernel(const R* __restrict__ ph, uint32_t m, R* __restri
         c[i] = lx::xcos(ph[i]);
         s[i] = lx::xsin(ph[i]);
     }
-}
-
-// ≤256 caller-index buckets of 2^shift elements (permutation plans, store grouping)
-int bucket_shift(uint32_t m) {
-    int bits = 0;
-    while ((1ull << bits) < m) ++bits;
-    return bits > 8 ? bits - 8 : 0;
 }
 
 void build_splan(Side& sd, cudaStream_t st) {
@@ -522,8 +537,8 @@ lx::ms::MainArgs<R> main_args(const View<R>& v, int rows) {
     a.cpsi = v.cpsi;
     a.spsi = v.spsi;
     a.inv_t = v.inv_t;
-    a.gshift_a = bucket_shift(v.n);
-    a.gshift_b = bucket_shift(v.k);
+    a.gmap_a = v.gm_a;
+    a.gmap_b = v.gm_b;
     return a;
 }
 

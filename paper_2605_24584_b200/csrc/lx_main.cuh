@@ -49,6 +49,7 @@ struct MainStage {
     alignas(16) R anch[kTile + 4 * kPad];   // A range at [offA], B range at [baseB + offB]
     alignas(16) R pay[kTile + 4 * kPad];    // row payloads, same layout
     alignas(16) uint32_t oidx[kTile + 16];  // output index ranges: A at [offIA], B at [baseIB + offIB]
+    alignas(16) uint16_t gm[kTile + 32];    // store order (lx_group_plan): A at [offGA], B at [baseGB]
 };
 
 constexpr int kMainStages = 2;
@@ -56,11 +57,6 @@ constexpr int kMainStages = 2;
 template <class R, int NC, int NW, int NACC>
 struct MainShared {
     MainStage<R, NC> st[kMainStages];
-    // store grouping of the current tile: gmap[side][k] = side-local index of
-    // the k-th element in output-bucket order; gcnt = bucket counters
-    uint16_t gmap[2][kTile];
-    uint32_t gcnt[2][kGroupBuckets];
-    uint32_t gwarp[2][NW];
     // backward: a_bar at [li], b_bar at [na + li] (and phi_bar / psi_bar),
     // accumulated over the batch rows by the element's owning thread
     R acc[NACC > 0 ? NACC : 1][kTile];
@@ -74,9 +70,9 @@ template <class R>
 struct TileGeom {
     uint32_t a0, b0;
     int na, nb;
-    int offA, baseB, offIA, baseIB;  // element offsets inside anch/pay and oidx
-    uint32_t bytesA, bytesB, ibytesA, ibytesB;
-    uint32_t a0al, b0al, a0i, b0i;
+    int offA, baseB, offIA, baseIB, offGA, baseGB;  // element offsets inside anch/pay, oidx, gm
+    uint32_t bytesA, bytesB, ibytesA, ibytesB, gbytesA, gbytesB;
+    uint32_t a0al, b0al, a0i, b0i, a0g, b0g;
     __device__ __forceinline__ void init(uint32_t a0_, uint32_t b0_, int na_, int nb_, bool outA, bool outB) {
         constexpr int kPad = 16 / sizeof(R);
         a0 = a0_;
@@ -97,6 +93,13 @@ struct TileGeom {
         ibytesA = (outA && na) ? (uint32_t)(((offIA + na + 3) / 4) * 16) : 0u;
         ibytesB = (outB && nb) ? (uint32_t)(((offIB + nb + 3) / 4) * 16) : 0u;
         baseIB = (int)(ibytesA / 4) + offIB;
+        a0g = a0 & ~7u;  // u16 store order: 8-element alignment
+        b0g = b0 & ~7u;
+        offGA = (int)(a0 - a0g);
+        const int offGB = (int)(b0 - b0g);
+        gbytesA = (outA && na) ? (uint32_t)(((offGA + na + 7) / 8) * 16) : 0u;
+        gbytesB = (outB && nb) ? (uint32_t)(((offGB + nb + 7) / 8) * 16) : 0u;
+        baseGB = (int)(gbytesA / 2) + offGB;
     }
 };
 
@@ -130,11 +133,13 @@ __device__ __forceinline__ void issue_tile(MainStage<R, NC>& S, const MainArgs<R
     S.s_last = dt.s_last;
     S.SL = SL;
     S.SR = dn.s_first;
-    mbar_expect_tx(&S.bar, g.bytesA + g.bytesB + g.ibytesA + g.ibytesB);
+    mbar_expect_tx(&S.bar, g.bytesA + g.bytesB + g.ibytesA + g.ibytesB + g.gbytesA + g.gbytesB);
     if (g.bytesA) bulk_g2s(S.anch, p.A + g.a0al, g.bytesA, &S.bar);
     if (g.bytesB) bulk_g2s(S.anch + (g.bytesA / sizeof(R)), p.B + g.b0al, g.bytesB, &S.bar);
     if (g.ibytesA) bulk_g2s(S.oidx, p.perm_a + g.a0i, g.ibytesA, &S.bar);
     if (g.ibytesB) bulk_g2s(S.oidx + g.ibytesA / 4, p.perm_b + g.b0i, g.ibytesB, &S.bar);
+    if (g.gbytesA) bulk_g2s(S.gm, p.gmap_a + g.a0g, g.gbytesA, &S.bar);
+    if (g.gbytesB) bulk_g2s(S.gm + g.gbytesA / 2, p.gmap_b + g.b0g, g.gbytesB, &S.bar);
     const R* srcA = SEQ ? p.Xs : p.Gs;
     mbar_expect_tx(&S.barp, (PAY_A ? g.bytesA : 0u) + (PAY_B ? g.bytesB : 0u));
     if (PAY_A && g.bytesA) bulk_g2s(S.pay, srcA + g.a0al, g.bytesA, &S.barp);
@@ -199,7 +204,6 @@ __global__ void __launch_bounds__(TPB + 32, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS 
     // of the producer warp claims a tile, loads its descriptors, waits for a
     // free stage and stages the tile by TMA; its latencies never stall the
     // consumers, which synchronise among themselves on named barrier 1.
-    for (int i = tid; i < 2 * kGroupBuckets; i += blockDim.x) (&sm.gcnt[0][0])[i] = 0u;
     if (tid == 0) {
         for (int s = 0; s < kMainStages; ++s) {
             mbar_init(&sm.st[s].bar, 1);
@@ -255,8 +259,8 @@ __global__ void __launch_bounds__(TPB + 32, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS 
         const R* pB = S.pay + g.baseB;
         const uint32_t* iA = S.oidx + g.offIA;
         const uint32_t* iB = S.oidx + g.baseIB;
-        if constexpr (OUT_A || OUT_B)
-            group_tile<TPB, NW, OUT_A, OUT_B, 1>(sm.gmap, sm.gcnt, sm.gwarp, iA, na, p.gshift_a, iB, nb, p.gshift_b, tid);
+        const uint16_t* gmA = S.gm + g.offGA;  // store order of the tile rows / cols
+        const uint16_t* gmB = S.gm + g.baseGB;
 
         // ---- merge: anchors and kinds of this thread's IPT elements ----
         R s[IPT];
@@ -727,19 +731,19 @@ __global__ void __launch_bounds__(TPB + 32, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS 
                 if constexpr (!BWD && NX > 0) {
                     R* y = p.y + (size_t)r * p.ldy;
                     for (int k = tid; k < na; k += TPB) {
-                        const int li = sm.gmap[0][k];
+                        const int li = gmA[k];
                         y[LXO(iA[li], g.a0 + li)] = stg[li];
                     }
                 } else if constexpr (!BWD) {
                     R* y = p.y + (size_t)r * p.ldy;
                     for (int k = tid; k < nb; k += TPB) {
-                        const int li = sm.gmap[1][k];
+                        const int li = gmB[k];
                         y[LXO(iB[li], g.b0 + li)] = stg[li];
                     }
                 } else {
                     R* xb = p.xbar + (size_t)r * p.ldxb;
                     for (int k = tid; k < nb; k += TPB) {
-                        const int li = sm.gmap[1][k];
+                        const int li = gmB[k];
                         xb[LXO(iB[li], g.b0 + li)] = stg[li];
                     }
                 }
@@ -750,13 +754,13 @@ __global__ void __launch_bounds__(TPB + 32, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS 
             const uint32_t* iA = S.oidx + g.offIA;
             const uint32_t* iB = S.oidx + g.baseIB;
             for (int k = tid; k < na; k += TPB) {
-                const int li = sm.gmap[0][k];
+                const int li = gmA[k];
                 const uint32_t u = LXO(iA[li], g.a0 + li);
                 p.abar[u] = sm.acc[0][li];
                 if constexpr (PHASED) p.phibar[u] = sm.acc[NACC - 1][li];
             }
             for (int k = tid; k < nb; k += TPB) {
-                const int li = sm.gmap[1][k];
+                const int li = gmB[k];
                 const uint32_t u = LXO(iB[li], g.b0 + li);
                 p.bbar[u] = sm.acc[0][na + li];
                 if constexpr (PHASED) p.psibar[u] = sm.acc[NACC - 1][na + li];

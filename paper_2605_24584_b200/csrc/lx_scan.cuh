@@ -175,7 +175,10 @@ struct MainArgs {
     const uint32_t* perm_b;
     const uint32_t* part;  // T+1 row offsets of the merged tiles
     uint32_t* tile_ctr;    // zeroed tile counter (lx_main's in-order tile schedule)
-    int gshift_a, gshift_b;  // output-position bucket = position >> gshift (store grouping)
+    // per-tile store order (lx_group_plan): gmap_a[a0 + k] = row-local index of
+    // the k-th tile row in output-bucket order (likewise gmap_b for cols)
+    const uint16_t* gmap_a;
+    const uint16_t* gmap_b;
     const TileDesc<R>* desc;  // T+1 tile descriptors
     uint32_t n, k, T;
     int rows;
@@ -299,6 +302,34 @@ __device__ __forceinline__ void group_tile(uint16_t (&gmap)[2][kTile], uint32_t 
     gbar<TPB, BAR>();
     if (SA) gcnt[0][tid] = 0u;  // ready for the next tile (read again only after later barriers)
     if (SB) gcnt[1][tid] = 0u;
+}
+
+// Plan-time store order of every merge tile (both sides), consumed by lx_main:
+// the grouping depends only on the plan (positions and tiles), so it is built
+// once per plan orientation instead of in every apply / backward.
+template <class R>
+__global__ void __launch_bounds__(kGroupBuckets) lx_group_plan(const TileDesc<R>* __restrict__ desc, uint32_t T,
+                                                               const uint32_t* __restrict__ posA, int shA,
+                                                               const uint32_t* __restrict__ posB, int shB,
+                                                               uint16_t* __restrict__ gA, uint16_t* __restrict__ gB) {
+    constexpr int TPB = kGroupBuckets, NW = TPB / 32;
+    __shared__ uint32_t sA[kTile], sB[kTile];
+    __shared__ uint16_t gmap[2][kTile];
+    __shared__ uint32_t gcnt[2][kGroupBuckets];
+    __shared__ uint32_t gwarp[2][NW];
+    const int tid = threadIdx.x;
+    const uint32_t t = blockIdx.x;
+    const TileDesc<R> dt = desc[t], dn = desc[t + 1];
+    const uint32_t a0 = dt.a0, b0 = dt.b0;
+    const int na = (int)(dn.a0 - a0), nb = (int)(dn.b0 - b0);
+    for (int i = tid; i < na; i += TPB) sA[i] = posA[a0 + i];
+    for (int i = tid; i < nb; i += TPB) sB[i] = posB[b0 + i];
+    gcnt[0][tid] = 0u;
+    gcnt[1][tid] = 0u;
+    __syncthreads();
+    group_tile<TPB, NW, true, true, 0>(gmap, gcnt, gwarp, sA, na, shA, sB, nb, shB, tid);
+    for (int k = tid; k < na; k += TPB) gA[a0 + k] = gmap[0][k];
+    for (int k = tid; k < nb; k += TPB) gB[b0 + k] = gmap[1][k];
 }
 
 // ---------------------------------------------------------------------------
