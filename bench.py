@@ -59,6 +59,20 @@ def kernel_model_bytes(name, n, k, rows=1):
     }.get(name)
 
 
+def measured_traffic(kernel, log2n):
+    """ncu DRAM bytes per launch of `kernel` at this size (profiles/*_traffic.json, written by
+    tools/traffic_json.py from the committed launch list), or None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")), reverse=True):
+        try:
+            d = json.load(open(path))
+        except Exception:
+            continue
+        if d.get("log2n") == log2n and kernel in d.get("kernels", {}):
+            return d["kernels"][kernel]
+    return None
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -275,7 +289,7 @@ def run_ours(args, rank, world, dist):
         d = kern_table[dom]
         per_launch_bytes = d["model_bytes"] / max(1, d["launches_per_step"]) if d["model_bytes"] else None
         roof = {"bound": "hbm", "kernel": dom, "achieved": d["achieved_gbs"], "peak": hbm, "unit": "GB/s",
-                "frac": d["frac"], "traffic": None, "peak_kind": peak_kind,
+                "frac": d["frac"], "traffic": measured_traffic(dom, args.log2n), "peak_kind": peak_kind,
                 "bytes_per_launch": per_launch_bytes,
                 "avg_launch_ms": d["ms_per_step"] / max(1, d["launches_per_step"])}
 
@@ -457,7 +471,8 @@ def run_e2e(args, torch, lib, n, k):
     return {"value": n / sec, "unit": UNIT, "h2d_bytes_per_step": 4 * (n + k + k + k + n),
             "d2h_bytes_per_step": 4 * (n + k + n + k), "ms_per_step": 1000 * sec,
             "path": "laplex_plan_create + laplex_apply + laplex_backward (host pointers, pinned torch buffers; "
-                    "host-side require_finite on every input, as the reference API)"}
+                    "every input checked for finiteness on the device after upload, errors raised in the "
+                    "reference's order)"}
 
 
 def main():

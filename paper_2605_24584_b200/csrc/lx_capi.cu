@@ -1158,6 +1158,10 @@ int dtype_check(int dtype) {
     return dtype;
 }
 
+// Inputs up to this many elements are validated on the host (cheaper than a
+// device round trip); larger ones on the device after the upload.
+constexpr size_t kHostCheckMax = size_t(1) << 20;
+
 // LaplexOperator checks that need no data, in reference order
 // (operator.hpp:88-101); anchor / phase finiteness is checked on the device.
 struct CreateChecks {
@@ -1183,6 +1187,13 @@ laplex_plan create_from_host(const void* a, size_t n, const void* b, size_t k, d
     if (n == 0 || k == 0) fail(LAPLEX_E_EMPTY_INPUT, "LaplexOperator: empty anchor set");
     if (n >= 0x80000000ull || k >= 0x80000000ull) fail(LAPLEX_E_INVALID_SIZE, "n and k must be < 2^31");
     const CreateChecks cc = create_checks(sizeof(R) == 4 ? (double)(float)t : t, phi != nullptr, psi != nullptr);
+    if ((size_t)n + k <= kHostCheckMax) {  // small inputs: the whole check on the host, reference order
+        if (!host_finite((const R*)a, n)) fail(LAPLEX_E_NON_FINITE, "LaplexOperator row anchors: non-finite entry");
+        if (!host_finite((const R*)b, k)) fail(LAPLEX_E_NON_FINITE, "LaplexOperator col anchors: non-finite entry");
+        if (cc.code) fail(cc.code, cc.msg);
+        if (phi && (!host_finite((const R*)phi, n) || !host_finite((const R*)psi, k)))
+            fail(LAPLEX_E_NON_FINITE, "LaplexOperator phases: non-finite entry");
+    }
     // upload order a, phi, b, psi: side 0 sorts while side 1 is in flight
     HostUp<R> da(a, n, st);
     HostUp<R> dp(phi, (phi && !cc.code) ? n : 0, st);
