@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(TPB + 32, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS 
             for (int it = 0;; ++it) {
                 const int s = it % kMainStages;
                 const uint32_t use = (uint32_t)(it / kMainStages);
-                if (it >= kMainStages) mbar_wait(&sm.st[s].empty, (use - 1u) & 1u);
+                if (it >= kMainStages) mbar_wait_sleep(&sm.st[s].empty, (use - 1u) & 1u);
                 issue_tile<R, NC, SEQ, PAY_A, PAY_B, OUT_A, OUT_B, C>(sm.st[s], p, tc, d0, d1, sl);
                 if (tc >= T) break;
                 claim(tc, d0, d1, sl);

@@ -13,7 +13,12 @@ h = rows[hdr]
 per_id = collections.OrderedDict()
 for r in rows[hdr + 1:]:
     d = dict(zip(h, r))
-    name = d["Kernel Name"].split("(")[0].replace("void ", "").strip().split("<")[0].split("::")[-1]
+    full = d["Kernel Name"]
+    name = full.split("(")[0].replace("void ", "").strip().split("<")[0].split("::")[-1]
+    if name == "lx_sort_pass" and full.replace(" ", "").split("(")[0].endswith(",1>"):
+        name = "lx_splan"  # the plan pass runs the sort-pass kernel with SPLAN = true
+    if not name:
+        continue  # input generation (torch) in the profiled script
     v = float(d["Metric Value"].replace(",", "")) if d["Metric Value"] else 0.0
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(d.get("Metric Unit", ""), 1)
     e = per_id.setdefault(d["ID"], {"name": name, "bytes": 0.0})
