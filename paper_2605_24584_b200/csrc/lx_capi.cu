@@ -434,14 +434,42 @@ DBuf stage_gather(const R* src, size_t ld, const uint32_t* dst, uint32_t m, int 
     return out;
 }
 
+// Host-pointer API: finished caller-order output ranges are handed to this
+// hook as the scatter completes them, so their device->host copies overlap
+// the rest of the scatter (and of the call).  Set per thread by the host API.
+struct OutHook {
+    std::function<void(const void* dev, size_t u0, size_t u1, int rows, size_t ld, cudaStream_t st)> fn;
+};
+thread_local OutHook* g_out_hook = nullptr;
+
 template <class R>
 void stage_scatter(const uint32_t* dst, uint32_t m, const R* s1, R* o1, size_t ld1, int rows1, const R* s2, R* o2,
                    const R* s3, R* o3, cudaStream_t st) {
     using namespace lx::sort;
     const uint32_t chunks = (m + kPermChunk - 1) / kPermChunk;
-    launch("lx_perm_scatter", st, [&] {
-        lx_perm_stage_scatter<R><<<chunks, kPermThreads, 0, st>>>(dst, m, s1, o1, ld1, rows1, s2, o2, s3, o3);
-    });
+    if (!g_out_hook) {
+        launch("lx_perm_scatter", st, [&] {
+            lx_perm_stage_scatter<R><<<chunks, kPermThreads, 0, st>>>(dst, m, s1, o1, ld1, rows1, s2, o2, s3, o3, 0u);
+        });
+        return;
+    }
+    // groups of whole caller windows (bucket w holds exactly the caller
+    // indices [w << shift, (w + 1) << shift), at the same bucketed positions)
+    const int shift = bucket_shift(m);
+    const uint32_t W = (uint32_t)(((uint64_t)m + (1ull << shift) - 1) >> shift);
+    const uint32_t G = std::min<uint32_t>(W, 8u);
+    for (uint32_t gi = 0; gi < G; ++gi) {
+        const uint64_t u0 = ((uint64_t)(gi * W / G)) << shift;
+        const uint64_t u1 = std::min<uint64_t>(((uint64_t)((gi + 1) * W / G)) << shift, m);
+        if (u1 <= u0) continue;
+        const uint32_t b0 = (uint32_t)(u0 / kPermChunk), b1 = (uint32_t)((u1 + kPermChunk - 1) / kPermChunk);
+        launch("lx_perm_scatter", st, [&] {
+            lx_perm_stage_scatter<R><<<b1 - b0, kPermThreads, 0, st>>>(dst, m, s1, o1, ld1, rows1, s2, o2, s3, o3, b0);
+        });
+        g_out_hook->fn(o1, u0, u1, rows1, ld1, st);
+        if (s2) g_out_hook->fn(o2, u0, u1, 1, m, st);
+        if (s3) g_out_hook->fn(o3, u0, u1, 1, m, st);
+    }
 }
 
 // any non-finite entry of v[0, m) sets *bad (host-pointer API validation,
@@ -1130,20 +1158,124 @@ struct HostUp {
 };
 
 // Device flags of the host-pointer API's finiteness checks (one int each).
+// snapshot() copies them to a per-thread pinned buffer behind the checks on
+// the stream; wait() blocks only until that copy, not the whole stream.
 struct Flags {
     DBuf d;
     int n;
+    int* h;
+    cudaEvent_t ev = nullptr;
     Flags(int n_, cudaStream_t st) : d(sizeof(int) * n_, st), n(n_) {
+        thread_local int* pinned = [] {
+            int* q = nullptr;
+            ck(cudaMallocHost(&q, 64 * sizeof(int)), "cudaMallocHost");
+            return q;
+        }();
+        h = pinned;
         ck(cudaMemsetAsync(d.p, 0, sizeof(int) * n_, st), "memset");
+        ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+    }
+    Flags(const Flags&) = delete;
+    Flags& operator=(const Flags&) = delete;
+    ~Flags() {
+        if (ev) cudaEventDestroy(ev);
     }
     int* at(int i) const { return d.as<int>() + i; }
-    // synchronises st; returns the host copy
-    std::vector<int> read(cudaStream_t st) const {
-        std::vector<int> h(n);
-        ck(cudaMemcpyAsync(h.data(), d.p, sizeof(int) * n, cudaMemcpyDeviceToHost, st), "D2H");
-        ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    void snapshot(cudaStream_t st) {
+        ck(cudaMemcpyAsync(h, d.p, sizeof(int) * n, cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaEventRecord(ev, st), "cudaEventRecord");
+    }
+    const int* wait() const {
+        ck(cudaEventSynchronize(ev), "cudaEventSynchronize");
         return h;
     }
+    // synchronises st; returns the host copy
+    std::vector<int> read(cudaStream_t st) {
+        snapshot(st);
+        wait();
+        return std::vector<int>(h, h + n);
+    }
+};
+
+// Downloads of the host-pointer API: a per-thread stream, so device->host
+// copies of finished output ranges overlap the remaining device work.
+cudaStream_t download_stream() {
+    thread_local cudaStream_t s = [] {
+        cudaStream_t x = nullptr;
+        ck(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking), "cudaStreamCreate");
+        return x;
+    }();
+    return s;
+}
+
+// Routes finished output ranges to the caller's host buffers.  The first
+// range waits for the input-finiteness flags (fail() before any host write).
+struct Downloader {
+    struct Map {
+        const void* dev;
+        void* host;
+        size_t count;  // elements per row
+        int rows;
+        bool streamed;
+    };
+    std::vector<Map> maps;
+    size_t rsz;
+    std::function<void()> check;
+    bool checked = false;
+    OutHook hook;
+    cudaStream_t dl = download_stream();
+    std::vector<cudaEvent_t> evs;
+    explicit Downloader(size_t rs) : rsz(rs) {
+        hook.fn = [this](const void* dev, size_t u0, size_t u1, int rows, size_t ld, cudaStream_t st) {
+            copy(dev, u0, u1, rows, ld, st);
+        };
+    }
+    Downloader(const Downloader&) = delete;
+    Downloader& operator=(const Downloader&) = delete;
+    ~Downloader() {
+        for (auto e : evs) cudaEventDestroy(e);
+    }
+    // device output [rows][count] (row pitch = count) -> host buffer of the same shape
+    void add(const void* dev, void* host, size_t count, int rows) {
+        if (dev && host && count) maps.push_back({dev, host, count, rows, false});
+    }
+    void run_check() {
+        if (!checked) {
+            checked = true;
+            if (check) check();
+        }
+    }
+    void copy(const void* dev, size_t u0, size_t u1, int rows, size_t ld, cudaStream_t st) {
+        run_check();
+        for (Map& mp : maps) {
+            if (mp.dev != dev) continue;
+            mp.streamed = true;
+            cudaEvent_t e;
+            ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+            evs.push_back(e);
+            ck(cudaEventRecord(e, st), "cudaEventRecord");
+            ck(cudaStreamWaitEvent(dl, e, 0), "cudaStreamWaitEvent");
+            ck(cudaMemcpy2DAsync((char*)mp.host + u0 * rsz, mp.count * rsz, (const char*)dev + u0 * rsz, ld * rsz,
+                                 (u1 - u0) * rsz, (size_t)rows, cudaMemcpyDeviceToHost, dl),
+               "D2H");
+        }
+    }
+    // outputs the scatter did not stream (direct permutations): whole copies; then wait
+    void finish(cudaStream_t st) {
+        run_check();
+        for (Map& mp : maps)
+            if (!mp.streamed) {
+                mp.streamed = true;
+                ck(cudaMemcpyAsync(mp.host, mp.dev, mp.count * mp.rows * rsz, cudaMemcpyDeviceToHost, st), "D2H");
+            }
+        ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        ck(cudaStreamSynchronize(dl), "cudaStreamSynchronize");
+    }
+};
+
+struct HookScope {  // installs the downloader's hook for the calling thread
+    explicit HookScope(OutHook* h) { g_out_hook = h; }
+    ~HookScope() { g_out_hook = nullptr; }
 };
 
 cudaStream_t host_stream() { return cudaStreamPerThread; }
@@ -1426,10 +1558,17 @@ int laplex_apply(laplex_plan plan, unsigned flags, const void* X, size_t rows, s
             Flags f(1, st);
             dx.wait(st);
             launch_finite<R>(dx.get(), rows * cols, f.at(0), st);
-            do_apply<R>(plan, flags, dx.get(), rows, dy.as<R>(), st);
-            if (f.read(st)[0]) fail(LAPLEX_E_NON_FINITE, "matvec x: non-finite entry");
-            d2h<R>(Y, dy, rows * out_len, st);
-            ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+            f.snapshot(st);
+            Downloader dl(sizeof(R));
+            dl.check = [&] {
+                if (f.wait()[0]) fail(LAPLEX_E_NON_FINITE, "matvec x: non-finite entry");
+            };
+            dl.add(dy.p, Y, out_len, (int)rows);
+            {
+                HookScope hs(&dl.hook);
+                do_apply<R>(plan, flags, dx.get(), rows, dy.as<R>(), st);
+            }
+            dl.finish(st);
         };
         if (c.dtype == LAPLEX_F64)
             run(0.0);
@@ -1476,22 +1615,29 @@ int laplex_backward(laplex_plan plan, unsigned flags, const void* X, size_t rows
             Flags f(2, st);
             dx.wait(st);
             launch_finite<R>(dx.get(), rows * k, f.at(0), st);
-            do_backward<R>(plan, flags, dx.get(), dg.get(), rows, xb.as<R>(), ab.as<R>(), bb.as<R>(), pb.as<R>(),
-                           qb.as<R>(), st, [&] {
-                               dg.wait(st);
-                               launch_finite<R>(dg.get(), rows * n, f.at(1), st);
-                           });
-            const auto h = f.read(st);
-            if (h[0]) fail(LAPLEX_E_NON_FINITE, "matvec_vjp x: non-finite entry");
-            if (h[1]) fail(LAPLEX_E_NON_FINITE, "matvec_vjp g: non-finite entry");
-            d2h<R>(x_bar, xb, rows * k, st);
-            d2h<R>(a_bar, ab, n, st);
-            d2h<R>(b_bar, bb, k, st);
+            Downloader dl(rs);
+            dl.check = [&] {
+                const int* h = f.wait();
+                if (h[0]) fail(LAPLEX_E_NON_FINITE, "matvec_vjp x: non-finite entry");
+                if (h[1]) fail(LAPLEX_E_NON_FINITE, "matvec_vjp g: non-finite entry");
+            };
+            dl.add(xb.p, x_bar, k, (int)rows);
+            dl.add(ab.p, a_bar, n, 1);
+            dl.add(bb.p, b_bar, k, 1);
             if (ph) {
-                d2h<R>(phi_bar, pb, n, st);
-                d2h<R>(psi_bar, qb, k, st);
+                dl.add(pb.p, phi_bar, n, 1);
+                dl.add(qb.p, psi_bar, k, 1);
             }
-            ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+            {
+                HookScope hs(&dl.hook);
+                do_backward<R>(plan, flags, dx.get(), dg.get(), rows, xb.as<R>(), ab.as<R>(), bb.as<R>(),
+                               pb.as<R>(), qb.as<R>(), st, [&] {
+                                   dg.wait(st);
+                                   launch_finite<R>(dg.get(), rows * n, f.at(1), st);
+                                   f.snapshot(st);
+                               });
+            }
+            dl.finish(st);
         };
         if (c.dtype == LAPLEX_F64)
             run(0.0);

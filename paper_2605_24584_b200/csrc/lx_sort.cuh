@@ -37,7 +37,10 @@ constexpr int kBits = 8;
 constexpr int kRadix = 256;
 constexpr int kThreads = 256;  // == kRadix: one look-back lane per digit
 constexpr int kWarps = kThreads / 32;
-constexpr int kItems = 16;
+#ifndef LX_SORT_ITEMS
+#define LX_SORT_ITEMS 16
+#endif
+constexpr int kItems = LX_SORT_ITEMS;
 constexpr int kTile = kThreads * kItems;  // 4096 keys per tile
 
 // look-back status word: [63:62] flag (1 aggregate, 2 inclusive prefix),
@@ -385,8 +388,8 @@ __global__ void __launch_bounds__(kPermThreads) lx_perm_stage_scatter(const uint
                                                                      const R* __restrict__ s1, R* __restrict__ o1,
                                                                      size_t ld1, int rows1, const R* __restrict__ s2,
                                                                      R* __restrict__ o2, const R* __restrict__ s3,
-                                                                     R* __restrict__ o3) {
-    const size_t q0 = (size_t)blockIdx.x * kPermChunk + threadIdx.x;
+                                                                     R* __restrict__ o3, uint32_t block0) {
+    const size_t q0 = (size_t)(blockIdx.x + block0) * kPermChunk + threadIdx.x;
     uint32_t u[kPermItems];
 #pragma unroll
     for (int j = 0; j < kPermItems; ++j) {
