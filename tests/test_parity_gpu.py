@@ -348,7 +348,8 @@ def test_error_taxonomy_on_device_plans():
 
 
 # ------------------------------------------------ fp32 at scale vs fp64
-@pytest.mark.parametrize("lg,span", [(16, 100.0), (20, 100.0), (20, 3.0), (22, 100.0)])
+# 2^23 sides take the permutation-plan path (staged outputs, per-tile store order)
+@pytest.mark.parametrize("lg,span", [(16, 100.0), (20, 100.0), (20, 3.0), (22, 100.0), (23, 100.0)])
 def test_fp32_against_fp64_oracle(lg, span):
     rng = np.random.default_rng(lg)
     N = 1 << lg
@@ -415,3 +416,32 @@ def test_device_plan_reports_nonfinite_anchor():
     b = torch.tensor([0.5], device="cuda:0")
     with pytest.raises(L.NonFinite):
         L.DeviceOperator(a, b)
+
+
+# ------------------------------------------------ batch rows on the plan path
+def test_batch_rows_on_plan_path():
+    """Rows > 1 with sides above the direct-permutation limit (2^22): per-row
+    payload staging, store order and the row-summed anchor cotangents."""
+    import torch
+    rng = np.random.default_rng(41)
+    N, B = (1 << 23) + 1234, 3
+    dev = torch.device("cuda:0")
+    a = torch.tensor(rng.uniform(-100, 100, N).astype(F32), device=dev)
+    b = torch.tensor(rng.uniform(-100, 100, N - 777).astype(F32), device=dev)
+    X = torch.tensor(rng.uniform(-1, 1, (B, N - 777)).astype(F32), device=dev)
+    G = torch.tensor(rng.uniform(-1, 1, (B, N)).astype(F32), device=dev)
+    op = L.DeviceOperator(a, b, 1.0)
+    Y = op.apply(X)
+    xb, ab, bb, _, _ = op.backward(X, G)
+    for r in range(B):  # batch row r == single-row call, bitwise (tests/test_operator.cpp:120-132)
+        assert torch.equal(Y[r], op.apply(X[r:r + 1])[0])
+        xr, ar, br, _, _ = op.backward(X[r:r + 1], G[r:r + 1])
+        assert torch.equal(xb[r], xr[0])
+    # anchor cotangents are sums over rows
+    parts = [op.backward(X[r:r + 1], G[r:r + 1]) for r in range(B)]
+    sa = sum(p[1].double() for p in parts)
+    sb = sum(p[2].double() for p in parts)
+    assert O.rel_err_l2(ab.double().cpu().numpy(), sa.cpu().numpy()) <= 1e-6
+    assert O.rel_err_l2(bb.double().cpu().numpy(), sb.cpu().numpy()) <= 1e-6
+    # x_bar of the VJP is the transpose, bitwise (SPEC.md:242)
+    assert torch.equal(xb, op.apply(G, transpose=True))
