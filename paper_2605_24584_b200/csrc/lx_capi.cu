@@ -301,6 +301,14 @@ View<R> view(Core& c, bool swapped, cudaStream_t st) {
 }
 
 // ---- sort -------------------------------------------------------------------
+// Pass structure: reduce-then-scan (count kernel + per-digit tile scan, then a
+// pass with known offsets) unless LX_SORT_LOOKBACK selects onesweep's
+// decoupled look-back.
+#ifdef LX_SORT_LOOKBACK
+constexpr bool kSortRts = false;
+#else
+constexpr bool kSortRts = true;
+#endif
 template <class R>
 void radix_sort(const R* raw, uint32_t m, R t, R* vals_out, uint32_t* perm_out, int* bad, cudaStream_t st) {
     using namespace lx::sort;
@@ -311,10 +319,11 @@ void radix_sort(const R* raw, uint32_t m, R t, R* vals_out, uint32_t* perm_out, 
     DBuf counters((size_t)P * 4, st);
     DBuf keys0((size_t)m * sizeof(K), st), keys1((size_t)m * sizeof(K), st);
     DBuf v0((size_t)m * 4, st), v1((size_t)m * 4, st);
-    DBuf look((size_t)tiles * kRadix * 8, st);
+    DBuf look(kSortRts ? 8 : (size_t)tiles * kRadix * 8, st);
+    DBuf cnt(kSortRts ? (size_t)tiles * kRadix * 4 : 4, st);
     ck(cudaMemsetAsync(hist.p, 0, (size_t)P * kRadix * 4, st), "memset");
     ck(cudaMemsetAsync(counters.p, 0, (size_t)P * 4, st), "memset");
-    ck(cudaMemsetAsync(look.p, 0, (size_t)tiles * kRadix * 8, st), "memset");
+    if (!kSortRts) ck(cudaMemsetAsync(look.p, 0, (size_t)tiles * kRadix * 8, st), "memset");
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const uint32_t per_block = kHistThreads * kHistItems;
@@ -343,16 +352,30 @@ void radix_sort(const R* raw, uint32_t m, R t, R* vals_out, uint32_t* perm_out, 
         uint32_t* ctr = counters.as<uint32_t>() + pass;
         unsigned long long* lb = look.as<unsigned long long>();
         const uint32_t epoch = (uint32_t)pass + 1;
+        const uint32_t* offs = nullptr;
+        if (kSortRts) {  // per-(digit, tile) offsets first: the pass needs no look-back
+            launch("lx_sort_count", st, [&] {
+                if (pass == 0)
+                    lx_sort_count<R, true, false><<<tiles, kThreads, 0, st>>>(in, m, t, 0, cnt.as<uint32_t>());
+                else
+                    lx_sort_count<R, false, false><<<tiles, kThreads, 0, st>>>(in, m, t, pass * kBits,
+                                                                               cnt.as<uint32_t>());
+            });
+            launch("lx_sort_scan", st, [&] {
+                lx_sort_scan<<<kRadix, kScanThreads, 0, st>>>(cnt.as<uint32_t>(), tiles, bptr, 0);
+            });
+            offs = cnt.as<uint32_t>();
+        }
         launch("lx_sort_pass", st, [&] {
             if (pass == 0)
                 lx_sort_pass<R, true, false><<<tiles, kThreads, smem, st>>>(in, inv, out, outv, m, t, pass * kBits,
-                                                                           bptr, lb, ctr, epoch);
+                                                                           bptr, lb, ctr, epoch, offs);
             else if (!last)
                 lx_sort_pass<R, false, false><<<tiles, kThreads, smem, st>>>(in, inv, out, outv, m, t, pass * kBits,
-                                                                            bptr, lb, ctr, epoch);
+                                                                            bptr, lb, ctr, epoch, offs);
             else
                 lx_sort_pass<R, false, true><<<tiles, kThreads, smem, st>>>(in, inv, out, outv, m, t, pass * kBits,
-                                                                           bptr, lb, ctr, epoch);
+                                                                           bptr, lb, ctr, epoch, offs);
         });
         in = out;
         inv = outv;
@@ -375,9 +398,21 @@ void build_splan(Side& sd, cudaStream_t st) {
     const uint32_t tiles = (m + kTile - 1) / kTile;
     sd.spos = DBuf((size_t)m * 4, st);
     sd.sdst = DBuf((size_t)m * 4, st);
-    DBuf look((size_t)tiles * kRadix * 8, st), ctr(4, st);
-    ck(cudaMemsetAsync(look.p, 0, (size_t)tiles * kRadix * 8, st), "memset");
+    DBuf look(kSortRts ? 8 : (size_t)tiles * kRadix * 8, st), ctr(4, st);
+    DBuf cnt(kSortRts ? (size_t)tiles * kRadix * 4 : 4, st);
+    if (!kSortRts) ck(cudaMemsetAsync(look.p, 0, (size_t)tiles * kRadix * 8, st), "memset");
     ck(cudaMemsetAsync(ctr.p, 0, 4, st), "memset");
+    const uint32_t* offs = nullptr;
+    if (kSortRts) {
+        launch("lx_splan_count", st, [&] {
+            lx_sort_count<float, false, true><<<tiles, kThreads, 0, st>>>(sd.perm.p, m, 1.0f, shift,
+                                                                          cnt.as<uint32_t>());
+        });
+        launch("lx_sort_scan", st, [&] {
+            lx_sort_scan<<<kRadix, kScanThreads, 0, st>>>(cnt.as<uint32_t>(), tiles, nullptr, shift);
+        });
+        offs = cnt.as<uint32_t>();
+    }
     const size_t smem = sizeof(PassSmem<float>);
     static std::once_flag once;
     std::call_once(once, [&] {
@@ -387,7 +422,7 @@ void build_splan(Side& sd, cudaStream_t st) {
     launch("lx_splan", st, [&] {
         lx_sort_pass<float, false, false, true><<<tiles, kThreads, smem, st>>>(
             sd.perm.p, nullptr, sd.sdst.p, sd.spos.as<uint32_t>(), m, 1.0f, shift, nullptr,
-            look.as<unsigned long long>(), ctr.as<uint32_t>(), 1u);
+            look.as<unsigned long long>(), ctr.as<uint32_t>(), 1u, offs);
     });
     sd.staged = true;
 }

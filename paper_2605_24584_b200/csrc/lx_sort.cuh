@@ -152,7 +152,8 @@ __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict_
                                                         uint32_t* __restrict__ out_vals, size_t n, R t,
                                                         int shift, const uint32_t* __restrict__ bases,
                                                         unsigned long long* __restrict__ lookback,
-                                                        uint32_t* __restrict__ tile_counter, uint32_t epoch) {
+                                                        uint32_t* __restrict__ tile_counter, uint32_t epoch,
+                                                        const uint32_t* __restrict__ offs = nullptr) {
     using K = typename Traits<R>::Key;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     PassSmem<R>& sm = *reinterpret_cast<PassSmem<R>*>(smem_raw);
@@ -161,8 +162,11 @@ __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict_
     const int lane = tid & 31;
     constexpr bool HAS_VALS = !FIRST && !SPLAN;
 
+    // offs (reduce-then-scan mode): global output offset of every (digit, tile),
+    // digit-major [kRadix][gridDim.x], from lx_sort_count + lx_sort_scan; the
+    // tile is then blockIdx.x and there is no look-back
     if (tid == 0) {
-        sm.tile = atomicAdd(tile_counter, 1u);
+        sm.tile = offs ? blockIdx.x : atomicAdd(tile_counter, 1u);
         mbar_init(&sm.bar, 1);
         fence_mbar_init();
     }
@@ -264,7 +268,7 @@ __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict_
         sm.whist[w][d] = count;
         count += c;
     }
-    st_relaxed_u64(my_status, status(tile == 0 ? kFlagInc : kFlagAgg, epoch, count));
+    if (!offs) st_relaxed_u64(my_status, status(tile == 0 ? kFlagInc : kFlagAgg, epoch, count));
 #endif
 
     // block exclusive scan of counts over digits -> shared-memory positions
@@ -282,6 +286,13 @@ __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict_
         if (w < warp) wpre += sm.scan[w];
     const uint32_t dstart = wpre + incl - count;
 
+    if (offs) {  // reduce-then-scan: the offset is known
+        sm.dstart[d] = dstart;
+        sm.gbase[d] = offs[(size_t)d * gridDim.x + tile] - dstart;
+        __syncthreads();
+        goto scatter;
+    }
+    {
     // ---- decoupled look-back (one lane per digit) ----
     uint32_t excl = 0;
     if (tile > 0) {
@@ -303,6 +314,8 @@ __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict_
     else
         sm.gbase[d] = bases[d] + excl - dstart;
     __syncthreads();
+    }
+scatter:
 
     // ---- scatter into shared memory in digit order ----
 #pragma unroll
@@ -340,6 +353,95 @@ __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict_
             reinterpret_cast<K*>(out_keys)[o] = kk;
             out_vals[o] = sm.ov[i];
         }
+    }
+}
+
+// ---- reduce-then-scan form of a pass (no look-back) --------------------------
+// lx_sort_count: per-tile digit counts of the pass (the same tiles and digit
+// function as lx_sort_pass), digit-major cnt[d * tiles + tile].
+template <class R, bool FIRST, bool SPLAN>
+__global__ void __launch_bounds__(kThreads) lx_sort_count(const void* __restrict__ in_keys, size_t n, R t, int shift,
+                                                         uint32_t* __restrict__ cnt) {
+    using K = typename Traits<R>::Key;
+    __shared__ uint32_t wh[kWarps][kRadix];
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < kWarps * kRadix; i += kThreads) (&wh[0][0])[i] = 0;
+    __syncthreads();
+    const size_t tile_start = (size_t)blockIdx.x * kTile;
+    const K* gk = reinterpret_cast<const K*>(in_keys);
+    constexpr int kV = 16 / sizeof(K);  // keys per 16-byte vector
+    constexpr int kVec = kItems / kV;   // vectors per thread
+    const bool full = tile_start + kTile <= n && (reinterpret_cast<uintptr_t>(gk) & 15) == 0;
+    if (full) {
+        uint4 q4[kVec];
+#pragma unroll
+        for (int j = 0; j < kVec; ++j)
+            q4[j] = reinterpret_cast<const uint4*>(gk + tile_start)[(size_t)j * kThreads + tid];
+#pragma unroll
+        for (int j = 0; j < kVec; ++j) {
+            const K* kk = reinterpret_cast<const K*>(&q4[j]);
+#pragma unroll
+            for (int e = 0; e < kV; ++e) {
+                K key = kk[e];
+                if constexpr (FIRST) key = radix_key<R>(xdiv(from_bits(key, R(0)), t));
+                atomicAdd(&wh[warp][(int)((key >> shift) & (kRadix - 1))], 1u);
+            }
+        }
+    } else {
+        for (int q = 0; q < kItems; ++q) {
+            const size_t i = tile_start + (size_t)q * kThreads + tid;
+            if (i >= n) continue;
+            K key = gk[i];
+            if constexpr (FIRST) key = radix_key<R>(xdiv(from_bits(key, R(0)), t));
+            atomicAdd(&wh[warp][(int)((key >> shift) & (kRadix - 1))], 1u);
+        }
+    }
+    __syncthreads();
+    uint32_t c = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) c += wh[w][tid];
+    cnt[(size_t)tid * gridDim.x + blockIdx.x] = c;
+}
+
+// lx_sort_scan: one CTA per digit; offs[d][tile] = base[d] + sum of the
+// digit's counts in earlier tiles (in place over cnt).  base = bases[d], or
+// d << shift for the plan pass (every caller bucket holds exactly 2^shift).
+// Coalesced: the CTA walks the digit's row in chunks of 4 * kScanThreads.
+constexpr int kScanThreads = 1024;
+__global__ void __launch_bounds__(kScanThreads) lx_sort_scan(uint32_t* __restrict__ cnt, uint32_t tiles,
+                                                            const uint32_t* __restrict__ bases, int shift) {
+    constexpr int NW = kScanThreads / 32;
+    __shared__ uint32_t ws[NW];
+    __shared__ uint32_t carry;
+    const int d = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint32_t* c = cnt + (size_t)d * tiles;
+    if (tid == 0) carry = bases ? bases[d] : ((uint32_t)d << shift);
+    __syncthreads();
+    for (uint32_t base = 0; base < tiles; base += 4 * kScanThreads) {
+        const uint32_t i0 = base + 4 * (uint32_t)tid;
+        uint32_t v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = i0 + j < tiles ? c[i0 + j] : 0u;
+        const uint32_t sum = v[0] + v[1] + v[2] + v[3];
+        uint32_t incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t x = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += x;
+        }
+        if (lane == 31) ws[warp] = incl;
+        __syncthreads();
+        uint32_t before = carry;
+        for (int w = 0; w < warp; ++w) before += ws[w];
+        uint32_t run = before + incl - sum;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (i0 + j < tiles) c[i0 + j] = run;
+            run += v[j];
+        }
+        __syncthreads();  // everyone has read carry and ws
+        if (tid == kScanThreads - 1) carry = run;
+        __syncthreads();
     }
 }
 
