@@ -125,23 +125,19 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
 __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
     asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-// wait with back-off: for a lane that only waits (the main pass's producer),
-// so its polling does not take issue slots from the compute warps
-__device__ __forceinline__ bool mbar_try(unsigned long long* bar, uint32_t parity) {
-    uint32_t ok;
+// wait with a hardware suspend hint: the waiting warp is descheduled until the
+// phase completes (or the hint expires) instead of polling, so a lane that
+// only waits (the main pass's producer) takes no issue slots from compute warps
+__device__ __forceinline__ void mbar_wait_sleep(unsigned long long* bar, uint32_t parity) {
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
-        "mbarrier.try_wait.parity.shared.b64 p, [%1], %2;\n"
-        "selp.u32 %0, 1, 0, p;\n"
-        "}\n"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
+        "WAITS_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra WAITS_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(1000000u)
         : "memory");
-    return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait_sleep(unsigned long long* bar, uint32_t parity) {
-    while (!mbar_try(bar, parity)) __nanosleep(64);
 }
 // 1-D TMA bulk copy global -> shared (16-byte aligned, size % 16 == 0), completes on bar
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {

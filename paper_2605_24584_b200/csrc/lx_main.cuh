@@ -46,8 +46,10 @@ struct MainStage {
     uint32_t a0, b0;
     int na, nb;
     R s_last, SL, SR;  // tile's last anchor, previous tile's last, next tile's first
-    alignas(16) R anch[kTile + 4 * kPad];   // A range at [offA], B range at [baseB + offB]
-    alignas(16) R pay[kTile + 4 * kPad];    // row payloads, same layout
+    // A range at [offA], then a 16-byte gap, B range at [baseB]; the gap and the
+    // tail leave room for the +inf sentinels behind each range (merge)
+    alignas(16) R anch[kTile + 8 * kPad];
+    alignas(16) R pay[kTile + 8 * kPad];  // row payloads, same layout
     alignas(16) uint32_t oidx[kTile + 16];  // output index ranges: A at [offIA], B at [baseIB + offIB]
     alignas(16) uint16_t gm[kTile + 32];    // store order (lx_group_plan): A at [offGA], B at [baseGB]
 };
@@ -85,7 +87,7 @@ struct TileGeom {
         const int offB = (int)(b0 - b0al);
         bytesA = na ? (uint32_t)(((offA + na + kPad - 1) / kPad) * 16) : 0u;
         bytesB = nb ? (uint32_t)(((offB + nb + kPad - 1) / kPad) * 16) : 0u;
-        baseB = (int)(bytesA / sizeof(R)) + offB;
+        baseB = (int)(bytesA / sizeof(R)) + kPad + offB;  // B region after a 16-byte gap
         a0i = a0 & ~3u;
         b0i = b0 & ~3u;
         offIA = (int)(a0 - a0i);
@@ -135,7 +137,7 @@ __device__ __forceinline__ void issue_tile(MainStage<R, NC>& S, const MainArgs<R
     S.SR = dn.s_first;
     mbar_expect_tx(&S.bar, g.bytesA + g.bytesB + g.ibytesA + g.ibytesB + g.gbytesA + g.gbytesB);
     if (g.bytesA) bulk_g2s(S.anch, p.A + g.a0al, g.bytesA, &S.bar);
-    if (g.bytesB) bulk_g2s(S.anch + (g.bytesA / sizeof(R)), p.B + g.b0al, g.bytesB, &S.bar);
+    if (g.bytesB) bulk_g2s(S.anch + (g.bytesA / sizeof(R)) + MainStage<R, NC>::kPad, p.B + g.b0al, g.bytesB, &S.bar);
     if (g.ibytesA) bulk_g2s(S.oidx, p.perm_a + g.a0i, g.ibytesA, &S.bar);
     if (g.ibytesB) bulk_g2s(S.oidx + g.ibytesA / 4, p.perm_b + g.b0i, g.ibytesB, &S.bar);
     if (g.gbytesA) bulk_g2s(S.gm, p.gmap_a + g.a0g, g.gbytesA, &S.bar);
@@ -143,7 +145,8 @@ __device__ __forceinline__ void issue_tile(MainStage<R, NC>& S, const MainArgs<R
     const R* srcA = SEQ ? p.Xs : p.Gs;
     mbar_expect_tx(&S.barp, (PAY_A ? g.bytesA : 0u) + (PAY_B ? g.bytesB : 0u));
     if (PAY_A && g.bytesA) bulk_g2s(S.pay, srcA + g.a0al, g.bytesA, &S.barp);
-    if (PAY_B && g.bytesB) bulk_g2s(S.pay + (g.bytesA / sizeof(R)), p.Xs + g.b0al, g.bytesB, &S.barp);
+    if (PAY_B && g.bytesB)
+        bulk_g2s(S.pay + (g.bytesA / sizeof(R)) + MainStage<R, NC>::kPad, p.Xs + g.b0al, g.bytesB, &S.barp);
 }
 
 // Channel layout: g channels first (c < NG), then x channels.  Strict prefix
@@ -253,8 +256,14 @@ __global__ void __launch_bounds__(TPB + 32, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS 
         const bool hl = t > 0 || has_ext_p, hr = t + 1 < T || has_ext_q;
         const R SL = t > 0 ? S.SL : ext_pa;
         const R SR = t + 1 < T ? S.SR : ext_qa;
-        const R* sA = S.anch + g.offA;
-        const R* sB = S.anch + g.baseB;
+        R* sA = S.anch + g.offA;
+        R* sB = S.anch + g.baseB;
+        const R kInf = R(__int_as_float(0x7f800000));
+        if (tid == 0) {  // +inf behind both ranges: the merge reads past an exhausted side
+            sA[na] = kInf;
+            sB[nb] = kInf;
+        }
+        cbar<TPB>();
         const R* pA = S.pay + g.offA;
         const R* pB = S.pay + g.baseB;
         const uint32_t* iA = S.oidx + g.offIA;
@@ -273,10 +282,10 @@ __global__ void __launch_bounds__(TPB + 32, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS 
             int ib = dd - ia;
             ia0 = ia;
             ib0 = ib;
-            const R kInf = R(__int_as_float(0x7f800000));
-            R av = ia < na ? sA[ia] : kInf, bv = ib < nb ? sB[ib] : kInf;
-            // branch-free: one compare, one shared load per element (an
-            // exhausted side reads as +inf; anchors are finite)
+            R av = sA[ia], bv = sB[ib];  // +inf sentinels behind both ranges
+            // branch-free: one compare and one shared load per element; anchors
+            // are finite, so an exhausted side (+inf) is never taken while the
+            // other has elements
 #pragma unroll
             for (int q = 0; q < IPT; ++q) {
                 const bool takeA = av <= bv;
@@ -284,10 +293,7 @@ __global__ void __launch_bounds__(TPB + 32, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS 
                 rowm |= (unsigned)takeA << q;
                 ia += takeA;
                 ib += !takeA;
-                const int ni = takeA ? ia : ib;
-                const int lim = takeA ? na : nb;
-                const R* base = takeA ? sA : sB;
-                const R nx = ni < lim ? base[ni] : kInf;
+                const R nx = takeA ? sA[ia] : sB[ib];
                 av = takeA ? nx : av;
                 bv = takeA ? bv : nx;
             }
@@ -480,7 +486,8 @@ __global__ void __launch_bounds__(TPB + 32, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS 
                 mbar_expect_tx(&S.barp, (PAY_A ? g.bytesA : 0u) + (PAY_B ? g.bytesB : 0u));
                 if (PAY_A && g.bytesA) bulk_g2s(S.pay, srcA + (size_t)(r + 1) * ldA + g.a0al, g.bytesA, &S.barp);
                 if (PAY_B && g.bytesB)
-                    bulk_g2s(S.pay + (g.bytesA / sizeof(R)), p.Xs + (size_t)(r + 1) * p.ldxs + g.b0al, g.bytesB,
+                    bulk_g2s(S.pay + (g.bytesA / sizeof(R)) + MainStage<R, NC>::kPad,
+                             p.Xs + (size_t)(r + 1) * p.ldxs + g.b0al, g.bytesB,
                              &S.barp);
             }
             // block-level geometry (warp anchors stay in shared memory for the whole tile)
