@@ -56,9 +56,12 @@ struct MainStage {
 
 constexpr int kMainStages = 2;
 
-template <class R, int NC, int NW, int NACC>
+template <class R, int NC, int NW, int NACC, int NOS>
 struct MainShared {
     MainStage<R, NC> st[kMainStages];
+    // suffix values recorded between the two re-scans, [k][q][thread] (fp32
+    // unphased backward: saves 8 registers where the kernel would spill)
+    R os[NOS > 0 ? NOS : 1];
     // backward: a_bar at [li], b_bar at [na + li] (and phi_bar / psi_bar),
     // accumulated over the batch rows by the element's owning thread
     R acc[NACC > 0 ? NACC : 1][kTile];
@@ -183,7 +186,8 @@ __global__ void __launch_bounds__(TPB + 32, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS 
     // suffix values recorded per element for the outputs
     constexpr int KS = SEQ ? 1 : (!BWD ? (NG > 0 ? NG : NX) : (PHASED ? 4 : 1));
     constexpr int NACC = BWD ? (PHASED ? 2 : 1) : 0;
-    using SM = MainShared<R, NC, NW, NACC>;
+    constexpr bool OS_SMEM = BWD && !PHASED && sizeof(R) == 4;
+    using SM = MainShared<R, NC, NW, NACC, OS_SMEM ? KS * kTile : 0>;
     extern __shared__ __align__(16) unsigned char smem_main[];
     SM& sm = *reinterpret_cast<SM*>(smem_main);
 
@@ -321,46 +325,6 @@ __global__ void __launch_bounds__(TPB + 32, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS 
         const bool first_t = tid == 0, last_t = tid == TPB - 1;
 
         for (int r = 0; r < rows; ++r) {
-            // tile carries of this row, combined with the external shard carries:
-            // ext (+) tiles<t  and  tiles>t (+) ext
-            R cpv[NC], cps[NC], cqv[NC], cqs[NC];
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                const size_t sl0 = ((size_t)(2 * c) * rows + r), sl1 = ((size_t)(2 * c + 1) * rows + r);
-                if (r == 0) {  // staged by the producer
-                    cpv[c] = S.c0[0][c];
-                    cps[c] = S.c0[1][c];
-                    cqv[c] = S.c0[2][c];
-                    cqs[c] = S.c0[3][c];
-                } else {
-                    cpv[c] = t > 0 ? p.cp[sl0 * T + t - 1] : R(0);
-                    cps[c] = (t > 0 && C::pst(c)) ? p.cp[sl1 * T + t - 1] : R(0);
-                    cqv[c] = t + 1 < T ? p.cq[sl0 * T + t + 1] : R(0);
-                    cqs[c] = (t + 1 < T && C::qst(c)) ? p.cq[sl1 * T + t + 1] : R(0);
-                }
-                if (has_ext_p) {
-                    const R ev = ext_pv[sl0], es = C::pst(c) ? ext_pv[sl1] : R(0);
-                    if (t > 0) {  // (ext_anchor, ev, es) then (SL, cpv, cps)
-                        const R e = xexp(xsub(ext_pa, SL));
-                        if (C::pst(c)) cps[c] = xadd(cps[c], ext_pa < SL ? xmul(e, ev) : es);
-                        cpv[c] = xfma(e, ev, cpv[c]);
-                    } else {
-                        cpv[c] = ev;
-                        cps[c] = es;
-                    }
-                }
-                if (has_ext_q) {
-                    const R ev = ext_qv[sl0], es = C::qst(c) ? ext_qv[sl1] : R(0);
-                    if (t + 1 < T) {  // (SR, cqv, cqs) then (ext_anchor, ev, es)
-                        const R e = xexp(xsub(SR, ext_qa));
-                        if (C::qst(c)) cqs[c] = xadd(cqs[c], SR < ext_qa ? xmul(e, ev) : es);
-                        cqv[c] = xfma(e, ev, cqv[c]);
-                    } else {
-                        cqv[c] = ev;
-                        cqs[c] = es;
-                    }
-                }
-            }
             mbar_wait(&S.barp, (use * (uint32_t)rows + (uint32_t)r) & 1u);
             // ---- payloads: modulated channel values of each element ----
             R pay[NP][IPT];
@@ -558,6 +522,46 @@ __global__ void __launch_bounds__(TPB + 32, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS 
                 YV[c] = __shfl_sync(FULL, cv, lq);
                 YW[c] = __shfl_sync(FULL, cw, lq);
             }
+            // tile carries of this row, combined with the external shard carries:
+            // ext (+) tiles<t  and  tiles>t (+) ext
+            R cpv[NC], cps[NC], cqv[NC], cqs[NC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const size_t sl0 = ((size_t)(2 * c) * rows + r), sl1 = ((size_t)(2 * c + 1) * rows + r);
+                if (r == 0) {  // staged by the producer
+                    cpv[c] = S.c0[0][c];
+                    cps[c] = S.c0[1][c];
+                    cqv[c] = S.c0[2][c];
+                    cqs[c] = S.c0[3][c];
+                } else {
+                    cpv[c] = t > 0 ? p.cp[sl0 * T + t - 1] : R(0);
+                    cps[c] = (t > 0 && C::pst(c)) ? p.cp[sl1 * T + t - 1] : R(0);
+                    cqv[c] = t + 1 < T ? p.cq[sl0 * T + t + 1] : R(0);
+                    cqs[c] = (t + 1 < T && C::qst(c)) ? p.cq[sl1 * T + t + 1] : R(0);
+                }
+                if (has_ext_p) {
+                    const R ev = ext_pv[sl0], es = C::pst(c) ? ext_pv[sl1] : R(0);
+                    if (t > 0) {  // (ext_anchor, ev, es) then (SL, cpv, cps)
+                        const R e = xexp(xsub(ext_pa, SL));
+                        if (C::pst(c)) cps[c] = xadd(cps[c], ext_pa < SL ? xmul(e, ev) : es);
+                        cpv[c] = xfma(e, ev, cpv[c]);
+                    } else {
+                        cpv[c] = ev;
+                        cps[c] = es;
+                    }
+                }
+                if (has_ext_q) {
+                    const R ev = ext_qv[sl0], es = C::qst(c) ? ext_qv[sl1] : R(0);
+                    if (t + 1 < T) {  // (SR, cqv, cqs) then (ext_anchor, ev, es)
+                        const R e = xexp(xsub(SR, ext_qa));
+                        if (C::qst(c)) cqs[c] = xadd(cqs[c], SR < ext_qa ? xmul(e, ev) : es);
+                        cqv[c] = xfma(e, ev, cqv[c]);
+                    } else {
+                        cqv[c] = ev;
+                        cqs[c] = es;
+                    }
+                }
+            }
             // ---- 3c. thread-exclusive carries (+ tile carries) ----
             R VE[NC], WE[NC], VEq[NC], WEq[NC];
 #pragma unroll
@@ -612,7 +616,13 @@ __global__ void __launch_bounds__(TPB + 32, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS 
             }
 
             // ---- 4a. suffix re-scan seeded with the right carry; record what outputs need ----
-            R os[KS][IPT];
+            R osr[OS_SMEM ? 1 : KS][IPT];
+            auto OS = [&](int k, int q) -> R& {
+                if constexpr (OS_SMEM)
+                    return sm.os[(k * IPT + q) * TPB + tid];
+                else
+                    return osr[k][q];
+            };
             {
                 R u[NC], z[NC];
 #pragma unroll
@@ -627,23 +637,23 @@ __global__ void __launch_bounds__(TPB + 32, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS 
                     }
                     const bool isr = (rowm >> q) & 1;
                     if constexpr (SEQ) {
-                        os[0][q] = u[0];
+                        OS(0, q) = u[0];
                     } else if constexpr (!BWD) {
                         if constexpr (NG > 0) {
 #pragma unroll
-                            for (int c = 0; c < NG; ++c) os[c][q] = u[c];
+                            for (int c = 0; c < NG; ++c) OS(c, q) = u[c];
                         } else {
 #pragma unroll
-                            for (int c = 0; c < NX; ++c) os[c][q] = u[c];
+                            for (int c = 0; c < NX; ++c) OS(c, q) = u[c];
                         }
                     } else if constexpr (!PHASED) {
-                        os[0][q] = isr ? z[1] : u[0];  // rows: strict suffix of x; cols: suffix of g
+                        OS(0, q) = isr ? z[1] : u[0];  // rows: strict suffix of x; cols: suffix of g
                     } else {
                         // rows: Q and strict Q of the two x channels; cols: Q of the two g channels
-                        os[0][q] = isr ? u[2] : u[0];
-                        os[1][q] = isr ? u[3] : u[1];
-                        os[2][q] = z[2];
-                        os[3][q] = z[3];
+                        OS(0, q) = isr ? u[2] : u[0];
+                        OS(1, q) = isr ? u[3] : u[1];
+                        OS(2, q) = z[2];
+                        OS(3, q) = z[3];
                     }
                 }
             }
@@ -677,52 +687,52 @@ __global__ void __launch_bounds__(TPB + 32, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS 
                     if constexpr (SEQ) {
                         const uint32_t i = g.a0 + ia;
                         p.pre[(size_t)r * p.n + i] = a[0];
-                        p.suf[(size_t)r * p.n + i] = os[0][q];
+                        p.suf[(size_t)r * p.n + i] = OS(0, q);
                         ++ia;
                     } else if (isr) {
                         const int li = ia++;
                         if constexpr (!BWD && NX > 0) {
-                            R out = xadd(a[0], os[0][q]);
+                            R out = xadd(a[0], OS(0, q));
                             if constexpr (NX == 2) {
                                 const uint32_t i = g.a0 + li;
-                                out = xadd(xmul(cphi[i], out), xmul(sphi[i], xadd(a[1], os[1][q])));
+                                out = xadd(xmul(cphi[i], out), xmul(sphi[i], xadd(a[1], OS(1, q))));
                             }
                             stg[li] = out;
                         } else if constexpr (BWD) {
                             if constexpr (!PHASED) {
                                 const R gg = pay[0][q];
-                                acc1 = xfma(xmul(gg, p.inv_t), xsub(os[0][q], a[1]), acc1);
+                                acc1 = xfma(xmul(gg, p.inv_t), xsub(OS(0, q), a[1]), acc1);
                             } else {
                                 const uint32_t i = g.a0 + li;
                                 const R gg = raw[q];
                                 const R m0 = cphi[i], m1 = sphi[i];
-                                const R in0 = xsub(os[2][q], a[NG]);  // sum_{b>a} - sum_{b<a}
-                                const R in1 = xsub(os[3][q], a[NG + 1]);
+                                const R in0 = xsub(OS(2, q), a[NG]);  // sum_{b>a} - sum_{b<a}
+                                const R in1 = xsub(OS(3, q), a[NG + 1]);
                                 acc1 = xfma(xmul(xmul(m0, gg), p.inv_t), in0, acc1);
                                 acc1 = xfma(xmul(xmul(m1, gg), p.inv_t), in1, acc1);
-                                const R p0 = xadd(a[NG], os[0][q]), p1 = xadd(a[NG + 1], os[1][q]);
+                                const R p0 = xadd(a[NG], OS(0, q)), p1 = xadd(a[NG + 1], OS(1, q));
                                 acc2 = xfma(gg, xadd(xmul(-m1, p0), xmul(m0, p1)), acc2);
                             }
                         }
                     } else {
                         const int li = ib++;
                         if constexpr (NG > 0) {
-                            const R xb0 = xadd(a[0], os[0][q]);  // x_bar: identical in transpose and VJP
+                            const R xb0 = xadd(a[0], OS(0, q));  // x_bar: identical in transpose and VJP
                             if constexpr (!BWD) {
                                 stg[li] = xb0;
                             } else if constexpr (!PHASED) {
                                 stg[li] = xb0;
                                 const R x = pay[0][q];
-                                acc1 = xfma(xmul(x, p.inv_t), xsub(os[0][q], b[0]), acc1);
+                                acc1 = xfma(xmul(x, p.inv_t), xsub(OS(0, q), b[0]), acc1);
                             } else {
                                 const uint32_t j = g.b0 + li;
                                 const R x = raw[q];
                                 const R m0 = cpsi[j], m1 = spsi[j];
-                                const R xb1 = xadd(a[1], os[1][q]);
+                                const R xb1 = xadd(a[1], OS(1, q));
                                 stg[li] = xadd(xmul(m0, xb0), xmul(m1, xb1));
                                 acc2 = xfma(x, xadd(xmul(-m1, xb0), xmul(m0, xb1)), acc2);
-                                acc1 = xfma(xmul(xmul(m0, x), p.inv_t), xsub(os[0][q], b[0]), acc1);
-                                acc1 = xfma(xmul(xmul(m1, x), p.inv_t), xsub(os[1][q], b[1]), acc1);
+                                acc1 = xfma(xmul(xmul(m0, x), p.inv_t), xsub(OS(0, q), b[0]), acc1);
+                                acc1 = xfma(xmul(xmul(m1, x), p.inv_t), xsub(OS(1, q), b[1]), acc1);
                             }
                         }
                     }
