@@ -477,14 +477,17 @@ struct OutHook {
 };
 thread_local OutHook* g_out_hook = nullptr;
 
+// One launch per output array: with two arrays in one pass the random writes of
+// both windows thrash L2 (measured at 2^30: 17.5 ms for x_bar + b_bar together
+// vs 7.2 ms for one array, with ~60% DRAM read/write amplification).
 template <class R>
-void stage_scatter(const uint32_t* dst, uint32_t m, const R* s1, R* o1, size_t ld1, int rows1, const R* s2, R* o2,
-                   const R* s3, R* o3, cudaStream_t st) {
+void stage_scatter_one(const uint32_t* dst, uint32_t m, const R* s1, R* o1, size_t ld1, int rows1, cudaStream_t st) {
     using namespace lx::sort;
     const uint32_t chunks = (m + kPermChunk - 1) / kPermChunk;
     if (!g_out_hook) {
         launch("lx_perm_scatter", st, [&] {
-            lx_perm_stage_scatter<R><<<chunks, kPermThreads, 0, st>>>(dst, m, s1, o1, ld1, rows1, s2, o2, s3, o3, 0u);
+            lx_perm_stage_scatter<R><<<chunks, kPermThreads, 0, st>>>(dst, m, s1, o1, ld1, rows1, nullptr, nullptr,
+                                                                      nullptr, nullptr, 0u);
         });
         return;
     }
@@ -499,12 +502,19 @@ void stage_scatter(const uint32_t* dst, uint32_t m, const R* s1, R* o1, size_t l
         if (u1 <= u0) continue;
         const uint32_t b0 = (uint32_t)(u0 / kPermChunk), b1 = (uint32_t)((u1 + kPermChunk - 1) / kPermChunk);
         launch("lx_perm_scatter", st, [&] {
-            lx_perm_stage_scatter<R><<<b1 - b0, kPermThreads, 0, st>>>(dst, m, s1, o1, ld1, rows1, s2, o2, s3, o3, b0);
+            lx_perm_stage_scatter<R><<<b1 - b0, kPermThreads, 0, st>>>(dst, m, s1, o1, ld1, rows1, nullptr, nullptr,
+                                                                       nullptr, nullptr, b0);
         });
         g_out_hook->fn(o1, u0, u1, rows1, ld1, st);
-        if (s2) g_out_hook->fn(o2, u0, u1, 1, m, st);
-        if (s3) g_out_hook->fn(o3, u0, u1, 1, m, st);
     }
+}
+
+template <class R>
+void stage_scatter(const uint32_t* dst, uint32_t m, const R* s1, R* o1, size_t ld1, int rows1, const R* s2, R* o2,
+                   const R* s3, R* o3, cudaStream_t st) {
+    stage_scatter_one<R>(dst, m, s1, o1, ld1, rows1, st);
+    if (s2) stage_scatter_one<R>(dst, m, s2, o2, m, 1, st);
+    if (s3) stage_scatter_one<R>(dst, m, s3, o3, m, 1, st);
 }
 
 // any non-finite entry of v[0, m) sets *bad (host-pointer API validation,
