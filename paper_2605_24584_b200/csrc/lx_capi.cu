@@ -354,12 +354,13 @@ void radix_sort(const R* raw, uint32_t m, R t, R* vals_out, uint32_t* perm_out, 
         const uint32_t epoch = (uint32_t)pass + 1;
         const uint32_t* offs = nullptr;
         if (kSortRts) {  // per-(digit, tile) offsets first: the pass needs no look-back
+            const uint32_t cgrid = (tiles + kCountTiles - 1) / kCountTiles;
             launch("lx_sort_count", st, [&] {
                 if (pass == 0)
-                    lx_sort_count<R, true, false><<<tiles, kThreads, 0, st>>>(in, m, t, 0, cnt.as<uint32_t>());
+                    lx_sort_count<R, true, false><<<cgrid, kThreads, 0, st>>>(in, m, t, 0, cnt.as<uint32_t>(), tiles);
                 else
-                    lx_sort_count<R, false, false><<<tiles, kThreads, 0, st>>>(in, m, t, pass * kBits,
-                                                                               cnt.as<uint32_t>());
+                    lx_sort_count<R, false, false><<<cgrid, kThreads, 0, st>>>(in, m, t, pass * kBits,
+                                                                               cnt.as<uint32_t>(), tiles);
             });
             launch("lx_sort_scan", st, [&] {
                 lx_sort_scan<<<kRadix, kScanThreads, 0, st>>>(cnt.as<uint32_t>(), tiles, bptr, 0);
@@ -405,8 +406,8 @@ void build_splan(Side& sd, cudaStream_t st) {
     const uint32_t* offs = nullptr;
     if (kSortRts) {
         launch("lx_splan_count", st, [&] {
-            lx_sort_count<float, false, true><<<tiles, kThreads, 0, st>>>(sd.perm.p, m, 1.0f, shift,
-                                                                          cnt.as<uint32_t>());
+            lx_sort_count<float, false, true><<<(tiles + kCountTiles - 1) / kCountTiles, kThreads, 0, st>>>(
+                sd.perm.p, m, 1.0f, shift, cnt.as<uint32_t>(), tiles);
         });
         launch("lx_sort_scan", st, [&] {
             lx_sort_scan<<<kRadix, kScanThreads, 0, st>>>(cnt.as<uint32_t>(), tiles, nullptr, shift);

@@ -359,48 +359,62 @@ scatter:
 // ---- reduce-then-scan form of a pass (no look-back) --------------------------
 // lx_sort_count: per-tile digit counts of the pass (the same tiles and digit
 // function as lx_sort_pass), digit-major cnt[d * tiles + tile].
+// kCountTiles pass tiles per CTA, all their loads issued up front (more bytes
+// in flight per round trip), each tile counted into its own column.
+#ifndef LX_COUNT_TILES
+#define LX_COUNT_TILES 1
+#endif
+constexpr int kCountTiles = LX_COUNT_TILES;
+
 template <class R, bool FIRST, bool SPLAN>
 __global__ void __launch_bounds__(kThreads) lx_sort_count(const void* __restrict__ in_keys, size_t n, R t, int shift,
-                                                         uint32_t* __restrict__ cnt) {
+                                                         uint32_t* __restrict__ cnt, uint32_t tiles) {
     using K = typename Traits<R>::Key;
-    __shared__ uint32_t wh[kWarps][kRadix];
+    __shared__ uint32_t wh[kCountTiles][kWarps][kRadix];
     const int tid = threadIdx.x, warp = tid >> 5;
-    for (int i = tid; i < kWarps * kRadix; i += kThreads) (&wh[0][0])[i] = 0;
+    for (int i = tid; i < kCountTiles * kWarps * kRadix; i += kThreads) (&wh[0][0][0])[i] = 0;
     __syncthreads();
-    const size_t tile_start = (size_t)blockIdx.x * kTile;
     const K* gk = reinterpret_cast<const K*>(in_keys);
     constexpr int kV = 16 / sizeof(K);  // keys per 16-byte vector
-    constexpr int kVec = kItems / kV;   // vectors per thread
-    const bool full = tile_start + kTile <= n && (reinterpret_cast<uintptr_t>(gk) & 15) == 0;
+    constexpr int kVec = kItems / kV;   // vectors per thread per tile
+    const uint32_t tile0 = blockIdx.x * kCountTiles;
+    const size_t start = (size_t)tile0 * kTile;
+    const bool full = start + (size_t)kCountTiles * kTile <= n && (reinterpret_cast<uintptr_t>(gk) & 15) == 0;
+    auto count = [&](int j, K key) {
+        if constexpr (FIRST) key = radix_key<R>(xdiv(from_bits(key, R(0)), t));
+        atomicAdd(&wh[j][warp][(int)((key >> shift) & (kRadix - 1))], 1u);
+    };
     if (full) {
-        uint4 q4[kVec];
+        uint4 q4[kCountTiles][kVec];
 #pragma unroll
-        for (int j = 0; j < kVec; ++j)
-            q4[j] = reinterpret_cast<const uint4*>(gk + tile_start)[(size_t)j * kThreads + tid];
+        for (int j = 0; j < kCountTiles; ++j)
 #pragma unroll
-        for (int j = 0; j < kVec; ++j) {
-            const K* kk = reinterpret_cast<const K*>(&q4[j]);
+            for (int v = 0; v < kVec; ++v)
+                q4[j][v] = reinterpret_cast<const uint4*>(gk + start + (size_t)j * kTile)[(size_t)v * kThreads + tid];
 #pragma unroll
-            for (int e = 0; e < kV; ++e) {
-                K key = kk[e];
-                if constexpr (FIRST) key = radix_key<R>(xdiv(from_bits(key, R(0)), t));
-                atomicAdd(&wh[warp][(int)((key >> shift) & (kRadix - 1))], 1u);
+        for (int j = 0; j < kCountTiles; ++j)
+#pragma unroll
+            for (int v = 0; v < kVec; ++v) {
+                const K* kk = reinterpret_cast<const K*>(&q4[j][v]);
+#pragma unroll
+                for (int e = 0; e < kV; ++e) count(j, kk[e]);
             }
-        }
     } else {
-        for (int q = 0; q < kItems; ++q) {
-            const size_t i = tile_start + (size_t)q * kThreads + tid;
-            if (i >= n) continue;
-            K key = gk[i];
-            if constexpr (FIRST) key = radix_key<R>(xdiv(from_bits(key, R(0)), t));
-            atomicAdd(&wh[warp][(int)((key >> shift) & (kRadix - 1))], 1u);
-        }
+        for (int j = 0; j < kCountTiles; ++j)
+            for (int q = 0; q < kItems; ++q) {
+                const size_t i = start + (size_t)j * kTile + (size_t)q * kThreads + tid;
+                if (i < n) count(j, gk[i]);
+            }
     }
     __syncthreads();
-    uint32_t c = 0;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) c += wh[w][tid];
-    cnt[(size_t)tid * gridDim.x + blockIdx.x] = c;
+    for (int j = 0; j < kCountTiles; ++j) {
+        if (tile0 + j >= tiles) break;
+        uint32_t c = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) c += wh[j][w][tid];
+        cnt[(size_t)tid * tiles + tile0 + j] = c;
+    }
 }
 
 // lx_sort_scan: one CTA per digit; offs[d][tile] = base[d] + sum of the
