@@ -445,3 +445,64 @@ def test_batch_rows_on_plan_path():
     assert O.rel_err_l2(bb.double().cpu().numpy(), sb.cpu().numpy()) <= 1e-6
     # x_bar of the VJP is the transpose, bitwise
     assert torch.equal(xb, op.apply(G, transpose=True))
+
+
+# ------------------------------------------------ plan path: phases, transpose, fp64
+def test_plan_path_phased_and_transpose_fp64():
+    """Sides above the direct-permutation limit (2^22) in fp64: phased forward and
+    VJP and the transpose against the reference oracle (staged outputs, per-tile
+    store order, window scatters)."""
+    rng = np.random.default_rng(43)
+    n, k = (1 << 22) + 7, (1 << 22) + 1000
+    a = rng.uniform(-100, 100, n)
+    b = rng.uniform(-100, 100, k)
+    b[:5000] = a[:5000]  # exact ties across the sides
+    phi, psi = rng.uniform(0, 6.28, n), rng.uniform(0, 6.28, k)
+    x, g = rng.uniform(-1, 1, k), rng.uniform(-1, 1, n)
+    op = L.LaplexOperator(a, b, 0.9, phi, psi)
+    oo = O.OracleOp(a, b, 0.9, phi, psi)
+    assert O.rel_err_l2(op.phased_matvec(x), oo.phased_matvec(x)) <= 1e-12
+    v = L.phased_matvec_vjp(op, x, g)
+    for got, w in zip((v.x_bar, v.a_bar, v.b_bar, v.phi_bar, v.psi_bar), oo.phased_vjp(x, g)):
+        assert O.rel_err_l2(got, w) <= 1e-11
+    plain = L.LaplexOperator(a, b, 0.9)
+    assert O.rel_err_l2(plain.matvec_transpose(g), O.OracleOp(a, b, 0.9).matvec_transpose(g)) <= 1e-12
+
+
+# ------------------------------------------------ host API: device-side validation above 2^20
+def test_host_api_large_inputs_nonfinite_order():
+    """Above 2^20 elements the host-pointer API checks finiteness on the device
+    after the upload; errors keep the reference order (operator.hpp:88-101,
+    gradients.hpp:113-117) and no output is written."""
+    import ctypes as C
+    from paper_2605_24584_b200 import _lib
+    lib = _lib.lib()
+    rng = np.random.default_rng(44)
+    n = k = (1 << 20) + 5
+    a = rng.uniform(-10, 10, n)
+    b = rng.uniform(-10, 10, k)
+    bad_b = b.copy()
+    bad_b[k // 2] = np.nan
+    with pytest.raises(L.NonFinite, match="col anchors"):
+        L.LaplexOperator(a, bad_b)
+    with pytest.raises(L.NonFinite, match="row anchors"):
+        L.LaplexOperator(np.where(np.arange(n) == 3, np.inf, a), bad_b, -1.0)  # anchors before temperature
+    with pytest.raises(L.NonFinite, match="temperature"):
+        L.LaplexOperator(a, b, 0.0)
+    op = L.LaplexOperator(a, b)
+    x = rng.uniform(-1, 1, k)
+    g = rng.uniform(-1, 1, n)
+    xb = x.copy()
+    xb[7] = np.nan
+    gb = g.copy()
+    gb[n - 1] = np.inf
+    y = np.full(n, 12345.0)
+    rc = lib.laplex_apply(op._h, 0, xb.ctypes.data, 1, k, y.ctypes.data)
+    assert rc == 2 and b"matvec x" in lib.laplex_last_error()
+    assert np.all(y == 12345.0)  # untouched
+    with pytest.raises(L.NonFinite, match="vjp g"):
+        L.matvec_vjp(op, x, gb)
+    with pytest.raises(L.NonFinite, match="vjp x"):
+        L.matvec_vjp(op, xb, gb)  # x reported first
+    # and the valid call still works afterwards
+    assert O.rel_err_l2(op.matvec(x), O.OracleOp(a, b).matvec(x)) <= 1e-12
