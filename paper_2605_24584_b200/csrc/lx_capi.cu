@@ -328,7 +328,7 @@ void radix_sort(const R* raw, uint32_t m, R t, R* vals_out, uint32_t* perm_out, 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const uint32_t per_block = kHistThreads * kHistItems;
     const uint32_t hgrid = std::max(1u, std::min<uint32_t>((m + per_block - 1) / per_block, (uint32_t)sms * 4));
-    const size_t hsmem = (size_t)4 * P * kRadix * sizeof(uint32_t);
+    const size_t hsmem = (size_t)kHistSub * P * kRadix * sizeof(uint32_t);
     launch("lx_sort_hist", st, [&] {
         lx_sort_hist<R><<<hgrid, kHistThreads, hsmem, st>>>(raw, m, t, hist.as<uint32_t>(), bad);
     });

@@ -57,6 +57,10 @@ __device__ __forceinline__ unsigned long long status(unsigned long long flag, ui
 // each thread keeps kHistItems independent loads in flight.
 constexpr int kHistThreads = 512;
 constexpr int kHistItems = 8;
+#ifndef LX_HIST_SUB
+#define LX_HIST_SUB 4
+#endif
+constexpr int kHistSub = LX_HIST_SUB;
 
 template <class R>
 __global__ void __launch_bounds__(kHistThreads) lx_sort_hist(const R* __restrict__ raw, size_t n, R t,
@@ -64,7 +68,7 @@ __global__ void __launch_bounds__(kHistThreads) lx_sort_hist(const R* __restrict
     using K = typename Traits<R>::Key;
     constexpr int P = Traits<R>::kPasses;
     constexpr int W = kHistThreads / 32;
-    constexpr int SUB = 4;  // sub-histograms per block (warp % SUB)
+    constexpr int SUB = kHistSub;  // sub-histograms per block (warp % SUB)
     extern __shared__ uint32_t shh[];  // [SUB][P][kRadix]
     for (int i = threadIdx.x; i < SUB * P * kRadix; i += kHistThreads) shh[i] = 0;
     __syncthreads();
