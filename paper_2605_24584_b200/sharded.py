@@ -398,7 +398,9 @@ class ShardedOperator:
         def sample(v):
             if v.numel() == 0:
                 return torch.full((samples,), float("nan"), dtype=v.dtype, device=v.device)
-            idx = torch.linspace(0, v.numel() - 1, samples, device=v.device).round().long()
+            # integer arithmetic: a float32 linspace rounds its endpoint past the last index
+            # once numel > 2^24 (e.g. 2^29 elements per rank)
+            idx = (torch.arange(samples, device=v.device, dtype=torch.int64) * (v.numel() - 1)) // max(1, samples - 1)
             return v[idx] / tt
         s = torch.cat([sample(a), sample(b)])
         allsamp = torch.cat(comm.all_gather(s))
