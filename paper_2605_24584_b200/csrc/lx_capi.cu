@@ -496,7 +496,7 @@ void stage_scatter_one(const uint32_t* dst, uint32_t m, const R* s1, R* o1, size
     // indices [w << shift, (w + 1) << shift), at the same bucketed positions)
     const int shift = bucket_shift(m);
     const uint32_t W = (uint32_t)(((uint64_t)m + (1ull << shift) - 1) >> shift);
-    const uint32_t G = std::min<uint32_t>(W, 8u);
+    const uint32_t G = std::min<uint32_t>(W, 16u);  // 16 groups: the last download tail is 1/16 of the array
     for (uint32_t gi = 0; gi < G; ++gi) {
         const uint64_t u0 = ((uint64_t)(gi * W / G)) << shift;
         const uint64_t u1 = std::min<uint64_t>(((uint64_t)((gi + 1) * W / G)) << shift, m);
