@@ -746,7 +746,11 @@ DBuf sorted_payload(const View<R>& v, int rows, const R* user, const Scratch& sc
     }
     launch("lx_gather_agg", st, [&] {
         const uint32_t grid = (v.T + lx::ms::kAggTiles - 1) / lx::ms::kAggTiles;
-        lx::ms::lx_gather_agg<R, NCH, SIDE_A, GFORM, STRICT><<<grid, lx::ms::kAggThreads, 0, st>>>(g);
+        // few tiles and many rows (batched calls): split the rows over CTAs too
+        const int groups = (int)std::max<uint32_t>(1u, std::min<uint32_t>((uint32_t)rows, (4u * 148u + grid - 1) / grid));
+        g.rows_per_cta = std::max(1, (rows + groups - 1) / groups);
+        const uint32_t gy = (uint32_t)std::max(1, (rows + g.rows_per_cta - 1) / g.rows_per_cta);
+        lx::ms::lx_gather_agg<R, NCH, SIDE_A, GFORM, STRICT><<<dim3(grid, gy), lx::ms::kAggThreads, 0, st>>>(g);
     });
     return out;
 }

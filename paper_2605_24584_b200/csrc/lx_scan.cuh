@@ -361,6 +361,7 @@ struct GatherAggArgs {
     R* aggp;              // [slot][rows][T]
     R* aggq;
     int cbase;            // first channel index of this side
+    int rows_per_cta;     // batch rows per CTA (grid.y = row groups)
 };
 
 // SIDE_A: the tile range is the rows range; GFORM: g-channel formulas (prefix
@@ -404,7 +405,9 @@ __global__ void __launch_bounds__(kAggThreads) lx_gather_agg(GatherAggArgs<R> g)
     const R* __restrict__ V = g.V;
     R* __restrict__ out = g.out;
     __shared__ R red[NT][4 * NCH][NW];
-    for (int r = 0; r < g.rows; ++r) {
+    // batch rows are split over blockIdx.y (row groups of g.rows_per_cta)
+    const int r_lo = (int)blockIdx.y * g.rows_per_cta, r_hi = min(g.rows, r_lo + g.rows_per_cta);
+    for (int r = r_lo; r < r_hi; ++r) {
         R pi[NT][NCH], ps[NT][NCH], qi[NT][NCH], qs[NT][NCH];
 #pragma unroll
         for (int j = 0; j < NT; ++j)
