@@ -1868,9 +1868,11 @@ int laplex_shard_partition_dev(int dtype, const void* raw, size_t m, double t, c
                 lx::shard::lx_shard_count<R><<<tiles, lx::shard::kThreads, 0, st>>>(rp, m, tr, sp, nsplit,
                                                                                     cnt.as<uint32_t>());
             });
-            launch("lx_shard_offsets", st, [&] {
-                lx::shard::lx_shard_offsets<<<1, lx::shard::kMaxShards, 0, st>>>(cnt.as<uint32_t>(), tiles, nsh,
-                                                                                counts);
+            launch("lx_shard_totals", st, [&] {
+                lx::shard::lx_shard_totals<<<nsh, lx::shard::kOffThreads, 0, st>>>(cnt.as<uint32_t>(), tiles, counts);
+            });
+            launch("lx_shard_scan", st, [&] {
+                lx::shard::lx_shard_scan<<<nsh, lx::shard::kOffThreads, 0, st>>>(cnt.as<uint32_t>(), tiles, counts);
             });
             launch("lx_shard_scatter", st, [&] {
                 lx::shard::lx_shard_scatter<R><<<tiles, lx::shard::kThreads, 0, st>>>(rp, m, tr, sp, nsplit,

@@ -4,7 +4,7 @@
 // one per GPU.  Splitters are VALUES shared by a and b and an element goes to
 // shard #{splitters < value}, so a run of equal values never straddles two
 // shards (the tie-inclusive co-ranks stay shard-local).  These kernels:
-//   lx_shard_count / lx_shard_offsets / lx_shard_scatter
+//   lx_shard_count / lx_shard_totals / lx_shard_scan / lx_shard_scatter
 //       stable partition of raw/t by shard: counts per shard and the local
 //       index of every element in shard order (what goes into the all-to-all);
 //   lx_collect_totals
@@ -50,25 +50,58 @@ __global__ void __launch_bounds__(kThreads) lx_shard_count(const R* __restrict__
     if (threadIdx.x < kMaxShards) cnt[(size_t)blockIdx.x * kMaxShards + threadIdx.x] = sc[threadIdx.x];
 }
 
-// exclusive offsets: off[tile][s] = sum_{s' < s} total[s'] + sum_{tile' < tile} cnt[tile'][s];
-// counts[s] = total[s].  One block, thread s walks its column.
-__global__ void lx_shard_offsets(uint32_t* __restrict__ cnt, uint32_t tiles, int nsh, uint32_t* __restrict__ counts) {
-    __shared__ uint32_t tot[kMaxShards];
-    const int s = threadIdx.x;
-    uint32_t run = 0;
-    if (s < nsh)
-        for (uint32_t t = 0; t < tiles; ++t) {
-            const uint32_t c = cnt[(size_t)t * kMaxShards + s];
-            cnt[(size_t)t * kMaxShards + s] = run;
-            run += c;
-        }
-    if (s < kMaxShards) tot[s] = s < nsh ? run : 0;
+// Exclusive offsets off[tile][s] = sum_{s' < s} total[s'] + sum_{tile' < tile}
+// cnt[tile'][s], one CTA per shard (a serial one-block walk took ~1.7 ms per
+// call at 2^27 elements): lx_shard_totals sums each shard's column (counts[s]),
+// lx_shard_scan turns it into offsets seeded with the lower shards' totals.
+constexpr int kOffThreads = 1024;
+
+__global__ void __launch_bounds__(kOffThreads) lx_shard_totals(const uint32_t* __restrict__ cnt, uint32_t tiles,
+                                                              uint32_t* __restrict__ counts) {
+    __shared__ uint32_t ws[kOffThreads / 32];
+    const int s = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint32_t sum = 0;
+    for (uint32_t t = tid; t < tiles; t += kOffThreads) sum += cnt[(size_t)t * kMaxShards + s];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
+    if (lane == 0) ws[warp] = sum;
     __syncthreads();
-    if (s < nsh) {
-        uint32_t base = 0;
-        for (int q = 0; q < s; ++q) base += tot[q];
-        counts[s] = run;
-        for (uint32_t t = 0; t < tiles; ++t) cnt[(size_t)t * kMaxShards + s] += base;
+    if (tid == 0) {
+        uint32_t tot = 0;
+        for (int w = 0; w < kOffThreads / 32; ++w) tot += ws[w];
+        counts[s] = tot;
+    }
+}
+
+__global__ void __launch_bounds__(kOffThreads) lx_shard_scan(uint32_t* __restrict__ cnt, uint32_t tiles,
+                                                            const uint32_t* __restrict__ counts) {
+    constexpr int NW = kOffThreads / 32;
+    __shared__ uint32_t ws[NW];
+    __shared__ uint32_t carry;
+    const int s = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        uint32_t b = 0;
+        for (int q = 0; q < s; ++q) b += counts[q];
+        carry = b;
+    }
+    __syncthreads();
+    for (uint32_t base = 0; base < tiles; base += kOffThreads) {
+        const uint32_t t = base + tid;
+        const uint32_t v = t < tiles ? cnt[(size_t)t * kMaxShards + s] : 0u;
+        uint32_t incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t x = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += x;
+        }
+        if (lane == 31) ws[warp] = incl;
+        __syncthreads();
+        uint32_t before = carry;
+        for (int w = 0; w < warp; ++w) before += ws[w];
+        if (t < tiles) cnt[(size_t)t * kMaxShards + s] = before + incl - v;
+        __syncthreads();
+        if (tid == kOffThreads - 1) carry = before + incl;
+        __syncthreads();
     }
 }
 
