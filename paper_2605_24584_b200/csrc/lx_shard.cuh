@@ -180,13 +180,39 @@ __global__ void lx_collect_totals(const R* __restrict__ cp, const R* __restrict_
     }
 }
 
+// Routing by index list (partition order <-> caller order).  Each thread
+// moves kRouteItems elements per round with every index load, then every
+// payload load, issued before use (the index list is a few increasing runs,
+// so both sides are near-sequential streams).
+constexpr int kRouteItems = 8;
+
 template <class R>
 __global__ void lx_gather_idx(const R* __restrict__ src, size_t ld_src, const uint32_t* __restrict__ idx, size_t m,
                               int rows, R* __restrict__ dst) {
     const size_t total = m * rows;
-    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
-        const size_t r = e / m, j = e - r * m;
-        dst[e] = src[r * ld_src + idx[j]];
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t e0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < total; e0 += stride * kRouteItems) {
+        uint32_t u[kRouteItems];
+        size_t rr[kRouteItems];
+#pragma unroll
+        for (int q = 0; q < kRouteItems; ++q) {
+            const size_t e = e0 + (size_t)q * stride;
+            const size_t r = (rows == 1 || e >= total) ? 0 : e / m;  // no 64-bit division for one row
+            const size_t j = e < total ? e - r * m : 0;
+            rr[q] = r;
+            u[q] = e < total ? idx[j] : 0u;
+        }
+        R v[kRouteItems];
+#pragma unroll
+        for (int q = 0; q < kRouteItems; ++q) {
+            const size_t e = e0 + (size_t)q * stride;
+            v[q] = e < total ? src[rr[q] * ld_src + u[q]] : R(0);
+        }
+#pragma unroll
+        for (int q = 0; q < kRouteItems; ++q) {
+            const size_t e = e0 + (size_t)q * stride;
+            if (e < total) dst[e] = v[q];
+        }
     }
 }
 
@@ -194,9 +220,22 @@ template <class R>
 __global__ void lx_scatter_idx(const R* __restrict__ src, const uint32_t* __restrict__ idx, size_t m, int rows,
                                R* __restrict__ dst, size_t ld_dst) {
     const size_t total = m * rows;
-    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
-        const size_t r = e / m, j = e - r * m;
-        dst[r * ld_dst + idx[j]] = src[e];
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t e0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < total; e0 += stride * kRouteItems) {
+        uint32_t u[kRouteItems];
+        R v[kRouteItems];
+#pragma unroll
+        for (int q = 0; q < kRouteItems; ++q) {
+            const size_t e = e0 + (size_t)q * stride;
+            const size_t j = e >= total ? 0 : (rows == 1 ? e : e % m);
+            u[q] = e < total ? idx[j] : 0u;
+            v[q] = e < total ? src[e] : R(0);
+        }
+#pragma unroll
+        for (int q = 0; q < kRouteItems; ++q) {
+            const size_t e = e0 + (size_t)q * stride;
+            if (e < total) dst[(rows == 1 ? 0 : e / m) * ld_dst + u[q]] = v[q];
+        }
     }
 }
 
