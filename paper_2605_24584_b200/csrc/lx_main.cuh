@@ -108,7 +108,6 @@ struct TileGeom {
     }
 };
 
-// Thread 0: stage tile t (anchors, output indices, row-0 payloads) by TMA.
 // Producer lane: stage tile t (header, row-0 carries, anchors, output
 // indices, row-0 payloads) and arm the stage's barriers.  t >= T stages the
 // end-of-work sentinel (header only).
@@ -152,24 +151,27 @@ __device__ __forceinline__ void issue_tile(MainStage<R, NC>& S, const MainArgs<R
         bulk_g2s(S.pay + (g.bytesA / sizeof(R)) + MainStage<R, NC>::kPad, p.Xs + g.b0al, g.bytesB, &S.barp);
 }
 
-// Channel layout: g channels first (c < NG), then x channels.  Strict prefix
-// variants for g channels and strict suffix variants for x channels, in the
-// backward (BWD) configuration only.  SEQ: one x channel carried by rows.
-// diagnostics only (LX_DIAG_CONTIG): write outputs at the sorted position
-// instead of perm / plan position, to isolate the cost of the scattered stores
+// Diagnostics only (LX_DIAG_CONTIG): write outputs at the sorted position
+// instead of the perm / plan position, to isolate the cost of the stores.
 #ifdef LX_DIAG_CONTIG
 #define LXO(perm_pos, sorted_pos) (sorted_pos)
 #else
 #define LXO(perm_pos, sorted_pos) (perm_pos)
 #endif
 
-template <class R, int NG, int NX, bool BWD, bool SEQ, int TPB, int IPT>
+// Resident threads per SM the register budget targets (fp32): 3 forward /
+// transpose CTAs, 2 backward CTAs (measured best).
 #ifndef LX_MAIN_CTAS
 #define LX_MAIN_CTAS 768
 #endif
 #ifndef LX_BWD_CTAS
 #define LX_BWD_CTAS 512
 #endif
+
+// Channel layout: g channels first (c < NG), then x channels.  Strict prefix
+// variants for g channels and strict suffix variants for x channels, in the
+// backward (BWD) configuration only.  SEQ: one x channel carried by rows.
+template <class R, int NG, int NX, bool BWD, bool SEQ, int TPB, int IPT>
 __global__ void __launch_bounds__(TPB + 32, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS : LX_MAIN_CTAS) / TPB : 1) lx_main(MainArgs<R> p) {
     static_assert(TPB * IPT == kTile, "a CTA covers one merge tile");
     constexpr int NW = TPB / 32;
