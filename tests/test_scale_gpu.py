@@ -82,3 +82,33 @@ def test_sorted_plan_is_a_permutation_at_scale(torch):
     assert np.all(np.diff(s.values) >= 0)
     assert np.array_equal(np.sort(s.perm), np.arange(N, dtype=np.uint64))
     assert np.array_equal(s.values, (a / np.float32(0.5))[s.perm.astype(np.int64)])
+
+
+@pytest.mark.parametrize("lg,span", [(28, 100.0), (27, 3.0)])
+def test_fp32_against_fp64_device_path_at_scale(torch, lg, span):
+    """north_star tolerance at scale: the fp32 path against the fp64 device path
+    (itself pinned to the reference oracle at <= 1e-12 on smaller inputs) on the
+    same fp32 inputs.  At 2^28 in [-100, 100] many anchors are exact duplicates
+    (fp32 spacing 7.6e-6 near |a| = 100); span 3 packs them denser still."""
+    N = 1 << lg
+    dev = torch.device("cuda:0")
+    g = torch.Generator(device=dev)
+    g.manual_seed(lg)
+    a = torch.empty(N, device=dev).uniform_(-span, span, generator=g)
+    b = torch.empty(N, device=dev).uniform_(-span, span, generator=g)
+    x = torch.empty(1, N, device=dev).uniform_(-1, 1, generator=g)
+    gg = torch.empty(1, N, device=dev).uniform_(-1, 1, generator=g)
+    op32 = L.DeviceOperator(a, b, 1.0)
+    y32 = op32.apply(x)
+    b32 = op32.backward(x, gg)[:3]
+    del op32
+    op64 = L.DeviceOperator(a.double(), b.double(), 1.0)
+    y64 = op64.apply(x.double())
+    b64 = op64.backward(x.double(), gg.double())[:3]
+    del op64
+
+    def rel(u, w):
+        return float(torch.linalg.vector_norm(u.double() - w) / torch.linalg.vector_norm(w))
+    assert rel(y32, y64) <= 1e-5
+    for u, w in zip(b32, b64):
+        assert rel(u, w) <= 1e-5
