@@ -156,10 +156,10 @@ struct Side {
 // L2-resident, 126 MB); larger ones go through the two-pass plan.
 constexpr uint32_t kDirectMax = 1u << 22;
 #ifndef LX_FWD_TPB
-#define LX_FWD_TPB 256
+#define LX_FWD_TPB 128
 #endif
 #ifndef LX_BWD_TPB
-#define LX_BWD_TPB 256
+#define LX_BWD_TPB 128
 #endif
 constexpr size_t kTmaPad = 64;  // slack after anchor arrays for 16-byte TMA rounding
 
@@ -616,19 +616,21 @@ lx::ms::MainArgs<R> main_args(const View<R>& v, int rows) {
     return a;
 }
 
-// Main-kernel shape per mode: threads per CTA x items per thread (= one 2048
-// element merge tile).  The backward carries twice the channels, so it runs
-// more threads with fewer items each to stay inside the register file.
-template <bool BWD>
+// Main-kernel shape: consumer threads per CTA x items per thread (= one 2048
+// element merge tile).  Unphased kernels run 128 x 16 (fewer per-thread
+// overheads per element; measured best at 2^30); the phased kernels carry
+// twice the channels and keep 256 x 8.  The transpose and the backward share
+// a shape, so x_bar of the VJP is bitwise the transpose.
+template <bool BWD, bool PHASED>
 struct MainShape {
-    static constexpr int TPB = BWD ? LX_BWD_TPB : LX_FWD_TPB;
+    static constexpr int TPB = PHASED ? 256 : (BWD ? LX_BWD_TPB : LX_FWD_TPB);
     static constexpr int IPT = lx::ms::kTile / TPB;
 };
 
 template <class R, int NG, int NX, bool BWD, bool SEQ = false>
 void launch_main(const char* name, const lx::ms::MainArgs<R>& a, cudaStream_t st) {
     using namespace lx::ms;
-    constexpr int TPB = MainShape<BWD>::TPB, IPT = MainShape<BWD>::IPT;
+    constexpr int TPB = MainShape<BWD, (NG == 2 || NX == 2)>::TPB, IPT = MainShape<BWD, (NG == 2 || NX == 2)>::IPT;
     auto kern = lx_main<R, NG, NX, BWD, SEQ, TPB, IPT>;
     constexpr bool os_smem = BWD && NG != 2 && sizeof(R) == 4;
     const size_t smem = sizeof(MainShared<R, NG + NX, TPB / 32, BWD ? (NG == 2 ? 2 : 1) : 0, os_smem ? kTile : 0>);

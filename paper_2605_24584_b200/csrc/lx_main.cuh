@@ -159,20 +159,25 @@ __device__ __forceinline__ void issue_tile(MainStage<R, NC>& S, const MainArgs<R
 #define LXO(perm_pos, sorted_pos) (perm_pos)
 #endif
 
-// Resident threads per SM the register budget targets (fp32): 3 forward /
-// transpose CTAs, 2 backward CTAs (measured best).
+// Resident consumer threads per SM the register budget targets (fp32): for
+// the 128-thread unphased shape 3 forward / transpose CTAs and 2 backward
+// CTAs; for the 256-thread phased shape 3 and 2 as well (measured best).
 #ifndef LX_MAIN_CTAS
-#define LX_MAIN_CTAS 768
+#define LX_MAIN_CTAS 384
 #endif
 #ifndef LX_BWD_CTAS
-#define LX_BWD_CTAS 512
+#define LX_BWD_CTAS 256
 #endif
+template <class R, bool BWD, int TPB>
+constexpr int main_min_blocks() {
+    return sizeof(R) != 4 ? 1 : TPB == 256 ? (BWD ? 2 : 3) : (BWD ? LX_BWD_CTAS : LX_MAIN_CTAS) / TPB;
+}
 
 // Channel layout: g channels first (c < NG), then x channels.  Strict prefix
 // variants for g channels and strict suffix variants for x channels, in the
 // backward (BWD) configuration only.  SEQ: one x channel carried by rows.
 template <class R, int NG, int NX, bool BWD, bool SEQ, int TPB, int IPT>
-__global__ void __launch_bounds__(TPB + 32, sizeof(R) == 4 ? (BWD ? LX_BWD_CTAS : LX_MAIN_CTAS) / TPB : 1) lx_main(MainArgs<R> p) {
+__global__ void __launch_bounds__(TPB + 32, main_min_blocks<R, BWD, TPB>()) lx_main(MainArgs<R> p) {
     static_assert(TPB * IPT == kTile, "a CTA covers one merge tile");
     constexpr int NW = TPB / 32;
     static_assert(NW <= 32 && (NW & (NW - 1)) == 0, "warps per CTA: power of two");
