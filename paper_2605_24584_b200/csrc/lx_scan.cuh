@@ -343,7 +343,10 @@ __global__ void __launch_bounds__(kGroupBuckets) lx_group_plan(const TileDesc<R>
 // of the batch size.  Rows carry the g channels (prefix-strict in the VJP),
 // cols the x channels (suffix-strict in the VJP).
 // ---------------------------------------------------------------------------
-constexpr int kAggThreads = 256;
+#ifndef LX_AGG_THREADS
+#define LX_AGG_THREADS 256
+#endif
+constexpr int kAggThreads = LX_AGG_THREADS;
 
 template <class R>
 struct GatherAggArgs {
