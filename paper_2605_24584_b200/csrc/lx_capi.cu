@@ -632,7 +632,7 @@ void launch_main(const char* name, const lx::ms::MainArgs<R>& a, cudaStream_t st
     using namespace lx::ms;
     constexpr int TPB = MainShape<BWD, (NG == 2 || NX == 2)>::TPB, IPT = MainShape<BWD, (NG == 2 || NX == 2)>::IPT;
     auto kern = lx_main<R, NG, NX, BWD, SEQ, TPB, IPT>;
-    constexpr bool os_smem = BWD && NG != 2 && sizeof(R) == 4;
+    constexpr bool os_smem = LX_OS_SMEM && BWD && NG != 2 && sizeof(R) == 4;
     const size_t smem = sizeof(MainShared<R, NG + NX, TPB / 32, BWD ? (NG == 2 ? 2 : 1) : 0, os_smem ? kTile : 0>);
     static int per_sm = 0, sms = 0;
     static std::once_flag once;

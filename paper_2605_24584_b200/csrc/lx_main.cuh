@@ -168,6 +168,11 @@ __device__ __forceinline__ void issue_tile(MainStage<R, NC>& S, const MainArgs<R
 #ifndef LX_BWD_CTAS
 #define LX_BWD_CTAS 256
 #endif
+// fp32 unphased backward: suffix values between the two re-scans in shared
+// memory (1) or registers (0)
+#ifndef LX_OS_SMEM
+#define LX_OS_SMEM 0
+#endif
 template <class R, bool BWD, int TPB>
 constexpr int main_min_blocks() {
     return sizeof(R) != 4 ? 1 : TPB == 256 ? (BWD ? 2 : 3) : (BWD ? LX_BWD_CTAS : LX_MAIN_CTAS) / TPB;
@@ -193,7 +198,7 @@ __global__ void __launch_bounds__(TPB + 32, main_min_blocks<R, BWD, TPB>()) lx_m
     // suffix values recorded per element for the outputs
     constexpr int KS = SEQ ? 1 : (!BWD ? (NG > 0 ? NG : NX) : (PHASED ? 4 : 1));
     constexpr int NACC = BWD ? (PHASED ? 2 : 1) : 0;
-    constexpr bool OS_SMEM = BWD && !PHASED && sizeof(R) == 4;
+    constexpr bool OS_SMEM = LX_OS_SMEM && BWD && !PHASED && sizeof(R) == 4;
     using SM = MainShared<R, NC, NW, NACC, OS_SMEM ? KS * kTile : 0>;
     extern __shared__ __align__(16) unsigned char smem_main[];
     SM& sm = *reinterpret_cast<SM*>(smem_main);
