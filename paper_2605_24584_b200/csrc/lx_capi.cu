@@ -257,9 +257,14 @@ void build_partition(Core& c, int which, cudaStream_t st) {
     const uint32_t* pb = b.staged ? b.spos.as<uint32_t>() : b.perm.as<uint32_t>();
     c.gmap[which][0] = DBuf(((size_t)a.m + 16) * 2, st);
     c.gmap[which][1] = DBuf(((size_t)b.m + 16) * 2, st);
+    const size_t gsm = lx::ms::group_plan_smem<R>();
+    static std::once_flag gonce;
+    std::call_once(gonce, [&] {
+        cudaFuncSetAttribute(lx::ms::lx_group_plan<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm);
+    });
     if (T)
         launch("lx_group_plan", st, [&] {
-            lx::ms::lx_group_plan<R><<<T, lx::ms::kGroupBuckets, 0, st>>>(
+            lx::ms::lx_group_plan<R><<<T, lx::ms::kGroupBuckets, gsm, st>>>(
                 c.desc[which].as<lx::ms::TileDesc<R>>(), T, pa, bucket_shift(a.m), pb, bucket_shift(b.m),
                 c.gmap[which][0].as<uint16_t>(), c.gmap[which][1].as<uint16_t>());
         });

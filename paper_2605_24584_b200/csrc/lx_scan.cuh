@@ -40,7 +40,10 @@ namespace ms {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kItems = 8;
+#ifndef LX_TILE_ITEMS
+#define LX_TILE_ITEMS 8
+#endif
+constexpr int kItems = LX_TILE_ITEMS;  // kTile = kThreads * kItems merged elements per tile
 constexpr int kTile = kThreads * kItems;  // merged elements per tile
 constexpr int kFixThreads = 256;
 
@@ -308,15 +311,30 @@ __device__ __forceinline__ void group_tile(uint16_t (&gmap)[2][kTile], uint32_t 
 // the grouping depends only on the plan (positions and tiles), so it is built
 // once per plan orientation instead of in every apply / backward.
 template <class R>
+constexpr size_t group_plan_smem() {
+    return sizeof(uint32_t) * 2 * kTile + sizeof(uint16_t) * 2 * kTile + sizeof(uint32_t) * 2 * kGroupBuckets +
+           sizeof(uint32_t) * 2 * (kGroupBuckets / 32) + 16;
+}
+
+template <class R>
 __global__ void __launch_bounds__(kGroupBuckets) lx_group_plan(const TileDesc<R>* __restrict__ desc, uint32_t T,
                                                                const uint32_t* __restrict__ posA, int shA,
                                                                const uint32_t* __restrict__ posB, int shB,
                                                                uint16_t* __restrict__ gA, uint16_t* __restrict__ gB) {
     constexpr int TPB = kGroupBuckets, NW = TPB / 32;
-    __shared__ uint32_t sA[kTile], sB[kTile];
-    __shared__ uint16_t gmap[2][kTile];
-    __shared__ uint32_t gcnt[2][kGroupBuckets];
-    __shared__ uint32_t gwarp[2][NW];
+    struct Smem {
+        uint32_t sA[kTile], sB[kTile];
+        uint16_t gmap[2][kTile];
+        uint32_t gcnt[2][kGroupBuckets];
+        uint32_t gwarp[2][NW];
+    };
+    extern __shared__ __align__(16) unsigned char smem_group[];  // dynamic: > 48 KB for large tiles
+    Smem& sm = *reinterpret_cast<Smem*>(smem_group);
+    uint32_t* sA = sm.sA;
+    uint32_t* sB = sm.sB;
+    auto& gmap = sm.gmap;
+    auto& gcnt = sm.gcnt;
+    auto& gwarp = sm.gwarp;
     const int tid = threadIdx.x;
     const uint32_t t = blockIdx.x;
     const TileDesc<R> dt = desc[t], dn = desc[t + 1];
