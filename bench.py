@@ -83,9 +83,12 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + clock-event (throttle) reasons sampled during the timed region by one
+    `nvidia-smi -lms` process started before it (polling from inside this process, by
+    fork + exec or by NVML, was measured to stall the enqueue thread: some runs showed
+    20-60 ms/step of GPU idle).  Only samples taken inside the timed window count."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
@@ -93,29 +96,51 @@ class ClockSampler:
         self.index = index
         self.interval = interval
         self.samples = []
-        self._stop = threading.Event()
-        self._t = None
+        self._p = None
+        self._t0 = self._t1 = None
+        self._lines = []
+        self._first = threading.Event()
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.FIELDS}",
+                                        "--format=csv,noheader,nounits", "-lms", str(int(interval * 1000))],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self._p = None
 
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(self.interval)
+    def _read(self):
+        for line in self._p.stdout:
+            self._lines.append(line)
+            self._first.set()
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        # nvidia-smi's start-up (driver / NVML initialisation) must not overlap the
+        # timed window: wait for its first sample
+        self._first.wait(timeout=30)
+        self._t0 = time.time()
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        self._t1 = time.time()
+        if self._p is None:
+            return
+        time.sleep(min(2.0, self.interval + 0.2))  # let the sample covering the window's end arrive
+        self._p.terminate()
+        try:
+            self._p.wait(timeout=10)
+        except Exception:
+            self._p.kill()
+        import datetime
+        for line in list(self._lines):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                continue
+            if self._t0 - 0.05 <= ts <= self._t1 + 0.05:
+                self.samples.append(f[1:])
 
     def summary(self):
         if not self.samples:
@@ -238,13 +263,14 @@ def run_ours(args, rank, world, dist):
             dist.barrier()
         torch.cuda.synchronize()
 
+    sampler = ClockSampler(local, args.clock_interval)  # started before the warm-up steps
     for _ in range(args.warmup):
         step()
     barrier()
     launches0 = L.kernel_launches()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local, args.clock_interval) as clk:
+    with sampler as clk:
         barrier()
         ev0.record(stream)
         for _ in range(args.steps):
@@ -361,13 +387,14 @@ def run_sharded(args, rank, world, dist, comm_factory):
         comm.all_gather(torch.zeros(1, device=dev))
         torch.cuda.synchronize()
 
+    sampler = ClockSampler(local if not args.sim else 0, args.clock_interval)  # before the warm-up
     for _ in range(args.warmup):
         step()
     barrier()
     launches0 = L.kernel_launches()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local if not args.sim else 0, args.clock_interval) as clk:
+    with sampler as clk:
         barrier()
         ev0.record()
         for _ in range(args.steps):
