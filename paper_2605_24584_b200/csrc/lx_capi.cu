@@ -11,6 +11,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -104,6 +105,32 @@ void init_pool() {
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         }
     });
+}
+
+// Working-set reservation.  The stream-ordered pool maps physical memory on
+// demand; at 2^30 it otherwise kept growing in some runs well after warm-up
+// (fragmentation), and each growth stalled the enqueue thread (measured:
+// 1 run in 4 with 10-60 ms/step of GPU idle).  A plan of m = n + k elements
+// reserves ~1.25x the measured fp32 step footprint (28 B per element) once, as
+// one block that the pool then sub-allocates.  LAPLEX_POOL_RESERVE_GB
+// overrides the size (0 disables).
+void reserve_pool(size_t m, size_t rsz, cudaStream_t st) {
+    static std::mutex mu;
+    static size_t done = 0;
+    size_t bytes = m * 35 * (rsz / 4);
+    if (const char* e = std::getenv("LAPLEX_POOL_RESERVE_GB")) bytes = (size_t)(std::atof(e) * (double)(1ull << 30));
+    if (bytes < (size_t(1) << 31)) return;  // small problems: on-demand growth is cheap
+    std::lock_guard<std::mutex> g(mu);
+    if (bytes <= done) return;
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return;
+    bytes = std::min(bytes, free_b - std::min(free_b, size_t(4) << 30));  // leave headroom
+    void* q = nullptr;
+    if (bytes > done && cudaMallocAsync(&q, bytes, st) == cudaSuccess) {
+        cudaFreeAsync(q, st);
+        done = bytes;
+    }
+    cudaGetLastError();
 }
 
 // stream-ordered device buffer
@@ -563,6 +590,7 @@ template <class R>
 laplex_plan create_plan(const R* a, uint32_t n, const R* b, uint32_t k, double t, const R* phi, const R* psi,
                         cudaStream_t st, const cudaEvent_t* ready = nullptr) {
     init_pool();
+    reserve_pool((size_t)n + k, sizeof(R), st);
     auto core = std::make_shared<Core>();
     core->dtype = sizeof(R) == 8 ? LAPLEX_F64 : LAPLEX_F32;
     cudaGetDevice(&core->device);
