@@ -54,7 +54,10 @@ struct MainStage {
     alignas(16) uint16_t gm[kTile + 32];    // store order (lx_group_plan): A at [offGA], B at [baseGB]
 };
 
-constexpr int kMainStages = 2;
+#ifndef LX_MAIN_STAGES
+#define LX_MAIN_STAGES 2
+#endif
+constexpr int kMainStages = LX_MAIN_STAGES;
 
 template <class R, int NC, int NW, int NACC, int NOS>
 struct MainShared {
