@@ -361,9 +361,17 @@ void radix_sort(const R* raw, uint32_t m, R t, R* vals_out, uint32_t* perm_out, 
     const uint32_t per_block = kHistThreads * kHistItems;
     const uint32_t hgrid = std::max(1u, std::min<uint32_t>((m + per_block - 1) / per_block, (uint32_t)sms * 4));
     const size_t hsmem = (size_t)kHistSub * P * kRadix * sizeof(uint32_t);
-    launch("lx_sort_hist", st, [&] {
-        lx_sort_hist<R><<<hgrid, kHistThreads, hsmem, st>>>(raw, m, t, hist.as<uint32_t>(), bad);
-    });
+    if (kSortRts) {  // histograms + pass 1's per-tile counts in one read of the keys
+        const uint32_t g0 = (tiles + kHistTilesPerCta - 1) / kHistTilesPerCta;
+        launch("lx_sort_hist", st, [&] {
+            lx_sort_hist_count0<R><<<g0, kThreads, 0, st>>>(raw, m, t, hist.as<uint32_t>(), bad, cnt.as<uint32_t>(),
+                                                            tiles);
+        });
+    } else {
+        launch("lx_sort_hist", st, [&] {
+            lx_sort_hist<R><<<hgrid, kHistThreads, hsmem, st>>>(raw, m, t, hist.as<uint32_t>(), bad);
+        });
+    }
     launch("lx_sort_bases", st, [&] {
         lx_sort_bases<P><<<P, kRadix, 0, st>>>(hist.as<uint32_t>(), bases.as<uint32_t>());
     });
@@ -387,13 +395,11 @@ void radix_sort(const R* raw, uint32_t m, R t, R* vals_out, uint32_t* perm_out, 
         const uint32_t* offs = nullptr;
         if (kSortRts) {  // per-(digit, tile) offsets first: the pass needs no look-back
             const uint32_t cgrid = (tiles + kCountTiles - 1) / kCountTiles;
-            launch("lx_sort_count", st, [&] {
-                if (pass == 0)
-                    lx_sort_count<R, true, false><<<cgrid, kThreads, 0, st>>>(in, m, t, 0, cnt.as<uint32_t>(), tiles);
-                else
+            if (pass > 0)  // pass 1's counts came with the histograms
+                launch("lx_sort_count", st, [&] {
                     lx_sort_count<R, false, false><<<cgrid, kThreads, 0, st>>>(in, m, t, pass * kBits,
                                                                                cnt.as<uint32_t>(), tiles);
-            });
+                });
             launch("lx_sort_scan", st, [&] {
                 lx_sort_scan<<<kRadix, kScanThreads, 0, st>>>(cnt.as<uint32_t>(), tiles, bptr, 0);
             });

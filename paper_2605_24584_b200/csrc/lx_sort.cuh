@@ -104,6 +104,68 @@ __global__ void __launch_bounds__(kHistThreads) lx_sort_hist(const R* __restrict
     }
 }
 
+// Reduce-then-scan form of the histogram: the same single read of the raw
+// keys also yields pass 1's per-tile digit counts (its tiles are the raw
+// order), so pass 1 needs no count kernel.  kHistTilesPerCta consecutive pass
+// tiles per CTA keep the global-histogram atomics few.
+constexpr int kHistTilesPerCta = 64;
+
+template <class R>
+__global__ void __launch_bounds__(kThreads) lx_sort_hist_count0(const R* __restrict__ raw, size_t n, R t,
+                                                               uint32_t* __restrict__ hist, int* __restrict__ bad,
+                                                               uint32_t* __restrict__ cnt, uint32_t tiles) {
+    using K = typename Traits<R>::Key;
+    constexpr int P = Traits<R>::kPasses;
+    constexpr int SUB = 4;
+    __shared__ uint32_t wt[kWarps][kRadix];        // this tile's digit-0 counts per warp
+    __shared__ uint32_t gh[SUB][P][kRadix];        // this CTA's histograms of every digit
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < kWarps * kRadix; i += kThreads) (&wt[0][0])[i] = 0;
+    for (int i = tid; i < SUB * P * kRadix; i += kThreads) (&gh[0][0][0])[i] = 0;
+    __syncthreads();
+    uint32_t* mine = &gh[warp % SUB][0][0];
+    int any_bad = 0;
+    const uint32_t t_lo = blockIdx.x * kHistTilesPerCta;
+    const uint32_t t_hi = min(tiles, t_lo + kHistTilesPerCta);
+    for (uint32_t tile = t_lo; tile < t_hi; ++tile) {
+        const size_t base = (size_t)tile * kTile;
+        R v[kItems];
+#pragma unroll
+        for (int q = 0; q < kItems; ++q) {
+            const size_t i = base + (size_t)q * kThreads + tid;
+            v[q] = i < n ? raw[i] : R(0);
+        }
+#pragma unroll
+        for (int q = 0; q < kItems; ++q) {
+            const size_t i = base + (size_t)q * kThreads + tid;
+            if (i >= n) continue;
+            if (!isfinite(v[q])) any_bad = 1;
+            const K key = radix_key<R>(xdiv(v[q], t));
+            atomicAdd(&wt[warp][(int)(key & (kRadix - 1))], 1u);
+#pragma unroll
+            for (int p = 0; p < P; ++p) atomicAdd(&mine[p * kRadix + (int)((key >> (p * kBits)) & (kRadix - 1))], 1u);
+        }
+        __syncthreads();
+        if (tid < kRadix) {
+            uint32_t c = 0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                c += wt[w][tid];
+                wt[w][tid] = 0;
+            }
+            cnt[(size_t)tid * tiles + tile] = c;
+        }
+        __syncthreads();
+    }
+    if (any_bad) atomicOr(bad, 1);
+    for (int i = tid; i < P * kRadix; i += kThreads) {
+        uint32_t c = 0;
+#pragma unroll
+        for (int sub = 0; sub < SUB; ++sub) c += (&gh[sub][0][0])[i];
+        if (c) atomicAdd(&hist[i], c);
+    }
+}
+
 // Exclusive scan of each pass's digit counts -> global bucket bases.
 template <int P>
 __global__ void __launch_bounds__(kRadix) lx_sort_bases(const uint32_t* __restrict__ hist,
