@@ -513,7 +513,7 @@ def main():
     ap.add_argument("--ref-trials", type=int, default=3)
     ap.add_argument("--ref-threads", type=int, default=64)
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--sim", type=int, default=0,
                     help="simulate N range shards with threads on one GPU (functional check only)")

@@ -111,13 +111,14 @@ void init_pool() {
 // demand; at 2^30 it otherwise kept growing in some runs well after warm-up
 // (fragmentation), and each growth stalled the enqueue thread (measured:
 // 1 run in 4 with 10-60 ms/step of GPU idle).  A plan of m = n + k elements
-// reserves ~1.25x the measured fp32 step footprint (28 B per element) once, as
-// one block that the pool then sub-allocates.  LAPLEX_POOL_RESERVE_GB
-// overrides the size (0 disables).
+// reserves 48 B per element once (the device-pointer step peaks at 28 B per
+// element, the host-pointer calls add the uploaded inputs and outputs), as one
+// block that the pool then sub-allocates.  LAPLEX_POOL_RESERVE_GB overrides
+// the size (0 disables).
 void reserve_pool(size_t m, size_t rsz, cudaStream_t st) {
     static std::mutex mu;
     static size_t done = 0;
-    size_t bytes = m * 35 * (rsz / 4);
+    size_t bytes = m * 48 * (rsz / 4);
     if (const char* e = std::getenv("LAPLEX_POOL_RESERVE_GB")) bytes = (size_t)(std::atof(e) * (double)(1ull << 30));
     if (bytes < (size_t(1) << 31)) return;  // small problems: on-demand growth is cheap
     std::lock_guard<std::mutex> g(mu);
