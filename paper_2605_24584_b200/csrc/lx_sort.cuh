@@ -108,7 +108,10 @@ __global__ void __launch_bounds__(kHistThreads) lx_sort_hist(const R* __restrict
 // keys also yields pass 1's per-tile digit counts (its tiles are the raw
 // order), so pass 1 needs no count kernel.  kHistTilesPerCta consecutive pass
 // tiles per CTA keep the global-histogram atomics few.
-constexpr int kHistTilesPerCta = 64;
+#ifndef LX_HIST_TILES
+#define LX_HIST_TILES 64
+#endif
+constexpr int kHistTilesPerCta = LX_HIST_TILES;
 
 template <class R>
 __global__ void __launch_bounds__(kThreads) lx_sort_hist_count0(const R* __restrict__ raw, size_t n, R t,
