@@ -29,7 +29,7 @@ _PREFIX = {"c": "lxo_", "ref": "lxr_"}
 _handles = {}
 
 ERRORS = {0: None, 1: "EmptyInput", 2: "NonFinite", 3: "DimensionMismatch", 4: "PhasePresent",
-          5: "PhaseAbsent", 6: "AsymmetricCotangent", 99: "Error"}
+          5: "PhaseAbsent", 6: "AsymmetricCotangent", 97: "UnverifiedOrder", 99: "Error"}
 
 
 class OracleError(RuntimeError):
@@ -96,6 +96,31 @@ class OracleOp:
         _check(f(_p(self.a), self.n, _p(self.b), self.k, t, _p(self.phi), _p(self.psi), C.byref(h)),
                "LaplexOperator")
         self._h = h
+
+    @classmethod
+    def from_sorted(cls, a, b, t, perm_rows, perm_cols, phi=None, psi=None, dtype=np.float64):
+        """The at-scale oracle: the same operator built over a GIVEN sort order
+        (e.g. the GPU's), which lxo_op_create_sorted first proves equal to the
+        reference's std::stable_sort (see lxo_verify_sort); only the sort itself
+        is skipped, and the co-ranks come from one merge walk.  Raises
+        OracleError(97) when a permutation is not the stable sort."""
+        self = cls.__new__(cls)
+        self.dtype = np.dtype(dtype)
+        self.backend = "c"
+        self.a, self.b = _arr(a, dtype), _arr(b, dtype)
+        self.phi, self.psi = _arr(phi, dtype), _arr(psi, dtype)
+        self.n, self.k = len(self.a), len(self.b)
+        self.t = t
+        pr = np.ascontiguousarray(perm_rows, dtype=np.uint32)
+        pc = np.ascontiguousarray(perm_cols, dtype=np.uint32)
+        h = C.c_void_p()
+        f = _fn("c", "op_create_sorted", dtype)
+        f.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t, _ctype(dtype), C.c_void_p,
+                      C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p)]
+        _check(f(_p(self.a), self.n, _p(self.b), self.k, t, _p(self.phi), _p(self.psi), _p(pr), _p(pc),
+                 C.byref(h)), "LaplexOperator(sorted)")
+        self._h = h
+        return self
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -206,6 +231,18 @@ def sort_anchors(raw, dtype=np.float64, backend="c"):
     f = _fn(backend, "sort_anchors", dtype)
     _check(f(_p(raw), C.c_size_t(m), _p(vals), _p(perm), _p(dec)), "sort_anchors")
     return vals[:m], perm[:m], dec[: max(m - 1, 0)]
+
+
+def verify_sort(raw, t, perm, dtype=np.float64) -> int:
+    """-1 when perm is exactly std::stable_sort of raw/t (scan.hpp:37-40) in
+    `dtype` arithmetic, else the first offending sorted position (len(raw)
+    when perm is not a permutation).  O(m): see lxo_verify_sort."""
+    raw = _arr(raw, dtype)
+    perm = np.ascontiguousarray(perm, dtype=np.uint32)
+    f = _fn("c", "verify_sort", dtype)
+    f.argtypes = [C.c_void_p, C.c_size_t, _ctype(dtype), C.c_void_p]
+    f.restype = C.c_int64
+    return int(f(_p(raw), len(raw), t, _p(perm)))
 
 
 def decay_scan(sorted_values, payload, dtype=np.float64, backend="c"):

@@ -213,3 +213,78 @@ def test_oracle_vs_reference_random(dt):
             assert np.array_equal(oc.matvec(x, d), orf.matvec(x, d))
         for u, v in zip(oc.vjp(x, g), orf.vjp(x, g)):
             assert np.array_equal(u, v)
+
+
+# ------------------------------- (d) the at-scale oracle (given sort order)
+@pytest.mark.parametrize("case", sorted(load("operator.npz")))
+def test_sorted_oracle_matches_reference_golden(case):
+    """OracleOp.from_sorted over the reference's own permutations reproduces
+    every reference output bit for bit (the sort is the only step skipped)."""
+    c = load("operator.npz")[case]
+    dt = c["a"].dtype
+    op = O.OracleOp.from_sorted(c["a"], c["b"], float(c["t"]), c["rows_perm"], c["cols_perm"],
+                                c.get("phi"), c.get("psi"), dtype=dt)
+    assert np.array_equal(op.ranks(0), c["j_of_row"]) and np.array_equal(op.ranks(1), c["r_of_col"])
+    assert np.array_equal(op.sorted(0)[0].view(np.uint8), c["rows_values"].view(np.uint8))
+    if "phi" in c:
+        assert np.array_equal(op.phased_matvec(c["x"]), c["phased_matvec"])
+        for g, key in zip(op.phased_vjp(c["x"], c["g"]), ("x_bar", "a_bar", "b_bar", "phi_bar", "psi_bar")):
+            assert np.array_equal(g, c["pvjp_" + key])
+    else:
+        assert np.array_equal(op.matvec(c["x"], 1), c["matvec_A"])
+        assert np.array_equal(op.matvec(c["x"], 2), c["matvec_B"])
+        assert np.array_equal(op.matvec_transpose(c["g"]), c["matvec_transpose"])
+        for g, key in zip(op.vjp(c["x"], c["g"]), ("x_bar", "a_bar", "b_bar")):
+            assert np.array_equal(g, c["vjp_" + key])
+
+
+@pytest.mark.parametrize("dt", [F64, F32])
+def test_verify_sort_accepts_only_the_stable_sort(dt):
+    rng = np.random.default_rng(5)
+    raw = rng.integers(-20, 20, 5000).astype(dt)  # heavy ties
+    raw[::7] = -0.0
+    raw[::11] = 0.0
+    for t in (1.0, 0.3):
+        _, perm, _ = O.sort_anchors(raw / dt(t), dtype=dt)
+        assert O.verify_sort(raw, t, perm, dtype=dt) == -1
+        # a swapped tie pair keeps the values sorted but breaks stability
+        v = (raw / dt(t))[perm.astype(np.int64)]
+        i = int(np.flatnonzero(v[:-1] == v[1:])[0])
+        bad = perm.copy()
+        bad[i], bad[i + 1] = bad[i + 1], bad[i]
+        assert O.verify_sort(raw, t, bad, dtype=dt) == i
+        # -0 and +0 compare equal: they must stay in index order too
+        z = np.flatnonzero(v == 0)
+        assert O.verify_sort(raw, t, perm, dtype=dt) == -1 and len(z) > 2
+        # not a permutation
+        dup = perm.copy()
+        dup[3] = dup[4]
+        assert O.verify_sort(raw, t, dup, dtype=dt) == len(raw)
+
+
+def test_sorted_oracle_rejects_a_wrong_order():
+    rng = np.random.default_rng(6)
+    a, b = rng.uniform(-5, 5, 300), rng.uniform(-5, 5, 200)
+    pa = np.argsort(a, kind="stable")
+    pb = np.argsort(b, kind="stable")
+    O.OracleOp.from_sorted(a, b, 1.0, pa, pb)
+    with pytest.raises(O.OracleError) as e:
+        O.OracleOp.from_sorted(a, b, 1.0, pa[::-1], pb)
+    assert e.value.code == 97
+
+
+def test_sorted_oracle_equals_sorting_oracle_random():
+    rng = np.random.default_rng(8)
+    for dt in (F64, F32):
+        n, k = 3000, 2000
+        a = rng.uniform(-30, 30, n).astype(dt)
+        b = rng.uniform(-30, 30, k).astype(dt)
+        b[:500] = a[:500]
+        x, g = rng.uniform(-1, 1, k).astype(dt), rng.uniform(-1, 1, n).astype(dt)
+        ref = O.OracleOp(a, b, 0.7, dtype=dt)
+        op = O.OracleOp.from_sorted(a, b, 0.7, ref.sorted(0)[1], ref.sorted(1)[1], dtype=dt)
+        for side in (0, 1):
+            assert np.array_equal(op.ranks(side), ref.ranks(side))
+        assert np.array_equal(op.matvec(x), ref.matvec(x))
+        for u, v in zip(op.vjp(x, g), ref.vjp(x, g)):
+            assert np.array_equal(u, v)
