@@ -140,6 +140,19 @@ class LaplexOperator {
         return Y;
     }
 
+    /// Extension (not a reference member): the Gram-vector product
+    /// Y_r = A^T (A X_r) of SPEC.md:187, i.e. matvec_transpose(matvec(x)) per
+    /// row in one device call; counts as the composition's two matvecs per row.
+    Matrix<Real> batch_gram_matvec(const Matrix<Real>& X) const {
+        if (has_phases()) throw PhasePresent("batch_gram_matvec: operator has phases");
+        if (X.cols != k()) throw DimensionMismatch("batch_gram_matvec: X columns");
+        require_finite(X.data, "batch_gram_matvec X");
+        Matrix<Real> Y(X.rows, k());
+        if (X.rows) throw_for_code(laplex_gram_apply(s_->plan, X.data.data(), X.rows, X.cols, Y.data.data()));
+        stats::matvec_calls().fetch_add(2 * X.rows, std::memory_order_relaxed);
+        return Y;
+    }
+
     GramResult<Real> weighted_gram(const std::vector<Real>& D) const {
         if (has_phases()) throw PhasePresent("weighted_gram: operator has phases");
         return gram(0u, D, "weighted_gram", 1);

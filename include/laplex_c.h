@@ -27,7 +27,8 @@
  * in host memory.  *_dev entry points take device pointers and a
  * cudaStream_t (as void*, NULL = legacy default stream); they are
  * stream-ordered and do not synchronise, except laplex_plan_create_dev which
- * synchronises once to report non-finite anchors synchronously.
+ * synchronises once to report non-finite anchors synchronously (the _async
+ * variant does not).
  *
  * Layout: batches are row-major (rows x cols, leading dimension = cols).
  * Permutations/ranks are returned as uint64 (the reference's size_t).
@@ -81,7 +82,23 @@ int laplex_plan_create(int dtype, const void* a, size_t n, const void* b, size_t
                        const void* phi, const void* psi, laplex_plan* out);
 int laplex_plan_create_dev(int dtype, const void* a, size_t n, const void* b, size_t k, double t,
                            const void* phi, const void* psi, void* stream, laplex_plan* out);
-/* Reference counting (plans are immutable and shareable across threads). */
+/* Same as laplex_plan_create_dev without its one host synchronisation (for
+ * training loops that build a plan per step): non-finite anchors / phases are
+ * then reported by laplex_plan_check (which waits for the build), in the
+ * reference's order; the products of a plan with non-finite anchors are
+ * undefined.  All other argument errors are still returned immediately. */
+int laplex_plan_create_dev_async(int dtype, const void* a, size_t n, const void* b, size_t k, double t,
+                                 const void* phi, const void* psi, void* stream, laplex_plan* out);
+int laplex_plan_check(laplex_plan plan);
+/* Device memory: temporaries and plans come from the library's own
+ * stream-ordered pool per device, trimmed when the device's last plan is
+ * released; laplex_pool_trim synchronises the device and returns every unused
+ * byte now.  LAPLEX_POOL_RESERVE_GB (env) sizes the up-front working-set
+ * reservation of large plans (0 disables). */
+int laplex_pool_trim(void);
+/* Reference counting (plans are immutable and shareable across threads and
+ * streams; release is stream-ordered after every stream that used the plan
+ * and never blocks the host). */
 int laplex_plan_retain(laplex_plan plan);
 int laplex_plan_release(laplex_plan plan);
 /* Role-swapped view sharing the sorted anchors (no re-sort). */
@@ -101,6 +118,13 @@ int laplex_plan_ranks(laplex_plan plan, int side, int strict, uint64_t* ranks);
  * `cols` is the caller's row length (checked -> DimensionMismatch). */
 int laplex_apply(laplex_plan plan, unsigned flags, const void* X, size_t rows, size_t cols, void* Y);
 int laplex_apply_dev(laplex_plan plan, unsigned flags, const void* X, size_t rows, void* Y, void* stream);
+
+/* Gram-vector product Y = A^T (A X) (rows x k -> rows x k) of an unphased
+ * plan: the composition matvec_transpose(matvec(x)) of SPEC.md:187
+ * (operator.hpp:162-172) in one call, with A X kept in sorted-row order on
+ * the device; bitwise equal to the two-call composition.  Errors as matvec. */
+int laplex_gram_apply(laplex_plan plan, const void* X, size_t rows, size_t cols, void* Y);
+int laplex_gram_apply_dev(laplex_plan plan, const void* X, size_t rows, void* Y, void* stream);
 
 /* Cotangents of L = sum_r G_r^T A X_r: x_bar (rows x k), a_bar (n) and
  * b_bar (k) summed over rows; with LAPLEX_PHASED also phi_bar (n), psi_bar (k). */

@@ -26,6 +26,21 @@
 #define LXO_PHASE_ABSENT 5
 #define LXO_ASYMMETRIC_COTANGENT 6
 
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/* Threads of the calling thread's parallel loops (OpenMP ICVs are per thread):
+   callers that run several oracle calls concurrently set 1.  The results do not
+   depend on it. */
+void lxo_set_num_threads(int n) {
+#ifdef _OPENMP
+    omp_set_num_threads(n > 0 ? n : 1);
+#else
+    (void)n;
+#endif
+}
+
 /* double instantiation */
 #define REAL double
 #define SFX _f64

@@ -233,16 +233,30 @@ def sort_anchors(raw, dtype=np.float64, backend="c"):
     return vals[:m], perm[:m], dec[: max(m - 1, 0)]
 
 
-def verify_sort(raw, t, perm, dtype=np.float64) -> int:
+def verify_sort(raw, t, perm, dtype=np.float64, values=None) -> int:
     """-1 when perm is exactly std::stable_sort of raw/t (scan.hpp:37-40) in
-    `dtype` arithmetic, else the first offending sorted position (len(raw)
-    when perm is not a permutation).  O(m): see lxo_verify_sort."""
+    `dtype` arithmetic (and, if given, values == (raw/t)[perm] bitwise), else
+    the first offending sorted position (len(raw) when perm is not a
+    permutation).  O(m): see lxo_verify_sort."""
     raw = _arr(raw, dtype)
     perm = np.ascontiguousarray(perm, dtype=np.uint32)
+    values = None if values is None else _arr(values, dtype)
     f = _fn("c", "verify_sort", dtype)
-    f.argtypes = [C.c_void_p, C.c_size_t, _ctype(dtype), C.c_void_p]
+    f.argtypes = [C.c_void_p, C.c_size_t, _ctype(dtype), C.c_void_p, C.c_void_p]
     f.restype = C.c_int64
-    return int(f(_p(raw), len(raw), t, _p(perm)))
+    return int(f(_p(raw), len(raw), t, _p(perm), _p(values)))
+
+
+def coranks(sorted_rows, sorted_cols, dtype=np.float64):
+    """(j_of_row, r_of_col) of two sorted anchor arrays: std::upper_bound
+    per element (operator.hpp:111-120) as one merge walk each."""
+    A, B = _arr(sorted_rows, dtype), _arr(sorted_cols, dtype)
+    jr = np.empty(len(A), np.uint64)
+    rc = np.empty(len(B), np.uint64)
+    f = _fn("c", "coranks", dtype)
+    f.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]
+    f(_p(A), len(A), _p(B), len(B), _p(jr), _p(rc))
+    return jr, rc
 
 
 def decay_scan(sorted_values, payload, dtype=np.float64, backend="c"):
@@ -278,6 +292,22 @@ def dense_gram(a, b, t, D, phi=None, psi=None, dtype=np.float64):
                   C.c_void_p, C.c_void_p, C.c_void_p]
     f(_p(a), len(a), _p(b), len(b), t, _p(D), _p(phi), _p(psi), _p(G))
     return G
+
+
+def map_rows(fn, items, workers=None):
+    """[fn(item) for item in items] on a thread pool: each worker runs the
+    oracle single-threaded (ctypes releases the GIL, so calls overlap).  For
+    per-row oracle calls of a batch; results are identical to a serial loop."""
+    import concurrent.futures as cf
+    workers = workers or max(1, min(len(items), os.cpu_count() or 1))
+    lib = _lib("c")
+
+    def run(it):
+        lib.lxo_set_num_threads(1)
+        return fn(it)
+
+    with cf.ThreadPoolExecutor(workers) as ex:
+        return list(ex.map(run, items))
 
 
 def rel_err_l2(got, want) -> float:

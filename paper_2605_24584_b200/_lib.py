@@ -28,6 +28,11 @@ _SIGS = {
     "laplex_profile_dump": (C.c_int, [C.c_char_p, sz]),
     "laplex_plan_create": (C.c_int, [C.c_int, vp, sz, vp, sz, C.c_double, vp, vp, C.POINTER(vp)]),
     "laplex_plan_create_dev": (C.c_int, [C.c_int, vp, sz, vp, sz, C.c_double, vp, vp, vp, C.POINTER(vp)]),
+    "laplex_plan_create_dev_async": (C.c_int, [C.c_int, vp, sz, vp, sz, C.c_double, vp, vp, vp, C.POINTER(vp)]),
+    "laplex_plan_check": (C.c_int, [vp]),
+    "laplex_pool_trim": (C.c_int, []),
+    "laplex_gram_apply": (C.c_int, [vp, vp, sz, sz, vp]),
+    "laplex_gram_apply_dev": (C.c_int, [vp, vp, sz, vp, vp]),
     "laplex_plan_retain": (C.c_int, [vp]),
     "laplex_plan_release": (C.c_int, [vp]),
     "laplex_plan_transposed": (C.c_int, [vp, C.POINTER(vp)]),

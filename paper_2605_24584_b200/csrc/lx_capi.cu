@@ -94,53 +94,136 @@ int guarded(F&& f) {
     }
 }
 
-std::once_flag g_pool_once;
-void init_pool() {
-    std::call_once(g_pool_once, [] {
-        int dev = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess) return;
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
+// ---- per-device state ---------------------------------------------------------
+// Everything cached per process is keyed by device, so one process may drive
+// several GPUs (one thread per device, or switching with cudaSetDevice).
+constexpr int kMaxDevices = 64;
+
+int current_device() {
+    int d = 0;
+    ck(cudaGetDevice(&d), "cudaGetDevice");
+    if (d < 0 || d >= kMaxDevices) fail(LAPLEX_E_INVALID_ARGUMENT, "device ordinal out of range");
+    return d;
+}
+
+// The library's own stream-ordered memory pool per device.  Its release
+// threshold is unbounded while plans are alive (per-call temporaries are free
+// after warm-up); when the last plan on the device is released the pool is
+// trimmed, so the memory goes back to the device (and to e.g. torch's caching
+// allocator) instead of staying with the library for the life of the process.
+struct DevState {
+    std::once_flag init;
+    cudaMemPool_t pool = nullptr;
+    int sms = 148;
+    std::mutex mu;
+    size_t reserved = 0;  // working-set reservation currently held by the pool
+    int live_plans = 0;
+    cudaStream_t release = nullptr;  // plan buffers are freed here, after every user stream
+};
+DevState g_dev[kMaxDevices];
+
+DevState& dev_state(int d = -1) {
+    if (d < 0) d = current_device();
+    DevState& s = g_dev[d];
+    std::call_once(s.init, [&] {
+        cudaMemPoolProps props;
+        std::memset(&props, 0, sizeof(props));
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = d;
+        ck(cudaMemPoolCreate(&s.pool, &props), "cudaMemPoolCreate");
+        uint64_t thr = UINT64_MAX;
+        ck(cudaMemPoolSetAttribute(s.pool, cudaMemPoolAttrReleaseThreshold, &thr), "cudaMemPoolSetAttribute");
+        cudaDeviceGetAttribute(&s.sms, cudaDevAttrMultiProcessorCount, d);
+        ck(cudaStreamCreateWithFlags(&s.release, cudaStreamNonBlocking), "cudaStreamCreate");
     });
+    return s;
+}
+
+int num_sms() { return dev_state().sms; }
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device)
+template <class K>
+void smem_attr(K kern, size_t bytes) {
+    static std::mutex mu;
+    static std::vector<std::pair<const void*, int>> done;
+    const int d = current_device();
+    const void* key = reinterpret_cast<const void*>(kern);
+    std::lock_guard<std::mutex> g(mu);
+    for (auto& e : done)
+        if (e.first == key && e.second == d) return;
+    ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes), "cudaFuncSetAttribute");
+    done.emplace_back(key, d);
+}
+
+// resident CTAs per SM of a kernel (after smem_attr), cached per (kernel, device)
+template <class K>
+int occupancy(K kern, int threads, size_t smem) {
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<const void*, int>, int>> done;
+    const int d = current_device();
+    const void* key = reinterpret_cast<const void*>(kern);
+    std::lock_guard<std::mutex> g(mu);
+    for (auto& e : done)
+        if (e.first.first == key && e.first.second == d) return e.second;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+    per_sm = std::max(per_sm, 1);
+    done.push_back({{key, d}, per_sm});
+    return per_sm;
 }
 
 // Working-set reservation.  The stream-ordered pool maps physical memory on
 // demand; at 2^30 it otherwise kept growing in some runs well after warm-up
 // (fragmentation), and each growth stalled the enqueue thread (measured:
 // 1 run in 4 with 10-60 ms/step of GPU idle).  A plan of m = n + k elements
-// reserves 48 B per element once (the device-pointer step peaks at 28 B per
-// element, the host-pointer calls add the uploaded inputs and outputs), as one
-// block that the pool then sub-allocates.  LAPLEX_POOL_RESERVE_GB overrides
-// the size (0 disables).
-void reserve_pool(size_t m, size_t rsz, cudaStream_t st) {
-    static std::mutex mu;
-    static size_t done = 0;
-    size_t bytes = m * 48 * (rsz / 4);
+// reserves its working set once, as one block that the pool then
+// sub-allocates: 36 B per element for device-pointer plans (the step peaks
+// at 28 B per element), 48 B for host-pointer plans (which add the uploaded
+// inputs and outputs).  LAPLEX_POOL_RESERVE_GB overrides the size (0
+// disables).  The reservation lives in the library's pool and is trimmed with
+// it when the device's last plan is released.
+void reserve_pool(size_t m, size_t rsz, size_t per_elem, cudaStream_t st) {
+    DevState& ds = dev_state();
+    size_t bytes = m * per_elem * (rsz / 4);
     if (const char* e = std::getenv("LAPLEX_POOL_RESERVE_GB")) bytes = (size_t)(std::atof(e) * (double)(1ull << 30));
     if (bytes < (size_t(1) << 31)) return;  // small problems: on-demand growth is cheap
-    std::lock_guard<std::mutex> g(mu);
-    if (bytes <= done) return;
+    std::lock_guard<std::mutex> g(ds.mu);
+    if (bytes <= ds.reserved) return;
     size_t free_b = 0, total_b = 0;
     if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return;
     bytes = std::min(bytes, free_b - std::min(free_b, size_t(4) << 30));  // leave headroom
     void* q = nullptr;
-    if (bytes > done && cudaMallocAsync(&q, bytes, st) == cudaSuccess) {
+    if (bytes > ds.reserved && cudaMallocFromPoolAsync(&q, bytes, ds.pool, st) == cudaSuccess) {
         cudaFreeAsync(q, st);
-        done = bytes;
+        ds.reserved = bytes;
     }
     cudaGetLastError();
 }
 
-// stream-ordered device buffer
+void plan_born(int d) {
+    DevState& ds = dev_state(d);
+    std::lock_guard<std::mutex> g(ds.mu);
+    ++ds.live_plans;
+}
+
+void plan_died(int d) {
+    DevState& ds = dev_state(d);
+    std::lock_guard<std::mutex> g(ds.mu);
+    if (--ds.live_plans == 0) {
+        // best effort: frees still queued on streams are returned on the next trim
+        cudaMemPoolTrimTo(ds.pool, 0);
+        ds.reserved = 0;
+    }
+}
+
+// stream-ordered device buffer from the library's pool
 struct DBuf {
     void* p = nullptr;
     cudaStream_t st = nullptr;
     DBuf() = default;
     DBuf(size_t bytes, cudaStream_t s) : st(s) {
-        if (bytes) ck(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync");
+        if (bytes) ck(cudaMallocFromPoolAsync(&p, bytes, dev_state().pool, s), "cudaMallocFromPoolAsync");
     }
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
@@ -204,12 +287,41 @@ struct Core {
     uint32_t T[2] = {0, 0};
     DBuf ranks[4];  // [side*2 + strict]
     bool has_ranks[4] = {false, false, false, false};
-    cudaEvent_t last = nullptr;
+    cudaEvent_t built[2] = {nullptr, nullptr};  // [0]: plan created; [1]: role-swapped data (lazy)
+    int bad_host[4] = {0, 0, 0, 0};
+    // Streams that used the plan, each with an event after its last use.  The
+    // buffers are freed on the device's release stream once it has waited
+    // for all of them: stream-ordered, and the releasing host thread never blocks.
+    std::mutex use_mu;
+    std::vector<std::pair<cudaStream_t, cudaEvent_t>> uses;
+    template <class F>
+    void for_each_buf(F&& f) {
+        for (Side& sd : side)
+            for (DBuf* b : {&sd.vals, &sd.perm, &sd.cph, &sd.sph, &sd.spos, &sd.sdst}) f(*b);
+        for (int o = 0; o < 2; ++o)
+            for (DBuf* b : {&part[o], &desc[o], &sfirst[o], &slast[o], &gmap[o][0], &gmap[o][1]}) f(*b);
+        for (DBuf& b : ranks) f(b);
+    }
     ~Core() {
-        if (last) {
-            cudaEventSynchronize(last);
-            cudaEventDestroy(last);
+        int prev = -1;
+        cudaGetDevice(&prev);
+        cudaSetDevice(device);
+        cudaStream_t rel = dev_state(device).release;
+        for (auto& u : uses) {
+            cudaStreamWaitEvent(rel, u.second, 0);
+            cudaEventDestroy(u.second);
         }
+        for (cudaEvent_t e : built)
+            if (e) {
+                cudaStreamWaitEvent(rel, e, 0);
+                cudaEventDestroy(e);
+            }
+        for_each_buf([&](DBuf& b) {
+            b.st = rel;
+            b.release();
+        });
+        plan_died(device);
+        if (prev >= 0) cudaSetDevice(prev);
     }
 };
 
@@ -286,10 +398,7 @@ void build_partition(Core& c, int which, cudaStream_t st) {
     c.gmap[which][0] = DBuf(((size_t)a.m + 16) * 2, st);
     c.gmap[which][1] = DBuf(((size_t)b.m + 16) * 2, st);
     const size_t gsm = lx::ms::group_plan_smem<R>();
-    static std::once_flag gonce;
-    std::call_once(gonce, [&] {
-        cudaFuncSetAttribute(lx::ms::lx_group_plan<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm);
-    });
+    smem_attr(lx::ms::lx_group_plan<R>, gsm);
     if (T)
         launch("lx_group_plan", st, [&] {
             lx::ms::lx_group_plan<R><<<T, lx::ms::kGroupBuckets, gsm, st>>>(
@@ -302,8 +411,16 @@ template <class R>
 View<R> view(Core& c, bool swapped, cudaStream_t st) {
     const int ia = swapped ? 1 : 0;
     {
+        // The role-swapped orientation is built on first use, on the first
+        // caller's stream; every caller (any stream) orders itself after it.
         std::lock_guard<std::mutex> g(c.mu);
-        if (!c.part[ia].p) build_partition<R>(c, ia, st);
+        if (!c.part[ia].p) {
+            build_partition<R>(c, ia, st);
+            if (!c.built[ia]) ck(cudaEventCreateWithFlags(&c.built[ia], cudaEventDisableTiming), "cudaEventCreate");
+            ck(cudaEventRecord(c.built[ia], st), "cudaEventRecord");
+        }
+        if (c.built[0]) ck(cudaStreamWaitEvent(st, c.built[0], 0), "cudaStreamWaitEvent");
+        if (ia && c.built[1]) ck(cudaStreamWaitEvent(st, c.built[1], 0), "cudaStreamWaitEvent");
     }
     View<R> v;
     const Side& a = c.side[ia];
@@ -357,8 +474,7 @@ void radix_sort(const R* raw, uint32_t m, R t, R* vals_out, uint32_t* perm_out, 
     ck(cudaMemsetAsync(hist.p, 0, (size_t)P * kRadix * 4, st), "memset");
     ck(cudaMemsetAsync(counters.p, 0, (size_t)P * 4, st), "memset");
     if (!kSortRts) ck(cudaMemsetAsync(look.p, 0, (size_t)tiles * kRadix * 8, st), "memset");
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int sms = num_sms();
     const uint32_t per_block = kHistThreads * kHistItems;
     const uint32_t hgrid = std::max(1u, std::min<uint32_t>((m + per_block - 1) / per_block, (uint32_t)sms * 4));
     const size_t hsmem = (size_t)kHistSub * P * kRadix * sizeof(uint32_t);
@@ -377,12 +493,9 @@ void radix_sort(const R* raw, uint32_t m, R t, R* vals_out, uint32_t* perm_out, 
         lx_sort_bases<P><<<P, kRadix, 0, st>>>(hist.as<uint32_t>(), bases.as<uint32_t>());
     });
     const size_t smem = sizeof(PassSmem<R>);
-    static std::once_flag once;
-    std::call_once(once, [&] {
-        cudaFuncSetAttribute(lx_sort_pass<R, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(lx_sort_pass<R, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(lx_sort_pass<R, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    });
+    smem_attr(lx_sort_pass<R, true, false>, smem);
+    smem_attr(lx_sort_pass<R, false, false>, smem);
+    smem_attr(lx_sort_pass<R, false, true>, smem);
     const void* in = raw;
     const uint32_t* inv = nullptr;
     for (int pass = 0; pass < P; ++pass) {
@@ -454,11 +567,7 @@ void build_splan(Side& sd, cudaStream_t st) {
         offs = cnt.as<uint32_t>();
     }
     const size_t smem = sizeof(PassSmem<float>);
-    static std::once_flag once;
-    std::call_once(once, [&] {
-        cudaFuncSetAttribute(lx_sort_pass<float, false, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    });
+    smem_attr(lx_sort_pass<float, false, false, true>, smem);
     launch("lx_splan", st, [&] {
         lx_sort_pass<float, false, false, true><<<tiles, kThreads, smem, st>>>(
             sd.perm.p, nullptr, sd.sdst.p, sd.spos.as<uint32_t>(), m, 1.0f, shift, nullptr,
@@ -491,8 +600,7 @@ void build_side(Side& sd, const R* raw, uint32_t m, R t, const R* phase, int* ba
 
 // ---- permutation application ------------------------------------------------
 int grid_for(size_t work) {
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int sms = num_sms();
     const size_t blocks = (work + 255) / 256;
     return (int)std::max<size_t>(1, std::min<size_t>(blocks, (size_t)sms * 16));
 }
@@ -583,27 +691,49 @@ __global__ void finite_check(const R* __restrict__ v, size_t m, int* __restrict_
 template <class R>
 void launch_finite(const R* v, size_t m, int* bad, cudaStream_t st) {
     if (!m) return;
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int sms = num_sms();
     const size_t blocks = std::min<size_t>((m + 1023) / 1024, (size_t)sms * 8);
     launch("finite_check", st, [&] { finite_check<R><<<(unsigned)blocks, 256, 0, st>>>(v, m, bad); });
+}
+
+// Record the end of this call's work on st (see Core::uses).
+void touch(Core& c, cudaStream_t st) {
+    std::lock_guard<std::mutex> g(c.use_mu);
+    for (auto& u : c.uses)
+        if (u.first == st) {
+            ck(cudaEventRecord(u.second, st), "cudaEventRecord");
+            return;
+        }
+    cudaEvent_t e;
+    ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    ck(cudaEventRecord(e, st), "cudaEventRecord");
+    c.uses.emplace_back(st, e);
+}
+
+// NonFinite of the anchors / phases found by the plan build, in the
+// reference's check order (operator.hpp:88-101); the flags must be on the host.
+void raise_bad(const Core& c) {
+    if (c.bad_host[0]) fail(LAPLEX_E_NON_FINITE, "LaplexOperator row anchors: non-finite entry");
+    if (c.bad_host[1]) fail(LAPLEX_E_NON_FINITE, "LaplexOperator col anchors: non-finite entry");
+    if (c.bad_host[2]) fail(LAPLEX_E_NON_FINITE, "LaplexOperator phases: non-finite entry");
 }
 
 // ready[s]: optional event the build of side s waits for (host-pointer API:
 // side 1 is still uploading while side 0 sorts).  Non-finite anchors (found by
 // the histogram pass) and phases raise NonFinite after the one synchronisation,
 // in the reference's check order (operator.hpp:88-101).
+// sync = false (laplex_plan_create_dev_async): no host synchronisation; the
+// finiteness flags land in the plan and laplex_plan_check reports them.
 template <class R>
 laplex_plan create_plan(const R* a, uint32_t n, const R* b, uint32_t k, double t, const R* phi, const R* psi,
-                        cudaStream_t st, const cudaEvent_t* ready = nullptr) {
-    init_pool();
-    reserve_pool((size_t)n + k, sizeof(R), st);
+                        cudaStream_t st, const cudaEvent_t* ready = nullptr, bool sync = true) {
+    reserve_pool((size_t)n + k, sizeof(R), ready ? 48 : 36, st);
     auto core = std::make_shared<Core>();
     core->dtype = sizeof(R) == 8 ? LAPLEX_F64 : LAPLEX_F32;
-    cudaGetDevice(&core->device);
+    core->device = current_device();
+    plan_born(core->device);
     core->t = t;
     core->phased = phi != nullptr;
-    ck(cudaEventCreateWithFlags(&core->last, cudaEventDisableTiming), "cudaEventCreate");
     DBuf bad(sizeof(int) * 4, st);
     ck(cudaMemsetAsync(bad.p, 0, sizeof(int) * 4, st), "memset");
     if (ready) ck(cudaStreamWaitEvent(st, ready[0], 0), "cudaStreamWaitEvent");
@@ -615,19 +745,20 @@ laplex_plan create_plan(const R* a, uint32_t n, const R* b, uint32_t k, double t
         launch_finite<R>(psi, k, bad.as<int>() + 2, st);
     }
     build_partition<R>(*core, 0, st);
-    int hbad[4] = {0, 0, 0, 0};
-    ck(cudaMemcpyAsync(hbad, bad.p, sizeof(hbad), cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
-    ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
-    if (hbad[0]) fail(LAPLEX_E_NON_FINITE, "LaplexOperator row anchors: non-finite entry");
-    if (hbad[1]) fail(LAPLEX_E_NON_FINITE, "LaplexOperator col anchors: non-finite entry");
-    if (hbad[2]) fail(LAPLEX_E_NON_FINITE, "LaplexOperator phases: non-finite entry");
-    ck(cudaEventRecord(core->last, st), "cudaEventRecord");
+    ck(cudaMemcpyAsync(core->bad_host, bad.p, sizeof(core->bad_host), cudaMemcpyDeviceToHost, st),
+       "cudaMemcpyAsync");
+    touch(*core, st);
+    ck(cudaEventCreateWithFlags(&core->built[0], cudaEventDisableTiming), "cudaEventCreate");
+    ck(cudaEventRecord(core->built[0], st), "cudaEventRecord");
+    if (sync) {
+        ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+        raise_bad(*core);
+    }
     auto* p = new laplex_plan_s;
     p->core = core;
     return p;
 }
 
-void touch(Core& c, cudaStream_t st) { cudaEventRecord(c.last, st); }
 
 // ---- apply --------------------------------------------------------------------
 template <class R>
@@ -674,14 +805,8 @@ void launch_main(const char* name, const lx::ms::MainArgs<R>& a, cudaStream_t st
     auto kern = lx_main<R, NG, NX, BWD, SEQ, TPB, IPT>;
     constexpr bool os_smem = LX_OS_SMEM && BWD && NG != 2 && sizeof(R) == 4;
     const size_t smem = sizeof(MainShared<R, NG + NX, TPB / 32, BWD ? (NG == 2 ? 2 : 1) : 0, os_smem ? kTile : 0>);
-    static int per_sm = 0, sms = 0;
-    static std::once_flag once;
-    std::call_once(once, [&] {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TPB + 32, smem);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-        if (per_sm < 1) per_sm = 1;
-    });
+    smem_attr(kern, smem);
+    const int per_sm = occupancy(kern, TPB + 32, smem), sms = num_sms();
     // persistent: one CTA per resident slot, tiles claimed in order
     const uint32_t grid = std::max<uint32_t>(1u, std::min<uint32_t>(a.T, (uint32_t)(sms * per_sm)));
     DBuf ctr(4, st);
@@ -1016,12 +1141,72 @@ void do_backward(laplex_plan_s* p, unsigned flags, const R* X, const R* G, size_
         if (before_g) before_g();
         ck(cudaMemsetAsync(abar, 0, (size_t)v.n * sizeof(R), st), "memset");
         ck(cudaMemsetAsync(bbar, 0, (size_t)v.k * sizeof(R), st), "memset");
+        if (ph && phibar) ck(cudaMemsetAsync(phibar, 0, (size_t)v.n * sizeof(R), st), "memset");
+        if (ph && psibar) ck(cudaMemsetAsync(psibar, 0, (size_t)v.k * sizeof(R), st), "memset");
+        touch(c, st);
         return;
     }
     if (ph)
         backward_impl<R, 2>(v, X, G, (int)rows, xbar, abar, bbar, phibar, psibar, st, before_g);
     else
         backward_impl<R, 1>(v, X, G, (int)rows, xbar, abar, bbar, nullptr, nullptr, st, before_g);
+    touch(c, st);
+}
+
+__global__ void lx_iota(uint32_t* __restrict__ out, uint32_t m) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) out[i] = i;
+}
+
+// Gram-vector product Y = A^T (A X) (matvec_transpose(matvec(x)),
+// operator.hpp:162-172), one pass pair over the plan.  The intermediate
+// Z = A X never leaves sorted-row order: the forward stores it at the sorted
+// position (output index = identity) and the transpose reads it as its
+// already-sorted payload, so Z pays no scatter and no gather (SURVEY 8(d):
+// 84n + 92k + B(8n + 8k) bytes incl. the plan).  Per row, the arithmetic is the
+// forward's and the transpose's exactly, so Y is bitwise equal to
+// laplex_apply(TRANSPOSE) of laplex_apply(X).
+template <class R>
+void do_gram_apply(laplex_plan_s* p, const R* X, size_t rows, R* Y, cudaStream_t st) {
+    Core& c = *p->core;
+    if (c.phased) fail(LAPLEX_E_PHASE_PRESENT, "gram_apply: operator has phases (matvec is unphased)");
+    if (rows == 0) return;
+    if (rows > 0x7fffffff) fail(LAPLEX_E_INVALID_SIZE, "too many rows");
+    View<R> v = view<R>(c, p->swapped, st);
+    const int nr = (int)rows;
+    DBuf zs((size_t)rows * v.n * sizeof(R) + kTmaPad, st);  // Z in sorted-row order
+    {
+        DBuf iota((size_t)v.n * 4 + 16, st);
+        launch("lx_iota", st, [&] { lx_iota<<<(v.n + 255) / 256, 256, 0, st>>>(iota.as<uint32_t>(), v.n); });
+        auto w = fwd_begin<R, 1>(v, X, nr, st);
+        auto& a = w->a;
+        a.ext = nullptr;
+        a.y = zs.as<R>();
+        a.perm_a = iota.as<uint32_t>();
+        a.ldy = v.n;
+        if (v.n) launch_main<R, 0, 1, false>("lx_main_fwd", a, st);
+    }
+    // Y = A^T Z, Z already sorted (apply_trn with the gather skipped)
+    auto a = main_args(v, nr);
+    Scratch sc(2, nr, v.T, sizeof(R), st);
+    DBuf gs = sorted_payload<R, 1, true, true, false>(v, nr, zs.as<R>(), sc, 0, a.ldgs, st, true);
+    zs.release();
+    a.Gs = gs.as<R>();
+    scan_carries<R, 1>(v, sc, nr, 0u, 0u, st);
+    a.cp = sc.cp.as<R>();
+    a.cq = sc.cq.as<R>();
+    DBuf yst;
+    if (v.dst_b) {
+        yst = DBuf((size_t)rows * v.k * sizeof(R), st);
+        a.y = yst.as<R>();
+        a.perm_b = v.pos_b;
+    } else {
+        a.y = Y;
+    }
+    a.ldy = v.k;
+    launch_main<R, 1, 0, false>("lx_main_trn", a, st);
+    gs.release();
+    if (v.dst_b) stage_scatter<R>(v.dst_b, v.k, yst.as<R>(), Y, v.k, nr, nullptr, nullptr, nullptr, nullptr, st);
     touch(c, st);
 }
 
@@ -1095,10 +1280,9 @@ void do_ranks(laplex_plan_s* p, int side, int strict, uint64_t* out, cudaStream_
     Core& c = *p->core;
     // physical side of the request
     const int phys = p->swapped ? 1 - side : side;
-    const int ia = p->swapped ? 1 : 0;  // view's row side
-    (void)ia;
     const int slot = phys * 2 + (strict ? 1 : 0);
     std::lock_guard<std::mutex> g(c.mu);
+    ck(cudaStreamWaitEvent(st, c.built[0], 0), "cudaStreamWaitEvent");
     if (!c.has_ranks[slot]) {
         // rows = physical side 0, cols = physical side 1.  A-first merge of
         // (rows, cols) gives J<(rows) and R<=(cols); B-first gives J<=, R<.
@@ -1141,7 +1325,6 @@ void do_ranks(laplex_plan_s* p, int side, int strict, uint64_t* out, cudaStream_
 
 template <class R>
 void do_scan(const R* sorted, uint32_t m, const R* payload, R* pre, R* suf, cudaStream_t st) {
-    init_pool();
     using namespace lx::ms;
     const uint32_t T = tiles_for(m);
     DBuf vals((size_t)m * sizeof(R) + kTmaPad, st), pay((size_t)m * sizeof(R), st);
@@ -1508,33 +1691,65 @@ int laplex_plan_create(int dtype, const void* a, size_t n, const void* b, size_t
         *out = nullptr;
         dtype_check(dtype);
         cudaStream_t st = host_stream();
-        init_pool();
-        if (dtype == LAPLEX_F64)
+            if (dtype == LAPLEX_F64)
             *out = create_from_host<double>(a, n, b, k, t, phi, psi, st);
         else
             *out = create_from_host<float>(a, n, b, k, t, phi, psi, st);
     });
 }
 
-int laplex_plan_create_dev(int dtype, const void* a, size_t n, const void* b, size_t k, double t, const void* phi,
-                           const void* psi, void* stream, laplex_plan* out) {
+// Device-pointer plan creation.  `shard`: a range shard may hold no anchors on
+// one side.  `sync` false: no host synchronisation (NonFinite anchors are
+// reported later by laplex_plan_check).
+static int create_dev(int dtype, const void* a, size_t n, const void* b, size_t k, double t, const void* phi,
+                      const void* psi, void* stream, laplex_plan* out, bool shard, bool sync) {
     return guarded([&] {
         if (!out) fail(LAPLEX_E_INVALID_ARGUMENT, "out is NULL");
         *out = nullptr;
         dtype_check(dtype);
-        if (n == 0 || k == 0) fail(LAPLEX_E_EMPTY_INPUT, "LaplexOperator: empty anchor set");
-        if (!(t > 0.0) || !std::isfinite(t))
-            fail(LAPLEX_E_NON_FINITE, "LaplexOperator: temperature must be positive and finite");
-        if ((phi == nullptr) != (psi == nullptr))
-            fail(LAPLEX_E_DIMENSION_MISMATCH, "LaplexOperator: phases must be given for both sides");
+        if (shard ? n + k == 0 : (n == 0 || k == 0))
+            fail(LAPLEX_E_EMPTY_INPUT, shard ? "shard plan: no anchors on this shard" : "LaplexOperator: empty anchor set");
+        // t as the plan's Real: an fp32 plan rejects a t that is 0 or inf once rounded
+        const CreateChecks cc = create_checks(dtype == LAPLEX_F32 ? (double)(float)t : t, phi != nullptr,
+                                              psi != nullptr);
+        if (cc.code) fail(cc.code, cc.msg);
         if (n >= 0x80000000ull || k >= 0x80000000ull) fail(LAPLEX_E_INVALID_SIZE, "n and k must be < 2^31");
         cudaStream_t st = as_stream(stream);
         if (dtype == LAPLEX_F64)
             *out = create_plan<double>((const double*)a, (uint32_t)n, (const double*)b, (uint32_t)k, t,
-                                       (const double*)phi, (const double*)psi, st);
+                                       (const double*)phi, (const double*)psi, st, nullptr, sync);
         else
             *out = create_plan<float>((const float*)a, (uint32_t)n, (const float*)b, (uint32_t)k, t,
-                                      (const float*)phi, (const float*)psi, st);
+                                      (const float*)phi, (const float*)psi, st, nullptr, sync);
+    });
+}
+
+int laplex_plan_create_dev(int dtype, const void* a, size_t n, const void* b, size_t k, double t, const void* phi,
+                           const void* psi, void* stream, laplex_plan* out) {
+    return create_dev(dtype, a, n, b, k, t, phi, psi, stream, out, false, true);
+}
+
+int laplex_plan_create_dev_async(int dtype, const void* a, size_t n, const void* b, size_t k, double t,
+                                 const void* phi, const void* psi, void* stream, laplex_plan* out) {
+    return create_dev(dtype, a, n, b, k, t, phi, psi, stream, out, false, false);
+}
+
+int laplex_plan_check(laplex_plan plan) {
+    return guarded([&] {
+        check_plan(plan);
+        Core& c = *plan->core;
+        ck(cudaEventSynchronize(c.built[0]), "cudaEventSynchronize");
+        raise_bad(c);
+    });
+}
+
+int laplex_pool_trim(void) {
+    return guarded([&] {
+        DevState& ds = dev_state();
+        ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+        std::lock_guard<std::mutex> g(ds.mu);
+        ck(cudaMemPoolTrimTo(ds.pool, 0), "cudaMemPoolTrimTo");
+        ds.reserved = 0;
     });
 }
 
@@ -1580,6 +1795,7 @@ int laplex_plan_sorted(laplex_plan plan, int side, void* values, uint64_t* perm,
         const int phys = plan->swapped ? 1 - side : side;
         const Side& sd = c.side[phys];
         cudaStream_t st = host_stream();
+        ck(cudaStreamWaitEvent(st, c.built[0], 0), "cudaStreamWaitEvent");
         const size_t rs = rsize(c.dtype);
         if (values) ck(cudaMemcpyAsync(values, sd.vals.p, (size_t)sd.m * rs, cudaMemcpyDeviceToHost, st), "D2H");
         std::vector<uint32_t> hp;
@@ -1610,10 +1826,6 @@ int laplex_plan_ranks(laplex_plan plan, int side, int strict, uint64_t* ranks) {
     return guarded([&] {
         check_plan(plan);
         if (side != LAPLEX_ROWS && side != LAPLEX_COLS) fail(LAPLEX_E_INVALID_ARGUMENT, "side");
-        if (plan->swapped) {
-            // ranks of a role-swapped view: rows of the view are the physical
-            // cols, and "<=" / "<" keep their meaning relative to the view.
-        }
         if (plan->core->dtype == LAPLEX_F64)
             do_ranks<double>(plan, side, strict, ranks, host_stream());
         else
@@ -1660,6 +1872,52 @@ int laplex_apply(laplex_plan plan, unsigned flags, const void* X, size_t rows, s
             {
                 HookScope hs(&dl.hook);
                 do_apply<R>(plan, flags, dx.get(), rows, dy.as<R>(), st);
+            }
+            dl.finish(st);
+        };
+        if (c.dtype == LAPLEX_F64)
+            run(0.0);
+        else
+            run(0.0f);
+    });
+}
+
+int laplex_gram_apply_dev(laplex_plan plan, const void* X, size_t rows, void* Y, void* stream) {
+    return guarded([&] {
+        check_plan(plan);
+        if (plan->core->dtype == LAPLEX_F64)
+            do_gram_apply<double>(plan, (const double*)X, rows, (double*)Y, as_stream(stream));
+        else
+            do_gram_apply<float>(plan, (const float*)X, rows, (float*)Y, as_stream(stream));
+    });
+}
+
+int laplex_gram_apply(laplex_plan plan, const void* X, size_t rows, size_t cols, void* Y) {
+    return guarded([&] {
+        check_plan(plan);
+        Core& c = *plan->core;
+        const int ia = plan->swapped ? 1 : 0;
+        const size_t k = c.side[1 - ia].m;
+        // the composition's checks: matvec (operator.hpp:162-165,255-257) first
+        if (c.phased) fail(LAPLEX_E_PHASE_PRESENT, "matvec: operator has phases");
+        if (cols != k) fail(LAPLEX_E_DIMENSION_MISMATCH, "matvec: x length");
+        cudaStream_t st = host_stream();
+        auto run = [&](auto zero) {
+            using R = decltype(zero);
+            HostUp<R> dx(X, rows * cols, st);
+            DBuf dy(rows * k * sizeof(R), st);
+            Flags f(1, st);
+            dx.wait(st);
+            launch_finite<R>(dx.get(), rows * cols, f.at(0), st);
+            f.snapshot(st);
+            Downloader dl(sizeof(R));
+            dl.check = [&] {
+                if (f.wait()[0]) fail(LAPLEX_E_NON_FINITE, "matvec x: non-finite entry");
+            };
+            dl.add(dy.p, Y, k, (int)rows);
+            {
+                HookScope hs(&dl.hook);
+                do_gram_apply<R>(plan, dx.get(), rows, dy.as<R>(), st);
             }
             dl.finish(st);
         };
@@ -1822,8 +2080,7 @@ int laplex_sort(int dtype, const void* raw, size_t m, void* values, uint64_t* pe
         if (m == 0) fail(LAPLEX_E_EMPTY_INPUT, "sort_anchors: empty input");
         if (m >= 0x80000000ull) fail(LAPLEX_E_INVALID_SIZE, "m must be < 2^31");
         cudaStream_t st = host_stream();
-        init_pool();
-        auto run = [&](auto zero) {
+            auto run = [&](auto zero) {
             using R = decltype(zero);
             if (!host_finite((const R*)raw, m)) fail(LAPLEX_E_NON_FINITE, "sort_anchors: non-finite entry");
             HostUp<R> dr(raw, m, st);
@@ -1869,22 +2126,7 @@ int laplex_scan(int dtype, const void* sorted_values, size_t m, const void* payl
 // ---------------------------------------------------------------------------
 int laplex_shard_plan_create_dev(int dtype, const void* a, size_t n, const void* b, size_t k, double t,
                                  const void* phi, const void* psi, void* stream, laplex_plan* out) {
-    return guarded([&] {
-        if (!out) fail(LAPLEX_E_INVALID_ARGUMENT, "out is NULL");
-        *out = nullptr;
-        dtype_check(dtype);
-        if (n + k == 0) fail(LAPLEX_E_EMPTY_INPUT, "shard plan: no anchors on this shard");
-        if (!(t > 0.0) || !std::isfinite(t))
-            fail(LAPLEX_E_NON_FINITE, "LaplexOperator: temperature must be positive and finite");
-        if (n >= 0x80000000ull || k >= 0x80000000ull) fail(LAPLEX_E_INVALID_SIZE, "n and k must be < 2^31");
-        cudaStream_t st = as_stream(stream);
-        if (dtype == LAPLEX_F64)
-            *out = create_plan<double>((const double*)a, (uint32_t)n, (const double*)b, (uint32_t)k, t,
-                                       (const double*)phi, (const double*)psi, st);
-        else
-            *out = create_plan<float>((const float*)a, (uint32_t)n, (const float*)b, (uint32_t)k, t,
-                                      (const float*)phi, (const float*)psi, st);
-    });
+    return create_dev(dtype, a, n, b, k, t, phi, psi, stream, out, true, true);
 }
 
 int laplex_shard_partition_dev(int dtype, const void* raw, size_t m, double t, const void* splitters, int nsplit,
@@ -1893,8 +2135,7 @@ int laplex_shard_partition_dev(int dtype, const void* raw, size_t m, double t, c
         dtype_check(dtype);
         if (nsplit < 0 || nsplit >= lx::shard::kMaxShards) fail(LAPLEX_E_INVALID_ARGUMENT, "nsplit");
         cudaStream_t st = as_stream(stream);
-        init_pool();
-        const int nsh = nsplit + 1;
+            const int nsh = nsplit + 1;
         if (m == 0) {
             ck(cudaMemsetAsync(counts, 0, (size_t)nsh * 4, st), "memset");
             return;

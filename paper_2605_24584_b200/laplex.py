@@ -140,8 +140,6 @@ class LaplexOperator:
         b = _host(col_anchors, self.dtype)
         phi = None if row_phases is None or len(row_phases) == 0 else _host(row_phases, self.dtype)
         psi = None if col_phases is None or len(col_phases) == 0 else _host(col_phases, self.dtype)
-        if (phi is None) != (psi is None) and not (len(a) == 0 or len(b) == 0):
-            pass  # the C-ABI reports DimensionMismatch in reference order
         if phi is not None and psi is not None and (len(phi) != len(a) or len(psi) != len(b)):
             # operator.hpp:96-98: lengths checked after emptiness/finiteness of anchors
             if len(a) == 0 or len(b) == 0:
@@ -239,6 +237,17 @@ class LaplexOperator:
         if X.ndim != 2:
             raise DimensionMismatch("batch_matvec: X must be 2-D")
         return self._apply(0, X, X.shape[0], X.shape[1], self.n())
+
+    def batch_gram_matvec(self, X) -> np.ndarray:
+        """Y = A^T (A X^T) row by row: the Gram-vector composition
+        matvec_transpose(matvec(x)) of SPEC.md:187 in one device call (the
+        intermediate stays in sorted order on the device; bitwise equal to
+        the composition).  Extension: not a member of the reference class."""
+        X = np.atleast_2d(_host(X, self.dtype))
+        rows, cols = X.shape
+        Y = np.empty((rows, self.k()), self.dtype)
+        _check(lib().laplex_gram_apply(self._h, _p(X), rows, cols, _p(Y)))
+        return Y
 
     def phased_matvec(self, x, dispatch: Dispatch = Dispatch.Auto) -> np.ndarray:
         x = _host(x, self.dtype)
@@ -386,6 +395,15 @@ class DeviceOperator:
         _check(lib().laplex_apply_dev(self._h, flags, X.data_ptr(), rows, out.data_ptr(), self._stream(stream)))
         return out
 
+    def gram_apply(self, X, out=None, stream=None):
+        """Y = A^T (A X) per row (rows x k -> rows x k), stream-ordered."""
+        torch = self.torch
+        rows = X.shape[0] if X.dim() == 2 else 1
+        if out is None:
+            out = torch.empty((rows, self.k), dtype=self.dtype, device=X.device)
+        _check(lib().laplex_gram_apply_dev(self._h, X.data_ptr(), rows, out.data_ptr(), self._stream(stream)))
+        return out
+
     def backward(self, X, G, x_bar=None, a_bar=None, b_bar=None, phi_bar=None, psi_bar=None, stream=None):
         torch = self.torch
         rows = X.shape[0] if X.dim() == 2 else 1
@@ -407,6 +425,24 @@ class DeviceOperator:
                                          phi_bar.data_ptr() if phi_bar is not None else None,
                                          psi_bar.data_ptr() if psi_bar is not None else None, self._stream(stream)))
         return x_bar, a_bar, b_bar, phi_bar, psi_bar
+
+
+    # ---- accessors (operator.hpp:151-154), copied to the host ----
+    def sorted(self, side: int):
+        """(values, perm) of one side in sorted order: numpy arrays of the plan's
+        dtype and uint32 (the device layout; the reference's size_t values fit)."""
+        m = self.n if side == ROWS else self.k
+        vals = np.empty(m, np.float64 if self.dtype == self.torch.float64 else np.float32)
+        perm = np.empty(m, np.uint64)
+        _check(lib().laplex_plan_sorted(self._h, side, _p(vals), _p(perm), None))
+        return vals, perm.astype(np.uint32)
+
+    def ranks(self, side: int, strict: bool = False) -> np.ndarray:
+        """side ROWS: j_of_row (J<=), COLS: r_of_col (R<=) -- operator.hpp:111-120."""
+        m = self.n if side == ROWS else self.k
+        out = np.empty(m, np.uint64)
+        _check(lib().laplex_plan_ranks(self._h, side, int(strict), _p(out)))
+        return out
 
 
 def kernel_launches() -> int:
