@@ -91,10 +91,12 @@ int laplex_plan_create_dev_async(int dtype, const void* a, size_t n, const void*
                                  const void* phi, const void* psi, void* stream, laplex_plan* out);
 int laplex_plan_check(laplex_plan plan);
 /* Device memory: temporaries and plans come from the library's own
- * stream-ordered pool per device, trimmed when the device's last plan is
- * released; laplex_pool_trim synchronises the device and returns every unused
- * byte now.  LAPLEX_POOL_RESERVE_GB (env) sizes the up-front working-set
- * reservation of large plans (0 disables). */
+ * stream-ordered pool per device (a caching allocator, separate from the
+ * device's default pool): freed blocks stay with it for reuse until
+ * laplex_pool_trim, which synchronises the device and returns every unused
+ * byte (the analogue of torch.cuda.empty_cache).  LAPLEX_POOL_RESERVE_GB
+ * (env) sizes the up-front working-set reservation of large plans (0
+ * disables). */
 int laplex_pool_trim(void);
 /* Reference counting (plans are immutable and shareable across threads and
  * streams; release is stream-ordered after every stream that used the plan
@@ -142,10 +144,24 @@ int laplex_gram_dev(laplex_plan plan, unsigned flags, const void* D, void* M, vo
 int laplex_gram_vjp_weights(laplex_plan plan, const void* D, size_t dlen, const void* G_bar, size_t grows,
                             size_t gcols, void* D_bar);
 
-/* Free functions of scan.hpp. */
+/* Device variant: G_bar (n x n) and D_bar (k) are device pointers.  The
+ * finiteness / symmetry checks of gradients.hpp:196-205 run on the device and
+ * the call synchronises once to report them. */
+int laplex_gram_vjp_weights_dev(laplex_plan plan, const void* G_bar, void* D_bar, void* stream);
+
+/* Free functions of scan.hpp: sort_anchors (scan.hpp:27-46) and
+ * prefix/suffix_decay_scan (scan.hpp:50-73) on sorted values. */
 int laplex_sort(int dtype, const void* raw, size_t m, void* values, uint64_t* perm, void* decays);
 int laplex_scan(int dtype, const void* sorted_values, size_t m, const void* payload, void* prefix,
                 void* suffix);
+/* Device variants.  laplex_sort_dev: values[m], perm[m] (uint32, the device
+ * layout), decays[m-1] (may be NULL); with nonfinite == NULL it synchronises
+ * once to return NonFinite, else *nonfinite (device int) is set instead and
+ * the call is stream-ordered.  laplex_scan_dev: prefix / suffix may be NULL. */
+int laplex_sort_dev(int dtype, const void* raw, size_t m, void* values, uint32_t* perm, void* decays,
+                    int* nonfinite, void* stream);
+int laplex_scan_dev(int dtype, const void* sorted_values, size_t m, const void* payload, void* prefix,
+                    void* suffix, void* stream);
 
 /* ---- range-sharded operator (multi-GPU) ----------------------
  * A long vector is split over ranks by VALUE: shard(v) = #{splitters < v} with
@@ -180,6 +196,45 @@ int laplex_shard_backward_begin(laplex_plan plan, unsigned flags, const void* X,
 int laplex_shard_backward_end(laplex_work work, const void* ext, void* x_bar, void* a_bar, void* b_bar,
                               void* phi_bar, void* psi_bar, void* stream);
 int laplex_work_release(laplex_work work);
+
+/* ---- multi-GPU host layer, C++ in the library ---------------
+ * Communicators: NCCL (libnccl.so.2 resolved at run time; rank 0 makes the
+ * 128-byte id, the caller broadcasts it, every rank calls
+ * laplex_comm_init_nccl on its device) or "local" (ranks are threads of one
+ * process sharing `key`, e.g. N shards on one GPU).  Collectives are
+ * stream-ordered on the stream each call is given. */
+typedef struct laplex_comm_s* laplex_comm;
+int laplex_nccl_unique_id(void* id128);
+int laplex_comm_init_nccl(const void* id128, int world, int rank, laplex_comm* out);
+int laplex_comm_init_local(uint64_t key, int world, int rank, laplex_comm* out);
+int laplex_comm_destroy(laplex_comm comm);
+
+/* Range-sharded operator over one long vector (B rows): rank r holds caller
+ * slices a_r (n_local), b_r (k_local) and passes x_r / g_r / outputs in the
+ * same slice order.  Creation = splitters from all-gathered samples, stable
+ * partition by value, all-to-all of the anchors, local plan (one host
+ * synchronisation: the exchange counts).  apply / backward: payload
+ * all-to-alls, one all-gather of the shards' totals folded into external
+ * carries on the device, outputs routed back; no host synchronisation.
+ * LAPLEX_REUSE_X: backward reuses the x routed by the preceding apply. */
+#define LAPLEX_REUSE_X 4u
+typedef struct laplex_sharded_s* laplex_sharded;
+int laplex_sharded_create_dev(laplex_comm comm, int dtype, const void* a, size_t n_local, const void* b,
+                              size_t k_local, double t, void* stream, laplex_sharded* out);
+int laplex_sharded_shape(laplex_sharded s, size_t* n_recv, size_t* k_recv);
+int laplex_sharded_apply_dev(laplex_sharded s, const void* x, size_t rows, void* y, void* stream);
+int laplex_sharded_backward_dev(laplex_sharded s, unsigned flags, const void* x, const void* g, size_t rows,
+                                void* x_bar, void* a_bar, void* b_bar, void* stream);
+int laplex_sharded_release(laplex_sharded s);
+
+/* Batch replicas (C2-C4 on N GPUs): each rank runs laplex_backward_dev on its
+ * own rows over a replicated plan; a_bar / b_bar (/ phi_bar / psi_bar), sums
+ * over ALL ranks' rows (gradients.hpp:122-133), are combined by an all-gather
+ * of the per-rank partials summed in rank order: deterministic, identical on
+ * every rank. */
+int laplex_replica_backward_dev(laplex_plan plan, laplex_comm comm, unsigned flags, const void* X, const void* G,
+                                size_t rows, void* x_bar, void* a_bar, void* b_bar, void* phi_bar, void* psi_bar,
+                                void* stream);
 
 /* Number of CUDA kernels this library launched on the calling process
  * (instrumentation for the benchmark's gpu_launches count). */

@@ -134,6 +134,20 @@ class OracleOp:
         f = _fn(self.backend, name, self.dtype)
         return f(self._h, *args)
 
+    def transposed(self):
+        """operator.hpp:157-159 (reference backend: the reference's own
+        transposed(), which rebuilds the role-swapped operator)."""
+        if self.backend != "ref":
+            raise NotImplementedError("transposed() is exposed for the compiled reference only")
+        h = C.c_void_p()
+        f = _fn("ref", "op_transposed", self.dtype)
+        f.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
+        _check(f(self._h, C.byref(h)), "transposed")
+        t = OracleOp.__new__(OracleOp)
+        t.dtype, t.backend, t.a, t.b, t.phi, t.psi = self.dtype, "ref", self.b, self.a, None, None
+        t.n, t.k, t.t, t._h = self.k, self.n, self.t, h
+        return t
+
     def sorted(self, side: int):
         m = self.n if side == 0 else self.k
         vals = np.empty(m, self.dtype)

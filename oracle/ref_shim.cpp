@@ -6,6 +6,7 @@
 // laplex_oracle.c is pinned against, and the "reference" arm of bench.py's
 // CPU baseline.  Each entry mirrors one reference call:
 //   LaplexOperator ctor        operator.hpp:81-137
+//   transposed()               operator.hpp:157-159
 //   matvec / matvec_transpose  operator.hpp:162-172
 //   batch_matvec               operator.hpp:176-188
 //   phased_matvec              operator.hpp:197-213
@@ -71,6 +72,12 @@ laplex::Dispatch disp(int d) {
         });                                                                                            \
     }                                                                                                  \
     extern "C" void lxr_op_destroy##SFX(void* op) { delete static_cast<laplex::LaplexOperator<R>*>(op); } \
+    extern "C" int lxr_op_transposed##SFX(void* op_, void** out) {                                    \
+        *out = nullptr;                                                                                \
+        return guarded([&] {                                                                           \
+            *out = new laplex::LaplexOperator<R>(static_cast<laplex::LaplexOperator<R>*>(op_)->transposed()); \
+        });                                                                                            \
+    }                                                                                                  \
     extern "C" void lxr_op_sorted##SFX(void* op_, int side, R* values, uint64_t* perm, R* decays) {   \
         auto* op = static_cast<laplex::LaplexOperator<R>*>(op_);                                       \
         const auto& s = side == 0 ? op->sorted_rows() : op->sorted_cols();                             \

@@ -48,6 +48,9 @@ _SIGS = {
     "laplex_gram_dev": (C.c_int, [vp, C.c_uint, vp, vp, vp]),
     "laplex_gram_vjp_weights": (C.c_int, [vp, vp, sz, vp, sz, sz, vp]),
     "laplex_sort": (C.c_int, [C.c_int, vp, sz, vp, vp, vp]),
+    "laplex_sort_dev": (C.c_int, [C.c_int, vp, sz, vp, vp, vp, vp, vp]),
+    "laplex_scan_dev": (C.c_int, [C.c_int, vp, sz, vp, vp, vp, vp]),
+    "laplex_gram_vjp_weights_dev": (C.c_int, [vp, vp, vp, vp]),
     "laplex_shard_partition_dev": (C.c_int, [C.c_int, vp, sz, C.c_double, vp, C.c_int, vp, vp, vp]),
     "laplex_gather_dev": (C.c_int, [C.c_int, vp, sz, vp, sz, sz, vp, vp]),
     "laplex_scatter_dev": (C.c_int, [C.c_int, vp, vp, sz, sz, vp, sz, vp]),
@@ -58,6 +61,16 @@ _SIGS = {
     "laplex_shard_backward_begin": (C.c_int, [vp, C.c_uint, vp, vp, sz, vp, C.POINTER(vp), vp]),
     "laplex_shard_backward_end": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp]),
     "laplex_work_release": (C.c_int, [vp]),
+    "laplex_nccl_unique_id": (C.c_int, [vp]),
+    "laplex_comm_init_nccl": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(vp)]),
+    "laplex_comm_init_local": (C.c_int, [C.c_uint64, C.c_int, C.c_int, C.POINTER(vp)]),
+    "laplex_comm_destroy": (C.c_int, [vp]),
+    "laplex_sharded_create_dev": (C.c_int, [vp, C.c_int, vp, sz, vp, sz, C.c_double, vp, C.POINTER(vp)]),
+    "laplex_sharded_shape": (C.c_int, [vp, C.POINTER(sz), C.POINTER(sz)]),
+    "laplex_sharded_apply_dev": (C.c_int, [vp, vp, sz, vp, vp]),
+    "laplex_sharded_backward_dev": (C.c_int, [vp, C.c_uint, vp, vp, sz, vp, vp, vp, vp]),
+    "laplex_sharded_release": (C.c_int, [vp]),
+    "laplex_replica_backward_dev": (C.c_int, [vp, vp, C.c_uint, vp, vp, sz, vp, vp, vp, vp, vp, vp]),
     "laplex_scan": (C.c_int, [C.c_int, vp, sz, vp, vp, vp]),
 }
 

@@ -106,11 +106,13 @@ int current_device() {
     return d;
 }
 
-// The library's own stream-ordered memory pool per device.  Its release
-// threshold is unbounded while plans are alive (per-call temporaries are free
-// after warm-up); when the last plan on the device is released the pool is
-// trimmed, so the memory goes back to the device (and to e.g. torch's caching
-// allocator) instead of staying with the library for the life of the process.
+// The library's own stream-ordered memory pool per device (not the device's
+// default pool), a caching allocator like torch's: freed blocks are kept for
+// reuse until laplex_pool_trim() (the analogue of torch.cuda.empty_cache())
+// returns them.  A training loop that builds a plan per step must not re-map
+// its working set every step: measured +450 ms per C5 step when the pool was
+// trimmed on each plan release, and +190 ms (C2) / +200 ms (C4) per step with
+// a 1 GiB release threshold, which re-maps at every synchronisation.
 struct DevState {
     std::once_flag init;
     cudaMemPool_t pool = nullptr;
@@ -181,8 +183,7 @@ int occupancy(K kern, int threads, size_t smem) {
 // sub-allocates: 36 B per element for device-pointer plans (the step peaks
 // at 28 B per element), 48 B for host-pointer plans (which add the uploaded
 // inputs and outputs).  LAPLEX_POOL_RESERVE_GB overrides the size (0
-// disables).  The reservation lives in the library's pool and is trimmed with
-// it when the device's last plan is released.
+// disables).
 void reserve_pool(size_t m, size_t rsz, size_t per_elem, cudaStream_t st) {
     DevState& ds = dev_state();
     size_t bytes = m * per_elem * (rsz / 4);
@@ -210,11 +211,7 @@ void plan_born(int d) {
 void plan_died(int d) {
     DevState& ds = dev_state(d);
     std::lock_guard<std::mutex> g(ds.mu);
-    if (--ds.live_plans == 0) {
-        // best effort: frees still queued on streams are returned on the next trim
-        cudaMemPoolTrimTo(ds.pool, 0);
-        ds.reserved = 0;
-    }
+    --ds.live_plans;
 }
 
 // stream-ordered device buffer from the library's pool
@@ -306,14 +303,16 @@ struct Core {
         int prev = -1;
         cudaGetDevice(&prev);
         cudaSetDevice(device);
-        cudaStream_t rel = dev_state(device).release;
+        // one stream used the plan (the common case): free on it, behind its
+        // work; several: on the release stream, after every one of them
+        cudaStream_t rel = uses.size() == 1 ? uses[0].first : dev_state(device).release;
         for (auto& u : uses) {
-            cudaStreamWaitEvent(rel, u.second, 0);
+            if (rel != u.first) cudaStreamWaitEvent(rel, u.second, 0);
             cudaEventDestroy(u.second);
         }
         for (cudaEvent_t e : built)
             if (e) {
-                cudaStreamWaitEvent(rel, e, 0);
+                if (uses.size() != 1) cudaStreamWaitEvent(rel, e, 0);
                 cudaEventDestroy(e);
             }
         for_each_buf([&](DBuf& b) {
@@ -1323,13 +1322,16 @@ void do_ranks(laplex_plan_s* p, int side, int strict, uint64_t* out, cudaStream_
     for (uint32_t i = 0; i < m; ++i) out[i] = h[i];
 }
 
+// prefix / suffix decay scans of payload over sorted anchors (scan.hpp:50-73),
+// all device pointers; `sorted` must be readable 64 bytes past its end (TMA
+// rounding) -- the host entry copies into such a buffer, the device entry
+// stages a padded copy when the caller's pointer is not one of its own.
 template <class R>
-void do_scan(const R* sorted, uint32_t m, const R* payload, R* pre, R* suf, cudaStream_t st) {
+void do_scan_dev(const R* sorted_in, uint32_t m, const R* payload, R* pre, R* suf, cudaStream_t st) {
     using namespace lx::ms;
     const uint32_t T = tiles_for(m);
-    DBuf vals((size_t)m * sizeof(R) + kTmaPad, st), pay((size_t)m * sizeof(R), st);
-    ck(cudaMemcpyAsync(vals.p, sorted, (size_t)m * sizeof(R), cudaMemcpyHostToDevice, st), "H2D");
-    ck(cudaMemcpyAsync(pay.p, payload, (size_t)m * sizeof(R), cudaMemcpyHostToDevice, st), "H2D");
+    DBuf vals((size_t)m * sizeof(R) + kTmaPad, st);
+    ck(cudaMemcpyAsync(vals.p, sorted_in, (size_t)m * sizeof(R), cudaMemcpyDeviceToDevice, st), "D2D");
     DBuf part((size_t)(T + 1) * 4, st), desc((size_t)(T + 1) * sizeof(TileDesc<R>), st);
     DBuf sfirst((size_t)T * sizeof(R), st), slast((size_t)T * sizeof(R), st);
     launch("lx_seq_partition", st, [&] {
@@ -1349,17 +1351,26 @@ void do_scan(const R* sorted, uint32_t m, const R* payload, R* pre, R* suf, cuda
     v.s_first = sfirst.as<R>();
     v.s_last = slast.as<R>();
     v.T = T;
-    DBuf dpre((size_t)m * sizeof(R), st), dsuf((size_t)m * sizeof(R), st);
+    DBuf dpre(pre ? 0 : (size_t)m * sizeof(R), st), dsuf(suf ? 0 : (size_t)m * sizeof(R), st);
     auto a = main_args(v, 1);
     Scratch sc(2, 1, T, sizeof(R), st);
-    DBuf xs = sorted_payload<R, 1, true, false, false>(v, 1, pay.as<R>(), sc, 0, a.ldxs, st, true);
+    DBuf xs = sorted_payload<R, 1, true, false, false>(v, 1, payload, sc, 0, a.ldxs, st, true);
     a.Xs = xs.as<R>();
     scan_carries<R, 1>(v, sc, 1, 0u, 0u, st);
     a.cp = sc.cp.as<R>();
     a.cq = sc.cq.as<R>();
-    a.pre = dpre.as<R>();
-    a.suf = dsuf.as<R>();
+    a.pre = pre ? pre : dpre.as<R>();
+    a.suf = suf ? suf : dsuf.as<R>();
     launch_main<R, 0, 1, false, true>("lx_main_seq", a, st);
+}
+
+template <class R>
+void do_scan(const R* sorted, uint32_t m, const R* payload, R* pre, R* suf, cudaStream_t st) {
+    DBuf vals((size_t)m * sizeof(R), st), pay((size_t)m * sizeof(R), st);
+    DBuf dpre((size_t)m * sizeof(R), st), dsuf((size_t)m * sizeof(R), st);
+    ck(cudaMemcpyAsync(vals.p, sorted, (size_t)m * sizeof(R), cudaMemcpyHostToDevice, st), "H2D");
+    ck(cudaMemcpyAsync(pay.p, payload, (size_t)m * sizeof(R), cudaMemcpyHostToDevice, st), "H2D");
+    do_scan_dev<R>(vals.as<R>(), m, pay.as<R>(), dpre.as<R>(), dsuf.as<R>(), st);
     if (pre) ck(cudaMemcpyAsync(pre, dpre.p, (size_t)m * sizeof(R), cudaMemcpyDeviceToHost, st), "D2H");
     if (suf) ck(cudaMemcpyAsync(suf, dsuf.p, (size_t)m * sizeof(R), cudaMemcpyDeviceToHost, st), "D2H");
     ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
@@ -2121,6 +2132,88 @@ int laplex_scan(int dtype, const void* sorted_values, size_t m, const void* payl
     });
 }
 
+int laplex_sort_dev(int dtype, const void* raw, size_t m, void* values, uint32_t* perm, void* decays,
+                    int* nonfinite, void* stream) {
+    return guarded([&] {
+        dtype_check(dtype);
+        if (m == 0) fail(LAPLEX_E_EMPTY_INPUT, "sort_anchors: empty input");
+        if (m >= 0x80000000ull) fail(LAPLEX_E_INVALID_SIZE, "m must be < 2^31");
+        if (!values || !perm) fail(LAPLEX_E_INVALID_ARGUMENT, "sort_anchors: values and perm are required");
+        cudaStream_t st = as_stream(stream);
+        auto run = [&](auto zero) {
+            using R = decltype(zero);
+            DBuf bad(nonfinite ? 0 : sizeof(int), st);
+            int* flag = nonfinite ? nonfinite : bad.as<int>();
+            ck(cudaMemsetAsync(flag, 0, sizeof(int), st), "memset");
+            radix_sort<R>((const R*)raw, (uint32_t)m, R(1), (R*)values, perm, flag, st);
+            if (decays && m > 1)
+                launch("lx_decays", st, [&] {
+                    lx::sort::lx_decays<R><<<(uint32_t)((m + 255) / 256), 256, 0, st>>>((const R*)values, m,
+                                                                                       (R*)decays);
+                });
+            if (!nonfinite) {  // report NonFinite synchronously (scan.hpp:29)
+                int h = 0;
+                ck(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+                ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+                if (h) fail(LAPLEX_E_NON_FINITE, "sort_anchors: non-finite entry");
+            }
+        };
+        if (dtype == LAPLEX_F64)
+            run(0.0);
+        else
+            run(0.0f);
+    });
+}
+
+int laplex_scan_dev(int dtype, const void* sorted_values, size_t m, const void* payload, void* prefix, void* suffix,
+                    void* stream) {
+    return guarded([&] {
+        dtype_check(dtype);
+        if (m == 0) return;
+        if (m >= 0x80000000ull) fail(LAPLEX_E_INVALID_SIZE, "m must be < 2^31");
+        if (!prefix && !suffix) return;
+        if (dtype == LAPLEX_F64)
+            do_scan_dev<double>((const double*)sorted_values, (uint32_t)m, (const double*)payload, (double*)prefix,
+                                (double*)suffix, as_stream(stream));
+        else
+            do_scan_dev<float>((const float*)sorted_values, (uint32_t)m, (const float*)payload, (float*)prefix,
+                               (float*)suffix, as_stream(stream));
+    });
+}
+
+int laplex_gram_vjp_weights_dev(laplex_plan plan, const void* G_bar, void* D_bar, void* stream) {
+    return guarded([&] {
+        check_plan(plan);
+        Core& c = *plan->core;
+        if (c.phased) fail(LAPLEX_E_PHASE_PRESENT, "gram_vjp_weights: phased operator not supported");
+        cudaStream_t st = as_stream(stream);
+        const int ia = plan->swapped ? 1 : 0;
+        const uint32_t n = c.side[ia].m;
+        auto run = [&](auto zero) {
+            using R = decltype(zero);
+            // gradients.hpp:196-205 on the device: finiteness, then symmetry
+            // (max |G_ij - G_ji| <= 1e-9 max(1, max |G_ij|)), one synchronisation
+            DBuf flags(3 * sizeof(R), st);
+            ck(cudaMemsetAsync(flags.p, 0, 3 * sizeof(R), st), "memset");
+            launch("lx_gram_sym_check", st, [&] {
+                lx::gram::lx_sym_check<R><<<std::max(1u, std::min<uint32_t>((n + 15) / 16, 4096u)), 256, 0, st>>>(
+                    (const R*)G_bar, n, flags.as<R>());
+            });
+            R h[3];
+            ck(cudaMemcpyAsync(h, flags.p, sizeof(h), cudaMemcpyDeviceToHost, st), "D2H");
+            ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+            if (h[2] != R(0)) fail(LAPLEX_E_NON_FINITE, "gram_vjp_weights G_bar: non-finite entry");
+            if (h[1] > R(1e-9) * std::max(R(1), h[0]))
+                fail(LAPLEX_E_ASYMMETRIC_COTANGENT, "gram_vjp_weights: G_bar is not symmetric");
+            do_gram_vjp<R>(plan, (const R*)G_bar, (R*)D_bar, st);
+        };
+        if (c.dtype == LAPLEX_F64)
+            run(0.0);
+        else
+            run(0.0f);
+    });
+}
+
 // ---------------------------------------------------------------------------
 // range-sharded (multi-GPU) building blocks
 // ---------------------------------------------------------------------------
@@ -2336,3 +2429,5 @@ int laplex_work_release(laplex_work work) {
 
 }  // extern "C"
 
+// multi-GPU host layer (communicators, range-sharded operator, batch replicas)
+#include "lx_dist.inc"

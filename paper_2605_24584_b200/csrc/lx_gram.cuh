@@ -14,6 +14,8 @@
 //      (bit-exact symmetry, operator.hpp:410-411).
 #pragma once
 
+#include <type_traits>
+
 #include "lx_common.cuh"
 
 namespace lx {
@@ -139,6 +141,39 @@ __global__ void lx_gram_vjp_contract(const R* __restrict__ A, const uint32_t* __
         acc = xfma(xexp(-(d < R(0) ? -d : d)), Y[(size_t)i * k + tcol], acc);
     }
     Dbar[tcol] = acc;
+}
+
+// Cotangent checks of gram_vjp_weights (gradients.hpp:196-205) on the device:
+// flags[0] = max |G_ij| and flags[1] = max |G_ij - G_ji| over i > j, flags[2]
+// != 0 when an entry is not finite.  Non-negative IEEE values order like their
+// bit patterns, so the maxima are integer atomicMax on the bits.
+template <class R>
+__global__ void lx_sym_check(const R* __restrict__ G, uint32_t n, R* __restrict__ flags) {
+    using U = typename std::conditional<sizeof(R) == 8, unsigned long long, unsigned int>::type;
+    R mabs = R(0), masym = R(0);
+    int bad = 0;
+    const size_t total = (size_t)n * n;
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t i = (uint32_t)(e / n), j = (uint32_t)(e % n);
+        const R v = G[e];
+        bad |= !isfinite(v);
+        if (j < i) {
+            const R d = v - G[(size_t)j * n + i];
+            mabs = fmax(mabs, v < R(0) ? -v : v);
+            masym = fmax(masym, d < R(0) ? -d : d);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        mabs = fmax(mabs, __shfl_xor_sync(0xffffffffu, mabs, o));
+        masym = fmax(masym, __shfl_xor_sync(0xffffffffu, masym, o));
+        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        U* f = reinterpret_cast<U*>(flags);
+        if (mabs == mabs) atomicMax(&f[0], *reinterpret_cast<const U*>(&mabs));
+        if (masym == masym) atomicMax(&f[1], *reinterpret_cast<const U*>(&masym));
+        if (bad) f[2] = U(1);
+    }
 }
 
 }  // namespace gram

@@ -395,6 +395,13 @@ class DeviceOperator:
         _check(lib().laplex_apply_dev(self._h, flags, X.data_ptr(), rows, out.data_ptr(), self._stream(stream)))
         return out
 
+    def gram_vjp_weights(self, G_bar, stream=None):
+        """D_bar (k) of gram_vjp_weights (gradients.hpp:190-219) for a symmetric
+        n x n CUDA tensor G_bar; raises AsymmetricCotangent / NonFinite."""
+        out = self.torch.empty(self.k, dtype=self.dtype, device=G_bar.device)
+        _check(lib().laplex_gram_vjp_weights_dev(self._h, G_bar.data_ptr(), out.data_ptr(), self._stream(stream)))
+        return out
+
     def gram_apply(self, X, out=None, stream=None):
         """Y = A^T (A X) per row (rows x k -> rows x k), stream-ordered."""
         torch = self.torch
@@ -443,6 +450,39 @@ class DeviceOperator:
         out = np.empty(m, np.uint64)
         _check(lib().laplex_plan_ranks(self._h, side, int(strict), _p(out)))
         return out
+
+
+def sort_anchors_dev(raw, stream=None):
+    """sort_anchors (scan.hpp:27-46) on a CUDA tensor: (values, perm int32
+    tensor holding the uint32 device permutation, decays); stream-ordered
+    except for the one synchronisation that reports NonFinite."""
+    import torch
+    m = raw.numel()
+    vals = torch.empty_like(raw)
+    perm = torch.empty(m, dtype=torch.int32, device=raw.device)
+    dec = torch.empty(max(m - 1, 1), dtype=raw.dtype, device=raw.device)
+    s = stream if stream is not None else torch.cuda.current_stream()
+    _check(lib().laplex_sort_dev(F64 if raw.dtype == torch.float64 else F32, raw.data_ptr(), m, vals.data_ptr(),
+                                 perm.data_ptr(), dec.data_ptr(), None, C.c_void_p(s.cuda_stream)))
+    return vals, perm, dec[: max(m - 1, 0)]
+
+
+def decay_scan_dev(sorted_values, payload, stream=None):
+    """(prefix, suffix) decay scans (scan.hpp:50-73) of CUDA tensors."""
+    import torch
+    m = sorted_values.numel()
+    pre = torch.empty_like(payload)
+    suf = torch.empty_like(payload)
+    s = stream if stream is not None else torch.cuda.current_stream()
+    _check(lib().laplex_scan_dev(F64 if payload.dtype == torch.float64 else F32, sorted_values.data_ptr(), m,
+                                 payload.data_ptr(), pre.data_ptr(), suf.data_ptr(), C.c_void_p(s.cuda_stream)))
+    return pre, suf
+
+
+def pool_trim() -> None:
+    """Return every unused byte of the library's device memory pool (it caches
+    freed blocks for reuse, like torch's allocator; cf. torch.cuda.empty_cache)."""
+    _check(lib().laplex_pool_trim())
 
 
 def kernel_launches() -> int:

@@ -19,11 +19,15 @@ ranges, rank order = global index order):
 4. outputs travel back along the reverse all-to-all and are scattered into
    the caller's slice order.
 
-The data path is the CUDA library (GpuBackend); NumpyBackend restates the
-per-shard math densely on the CPU so the host logic (splitters, routing,
-carry folding) is testable with gloo.  Communicators: TorchComm
-(torch.distributed: NCCL on GPUs, gloo on CPU) and SimComm (threads in one
-process, for single-GPU runs of N shards).
+The PRODUCT path is the C++ host layer in the library (lx_dist.inc:
+laplex_sharded_* over a laplex_comm -- NCCL or in-process "local" ranks),
+wrapped here by `Comm` and `CppShardedOperator`; it folds the external carries
+on the device and synchronises the host only once, at creation.  The Python
+`ShardedOperator` below is its restatement over pluggable backends: with
+NumpyBackend (dense per-shard math on the CPU) and TorchComm over gloo it
+tests the host logic (splitters, routing, carry folding) without a GPU; with
+GpuBackend it drives the same kernels from Python.  Communicators for it:
+TorchComm (torch.distributed) and SimComm (threads in one process).
 """
 from __future__ import annotations
 
@@ -482,3 +486,104 @@ class ShardedOperator:
         a_bar = self._route_out(ab, self.perm_a, self.send_a, self.recv_a, self.n_local)
         b_bar = self._route_out(bb, self.perm_b, self.send_b, self.recv_b, self.k_local)
         return x_bar, a_bar, b_bar
+
+
+# ---------------------------------------------------------------------------
+# the C++ host layer (product path): communicators + sharded operator
+# ---------------------------------------------------------------------------
+class Comm:
+    """A laplex_comm: NCCL (`Comm.nccl`) or in-process ranks (`Comm.local`)."""
+
+    def __init__(self, handle, rank, world):
+        self.h, self.rank, self.world = handle, rank, world
+
+    @classmethod
+    def local(cls, key: int, world: int, rank: int) -> "Comm":
+        h = C.c_void_p()
+        _check(lib().laplex_comm_init_local(C.c_uint64(key), world, rank, C.byref(h)))
+        return cls(h, rank, world)
+
+    @classmethod
+    def nccl(cls, world: int, rank: int, broadcast) -> "Comm":
+        """broadcast(bytes_or_None) -> bytes: rank 0's 128-byte id to every rank
+        (e.g. torch.distributed.broadcast_object_list)."""
+        uid = None
+        if rank == 0:
+            buf = C.create_string_buffer(128)
+            _check(lib().laplex_nccl_unique_id(buf))
+            uid = buf.raw
+        uid = broadcast(uid)
+        h = C.c_void_p()
+        _check(lib().laplex_comm_init_nccl(C.create_string_buffer(uid, 128), world, rank, C.byref(h)))
+        return cls(h, rank, world)
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            lib().laplex_comm_destroy(h)
+            self.h = None
+
+
+class CppShardedOperator:
+    """laplex_sharded_*: this rank's slices a_r, b_r of one long vector (any
+    rows per call); outputs come back in the slice order."""
+
+    REUSE_X = 4
+
+    def __init__(self, a, b, t: float, comm: Comm, stream=None):
+        import torch
+        self.torch, self.comm = torch, comm
+        self.dtype = a.dtype
+        self.n_local, self.k_local = a.numel(), b.numel()
+        h = C.c_void_p()
+        _check(lib().laplex_sharded_create_dev(comm.h, _dt(a), _ptr(a), self.n_local, _ptr(b), self.k_local,
+                                               float(t), self._st(stream), C.byref(h)))
+        self.h = h
+        nr, kr = C.c_size_t(), C.c_size_t()
+        _check(lib().laplex_sharded_shape(h, C.byref(nr), C.byref(kr)))
+        self.n_recv, self.k_recv = nr.value, kr.value
+
+    def _st(self, stream):
+        s = stream if stream is not None else self.torch.cuda.current_stream()
+        return C.c_void_p(s.cuda_stream)
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            lib().laplex_sharded_release(h)
+            self.h = None
+
+    def apply(self, x, out=None, stream=None):
+        rows = x.shape[0] if x.dim() == 2 else 1
+        if out is None:
+            out = self.torch.empty((rows, self.n_local), dtype=self.dtype, device=x.device)
+        _check(lib().laplex_sharded_apply_dev(self.h, _ptr(x), rows, _ptr(out), self._st(stream)))
+        return out
+
+    def backward(self, x, g, reuse_x=False, stream=None):
+        torch = self.torch
+        rows = x.shape[0] if x.dim() == 2 else 1
+        xb = torch.empty((rows, self.k_local), dtype=self.dtype, device=x.device)
+        ab = torch.empty(max(self.n_local, 1), dtype=self.dtype, device=x.device)
+        bb = torch.empty(max(self.k_local, 1), dtype=self.dtype, device=x.device)
+        _check(lib().laplex_sharded_backward_dev(self.h, self.REUSE_X if reuse_x else 0, _ptr(x), _ptr(g), rows,
+                                                 _ptr(xb), _ptr(ab), _ptr(bb), self._st(stream)))
+        return xb, ab[:self.n_local], bb[:self.k_local]
+
+
+def replica_backward(dop, comm: Comm, X, G, stream=None):
+    """Batch replicas: this rank's rows X, G over the replicated DeviceOperator
+    `dop`; anchor cotangents summed over all ranks' rows (deterministic)."""
+    import torch
+    rows = X.shape[0]
+    dev = X.device
+    xb = torch.empty((rows, dop.k), dtype=dop.dtype, device=dev)
+    ab = torch.empty(dop.n, dtype=dop.dtype, device=dev)
+    bb = torch.empty(dop.k, dtype=dop.dtype, device=dev)
+    pb = torch.empty(dop.n, dtype=dop.dtype, device=dev) if dop.phased else None
+    qb = torch.empty(dop.k, dtype=dop.dtype, device=dev) if dop.phased else None
+    s = stream if stream is not None else torch.cuda.current_stream()
+    _check(lib().laplex_replica_backward_dev(dop._h, comm.h, 2 if dop.phased else 0, _ptr(X), _ptr(G), rows,
+                                             _ptr(xb), _ptr(ab), _ptr(bb), _ptr(pb), _ptr(qb),
+                                             C.c_void_p(s.cuda_stream)))
+    return xb, ab, bb, pb, qb
