@@ -414,12 +414,13 @@ def make_step(L, torch, c, t):
         if kind == "gram":
             op.gram_apply(t["X"], out=o["Y"])
             return op
-        op.apply(t["X"], out=o["Y"])
+        # a training step: the forward saves its sorted x for the backward (LAPLEX_SAVE_X / REUSE_X)
+        op.apply(t["X"], out=o["Y"], save_x=kind != "fwd")
         if kind == "fwdbwd":
-            op.backward(t["X"], t["G"], x_bar=o["xb"], a_bar=o["ab"], b_bar=o["bb"])
+            op.backward(t["X"], t["G"], x_bar=o["xb"], a_bar=o["ab"], b_bar=o["bb"], reuse_x=True)
         elif kind == "phased":
             op.backward(t["X"], t["G"], x_bar=o["xb"], a_bar=o["ab"], b_bar=o["bb"], phi_bar=o["pb"],
-                        psi_bar=o["qb"])
+                        psi_bar=o["qb"], reuse_x=True)
         return op
     return step, o
 

@@ -57,6 +57,14 @@ extern "C" {
 /* apply / backward / gram flags */
 #define LAPLEX_TRANSPOSE 1u /* apply: y = A^T g (matvec_transpose) */
 #define LAPLEX_PHASED 2u    /* phased_matvec / phased_matvec_vjp / phased_gram */
+/* laplex_apply_dev: keep the forward's sorted x (and its tile aggregates) in
+ * the plan for the backward -- the autograd "save for backward" of x; one x
+ * per plan, replaced by the next save, released when consumed. */
+#define LAPLEX_SAVE_X 8u
+/* laplex_backward_dev / laplex_sharded_backward_dev: reuse the x saved by the
+ * preceding forward (same X pointer, rows and orientation; the caller asserts X
+ * is unchanged) instead of gathering it again.  Results are bitwise identical. */
+#define LAPLEX_REUSE_X 4u
 
 /* error codes (reference exception types) */
 #define LAPLEX_OK 0
@@ -217,7 +225,6 @@ int laplex_comm_destroy(laplex_comm comm);
  * all-to-alls, one all-gather of the shards' totals folded into external
  * carries on the device, outputs routed back; no host synchronisation.
  * LAPLEX_REUSE_X: backward reuses the x routed by the preceding apply. */
-#define LAPLEX_REUSE_X 4u
 typedef struct laplex_sharded_s* laplex_sharded;
 int laplex_sharded_create_dev(laplex_comm comm, int dtype, const void* a, size_t n_local, const void* b,
                               size_t k_local, double t, void* stream, laplex_sharded* out);

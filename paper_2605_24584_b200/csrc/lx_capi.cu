@@ -285,6 +285,18 @@ struct Core {
     DBuf ranks[4];  // [side*2 + strict]
     bool has_ranks[4] = {false, false, false, false};
     cudaEvent_t built[2] = {nullptr, nullptr};  // [0]: plan created; [1]: role-swapped data (lazy)
+    // x of the last forward kept for its backward (LAPLEX_SAVE_X / LAPLEX_REUSE_X):
+    // the sorted payload and its tile aggregates (inclusive + strict), i.e.
+    // exactly what the backward's x gather would recompute
+    struct SavedX {
+        const void* X = nullptr;
+        size_t rows = 0;
+        bool swapped = false, phased = false;
+        DBuf xs, aggp, aggq;
+        size_t ldxs = 0, agg_count = 0;
+        cudaEvent_t ready = nullptr;
+    } saved;
+    std::mutex saved_mu;
     int bad_host[4] = {0, 0, 0, 0};
     // Streams that used the plan, each with an event after its last use.  The
     // buffers are freed on the device's release stream once it has waited
@@ -298,6 +310,7 @@ struct Core {
         for (int o = 0; o < 2; ++o)
             for (DBuf* b : {&part[o], &desc[o], &sfirst[o], &slast[o], &gmap[o][0], &gmap[o][1]}) f(*b);
         for (DBuf& b : ranks) f(b);
+        f(saved.xs), f(saved.aggp), f(saved.aggq);
     }
     ~Core() {
         int prev = -1;
@@ -310,7 +323,7 @@ struct Core {
             if (rel != u.first) cudaStreamWaitEvent(rel, u.second, 0);
             cudaEventDestroy(u.second);
         }
-        for (cudaEvent_t e : built)
+        for (cudaEvent_t e : {built[0], built[1], saved.ready})
             if (e) {
                 if (uses.size() != 1) cudaStreamWaitEvent(rel, e, 0);
                 cudaEventDestroy(e);
@@ -548,7 +561,7 @@ void build_splan(Side& sd, cudaStream_t st) {
     const uint32_t m = sd.m;
     const int shift = bucket_shift(m);
     const uint32_t tiles = (m + kTile - 1) / kTile;
-    sd.spos = DBuf((size_t)m * 4, st);
+    sd.spos = DBuf((size_t)m * 4 + 16, st);  // + slack: the main kernel TMA-reads it in 16-byte units
     sd.sdst = DBuf((size_t)m * 4, st);
     DBuf look(kSortRts ? 8 : (size_t)tiles * kRadix * 8, st), ctr(4, st);
     DBuf cnt(kSortRts ? (size_t)tiles * kRadix * 4 : 4, st);
@@ -956,11 +969,13 @@ struct FwdWork : WorkBase {
     FwdWork(const View<R>& v_, int rows_, cudaStream_t st) : v(v_), sc(2 * NX, rows_, v_.T, sizeof(R), st), rows(rows_) {}
 };
 
-template <class R, int NX>
+// STRICT: also the strict aggregates of x (unused by the forward; computed when
+// the sorted x is kept for the backward, whose x channel needs them)
+template <class R, int NX, bool STRICT = false>
 std::unique_ptr<FwdWork<R, NX>> fwd_begin(const View<R>& v, const R* X, int rows, cudaStream_t st) {
     auto w = std::make_unique<FwdWork<R, NX>>(v, rows, st);
     w->a = main_args(v, rows);
-    w->xs = sorted_payload<R, NX, false, false, false>(v, rows, X, w->sc, 0, w->a.ldxs, st);
+    w->xs = sorted_payload<R, NX, false, false, STRICT>(v, rows, X, w->sc, 0, w->a.ldxs, st);
     w->a.Xs = w->xs.template as<R>();
     scan_carries<R, NX>(v, w->sc, rows, 0u, 0u, st);
     w->a.cp = w->sc.cp.template as<R>();
@@ -970,7 +985,7 @@ std::unique_ptr<FwdWork<R, NX>> fwd_begin(const View<R>& v, const R* X, int rows
 }
 
 template <class R, int NX>
-void fwd_end(FwdWork<R, NX>& w, const R* ext, R* Y, cudaStream_t st) {
+void fwd_end(FwdWork<R, NX>& w, const R* ext, R* Y, cudaStream_t st, bool keep_xs = false) {
     const View<R>& v = w.v;
     auto& a = w.a;
     a.ext = ext;
@@ -984,7 +999,7 @@ void fwd_end(FwdWork<R, NX>& w, const R* ext, R* Y, cudaStream_t st) {
     }
     a.ldy = v.n;
     if (v.n) launch_main<R, 0, NX, false>(NX == 2 ? "lx_main_fwd_phased" : "lx_main_fwd", a, st);
-    w.xs.release();
+    if (!keep_xs) w.xs.release();
     if (v.dst_a)
         stage_scatter<R>(v.dst_a, v.n, yst.as<R>(), Y, v.n, w.rows, nullptr, nullptr, nullptr, nullptr, st);
 }
@@ -999,9 +1014,28 @@ struct laplex_work_s {
 namespace {
 
 template <class R, int NX>
-void apply_fwd(const View<R>& v, const R* X, int rows, R* Y, cudaStream_t st) {
-    auto w = fwd_begin<R, NX>(v, X, rows, st);
-    fwd_end<R, NX>(*w, nullptr, Y, st);
+void apply_fwd(const View<R>& v, const R* X, int rows, R* Y, cudaStream_t st, Core* save = nullptr,
+               bool swapped = false) {
+    if (!save) {
+        auto w = fwd_begin<R, NX>(v, X, rows, st);
+        fwd_end<R, NX>(*w, nullptr, Y, st);
+        return;
+    }
+    auto w = fwd_begin<R, NX, true>(v, X, rows, st);
+    fwd_end<R, NX>(*w, nullptr, Y, st, true);
+    std::lock_guard<std::mutex> g(save->saved_mu);
+    auto& sv = save->saved;
+    sv.X = X;
+    sv.rows = (size_t)rows;
+    sv.swapped = swapped;
+    sv.phased = NX == 2;
+    sv.xs = std::move(w->xs);
+    sv.ldxs = w->a.ldxs;
+    sv.aggp = std::move(w->sc.aggp);
+    sv.aggq = std::move(w->sc.aggq);
+    sv.agg_count = (size_t)2 * NX * rows * v.T;
+    if (!sv.ready) ck(cudaEventCreateWithFlags(&sv.ready, cudaEventDisableTiming), "cudaEventCreate");
+    ck(cudaEventRecord(sv.ready, st), "cudaEventRecord");
 }
 
 template <class R>
@@ -1039,14 +1073,32 @@ struct BwdWork : WorkBase {
         : v(v_), sc(2 * 2 * NCH, rows_, v_.T, sizeof(R), st), rows(rows_) {}
 };
 
+// reuse: the Core whose saved forward x (LAPLEX_REUSE_X) matches X / rows /
+// orientation, or null.  The saved sorted x and aggregates replace the x gather.
 template <class R, int NCH>
 std::unique_ptr<BwdWork<R, NCH>> bwd_begin(const View<R>& v, const R* X, const R* G, int rows, cudaStream_t st,
-                                           const std::function<void()>& before_g = {}) {
+                                           const std::function<void()>& before_g = {}, Core* reuse = nullptr) {
     constexpr int NC = 2 * NCH;
     auto w = std::make_unique<BwdWork<R, NCH>>(v, rows, st);
     auto& a = w->a;
     a = main_args(v, rows);
-    w->xs = sorted_payload<R, NCH, false, false, true>(v, rows, X, w->sc, NCH, a.ldxs, st);
+    if (reuse) {
+        auto& sv = reuse->saved;
+        ck(cudaStreamWaitEvent(st, sv.ready, 0), "cudaStreamWaitEvent");
+        w->xs = std::move(sv.xs);
+        w->xs.st = st;  // read and freed on this stream from now on
+        a.ldxs = sv.ldxs;
+        const size_t off = (size_t)2 * NCH * rows * v.T * sizeof(R);  // x channels follow the g channels
+        ck(cudaMemcpyAsync(w->sc.aggp.template as<char>() + off, sv.aggp.p, sv.agg_count * sizeof(R),
+                           cudaMemcpyDeviceToDevice, st), "D2D");
+        ck(cudaMemcpyAsync(w->sc.aggq.template as<char>() + off, sv.aggq.p, sv.agg_count * sizeof(R),
+                           cudaMemcpyDeviceToDevice, st), "D2D");
+        sv.aggp.st = st, sv.aggq.st = st;
+        sv.aggp.release(), sv.aggq.release();
+        sv.X = nullptr;
+    } else {
+        w->xs = sorted_payload<R, NCH, false, false, true>(v, rows, X, w->sc, NCH, a.ldxs, st);
+    }
     if (before_g) before_g();  // host API: g may still be uploading
     w->gs = sorted_payload<R, NCH, true, true, true>(v, rows, G, w->sc, 0, a.ldgs, st);
     a.Gs = w->gs.template as<R>();
@@ -1104,8 +1156,8 @@ void bwd_end(BwdWork<R, NCH>& w, const R* ext, R* xbar, R* abar, R* bbar, R* phi
 
 template <class R, int NCH>
 void backward_impl(const View<R>& v, const R* X, const R* G, int rows, R* xbar, R* abar, R* bbar, R* phibar,
-                   R* psibar, cudaStream_t st, const std::function<void()>& before_g) {
-    auto w = bwd_begin<R, NCH>(v, X, G, rows, st, before_g);
+                   R* psibar, cudaStream_t st, const std::function<void()>& before_g, Core* reuse = nullptr) {
+    auto w = bwd_begin<R, NCH>(v, X, G, rows, st, before_g, reuse);
     bwd_end<R, NCH>(*w, nullptr, xbar, abar, bbar, phibar, psibar, st);
 }
 
@@ -1119,12 +1171,13 @@ void do_apply(laplex_plan_s* p, unsigned flags, const R* X, size_t rows, R* Y, c
     if (rows == 0) return;
     if (rows > 0x7fffffff) fail(LAPLEX_E_INVALID_SIZE, "too many rows");
     View<R> v = view<R>(c, p->swapped, st);
+    Core* save = (flags & LAPLEX_SAVE_X) && !trn ? &c : nullptr;
     if (trn)
         apply_trn<R>(v, X, (int)rows, Y, st);
     else if (ph)
-        apply_fwd<R, 2>(v, X, (int)rows, Y, st);
+        apply_fwd<R, 2>(v, X, (int)rows, Y, st, save, p->swapped);
     else
-        apply_fwd<R, 1>(v, X, (int)rows, Y, st);
+        apply_fwd<R, 1>(v, X, (int)rows, Y, st, save, p->swapped);
     touch(c, st);
 }
 
@@ -1145,10 +1198,19 @@ void do_backward(laplex_plan_s* p, unsigned flags, const R* X, const R* G, size_
         touch(c, st);
         return;
     }
-    if (ph)
-        backward_impl<R, 2>(v, X, G, (int)rows, xbar, abar, bbar, phibar, psibar, st, before_g);
+    // LAPLEX_REUSE_X: the caller asserts X is unchanged since the apply that
+    // saved it (LAPLEX_SAVE_X); a saved x that does not match is ignored
+    std::unique_lock<std::mutex> lk(c.saved_mu);
+    Core* reuse = nullptr;
+    if ((flags & LAPLEX_REUSE_X) && c.saved.xs.p && c.saved.X == (const void*)X && c.saved.rows == rows &&
+        c.saved.swapped == p->swapped && c.saved.phased == ph)
+        reuse = &c;
     else
-        backward_impl<R, 1>(v, X, G, (int)rows, xbar, abar, bbar, nullptr, nullptr, st, before_g);
+        lk.unlock();
+    if (ph)
+        backward_impl<R, 2>(v, X, G, (int)rows, xbar, abar, bbar, phibar, psibar, st, before_g, reuse);
+    else
+        backward_impl<R, 1>(v, X, G, (int)rows, xbar, abar, bbar, nullptr, nullptr, st, before_g, reuse);
     touch(c, st);
 }
 
@@ -1882,7 +1944,7 @@ int laplex_apply(laplex_plan plan, unsigned flags, const void* X, size_t rows, s
             dl.add(dy.p, Y, out_len, (int)rows);
             {
                 HookScope hs(&dl.hook);
-                do_apply<R>(plan, flags, dx.get(), rows, dy.as<R>(), st);
+                do_apply<R>(plan, flags & ~LAPLEX_SAVE_X, dx.get(), rows, dy.as<R>(), st);
             }
             dl.finish(st);
         };

@@ -29,7 +29,7 @@ from ._lib import lib
 
 F32, F64 = 0, 1
 ROWS, COLS = 0, 1
-TRANSPOSE, PHASED = 1, 2
+TRANSPOSE, PHASED, REUSE_X, SAVE_X = 1, 2, 4, 8
 
 
 class Error(RuntimeError):
@@ -385,13 +385,15 @@ class DeviceOperator:
                 pass
             self._h = None
 
-    def apply(self, X, out=None, transpose=False, stream=None):
+    def apply(self, X, out=None, transpose=False, stream=None, save_x=False):
+        """Y = A X (or A^T X).  save_x: keep the sorted x for backward(..., reuse_x=True)
+        (LAPLEX_SAVE_X, the autograd "save for backward" of x)."""
         torch = self.torch
         rows = X.shape[0] if X.dim() == 2 else 1
         out_len = self.k if transpose else self.n
         if out is None:
             out = torch.empty((rows, out_len), dtype=self.dtype, device=X.device)
-        flags = (TRANSPOSE if transpose else 0) | (PHASED if self.phased else 0)
+        flags = (TRANSPOSE if transpose else 0) | (PHASED if self.phased else 0) | (SAVE_X if save_x else 0)
         _check(lib().laplex_apply_dev(self._h, flags, X.data_ptr(), rows, out.data_ptr(), self._stream(stream)))
         return out
 
@@ -411,7 +413,10 @@ class DeviceOperator:
         _check(lib().laplex_gram_apply_dev(self._h, X.data_ptr(), rows, out.data_ptr(), self._stream(stream)))
         return out
 
-    def backward(self, X, G, x_bar=None, a_bar=None, b_bar=None, phi_bar=None, psi_bar=None, stream=None):
+    def backward(self, X, G, x_bar=None, a_bar=None, b_bar=None, phi_bar=None, psi_bar=None, stream=None,
+                 reuse_x=False):
+        """(x_bar, a_bar, b_bar, phi_bar, psi_bar).  reuse_x: X is the (unchanged) tensor of
+        the preceding apply(..., save_x=True); its sorted copy is reused (bitwise same results)."""
         torch = self.torch
         rows = X.shape[0] if X.dim() == 2 else 1
         dev = X.device
@@ -426,7 +431,7 @@ class DeviceOperator:
                 phi_bar = torch.empty(self.n, dtype=self.dtype, device=dev)
             if psi_bar is None:
                 psi_bar = torch.empty(self.k, dtype=self.dtype, device=dev)
-        flags = PHASED if self.phased else 0
+        flags = (PHASED if self.phased else 0) | (REUSE_X if reuse_x else 0)
         _check(lib().laplex_backward_dev(self._h, flags, X.data_ptr(), G.data_ptr(), rows, x_bar.data_ptr(),
                                          a_bar.data_ptr(), b_bar.data_ptr(),
                                          phi_bar.data_ptr() if phi_bar is not None else None,

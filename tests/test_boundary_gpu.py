@@ -167,3 +167,31 @@ def test_backward_zero_rows_zeroes_phase_cotangents(torch):
     torch.cuda.synchronize()
     for o in outs:
         assert torch.count_nonzero(o) == 0
+
+
+@pytest.mark.parametrize("phased,n", [(False, 5000), (True, 7000), (False, (1 << 22) + 9)])
+def test_saved_forward_x_reuse_is_bitwise(torch, phased, n):
+    """apply(save_x) + backward(reuse_x) == plain backward, bitwise; a reuse
+    request for a different x (or after the saved x was consumed) recomputes."""
+    g_ = torch.Generator(device="cuda")
+    g_.manual_seed(n)
+    u = lambda *s, lo=-1.0, hi=1.0: torch.empty(*s, device="cuda").uniform_(lo, hi, generator=g_)  # noqa: E731
+    k = n + 31
+    a, b = u(n, lo=-40, hi=40), u(k, lo=-40, hi=40)
+    ph = (u(n, lo=0, hi=6), u(k, lo=0, hi=6)) if phased else (None, None)
+    X, X2, G = u(2, k), u(2, k), u(2, n)
+    dop = L.DeviceOperator(a, b, 1.0, *ph)
+    want = dop.backward(X, G)
+    y1 = dop.apply(X, save_x=True)
+    got = dop.backward(X, G, reuse_x=True)
+    for w, gg in zip(want, got):
+        assert (w is None and gg is None) or torch.equal(w, gg)
+    assert torch.equal(y1, dop.apply(X))
+    dop.apply(X2, save_x=True)
+    got2 = dop.backward(X, G, reuse_x=True)  # not the saved x: recomputed
+    for w, gg in zip(want, got2):
+        assert (w is None and gg is None) or torch.equal(w, gg)
+    got3 = dop.backward(X2, G, reuse_x=True)
+    want3 = dop.backward(X2, G)
+    for w, gg in zip(want3, got3):
+        assert (w is None and gg is None) or torch.equal(w, gg)

@@ -30,8 +30,6 @@ def test_compute_sanitizer(tool, n, rows):
     cmd = [SAN, "--tool", tool, "--error-exitcode", "97"]
     if tool == "memcheck":
         cmd += ["--leak-check", "no"]
-    if tool == "initcheck":
-        cmd += ["--track-unused-memory", "no"]
     r = subprocess.run(cmd + [DRIVER, str(n), str(rows)], capture_output=True, text=True, timeout=1500)
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
