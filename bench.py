@@ -73,14 +73,18 @@ STEP_MODEL_TEXT = {"fwd": "84n+80k+B(4n+4k)", "fwdbwd": "100n+96k+B(8n+12k)", "p
 def kernel_model_bytes(name, c):
     n, k, B, kind = c["n"], c["k"], c["B"], c["kind"]
     m2 = n + k
-    big = 1 << 22  # kDirectMax: larger sides use the two-pass permutation plans
-    staged = [m for m in (n, k) if m > big]
+    # sides permuted through the two-pass plans: larger than kDirectMax (2^22),
+    # or any side above 2^16 in a batch whose rows x side exceeds 48 MB
+    # (kBatchStageBytes, lx_capi.cu)
+    def is_staged(m):
+        return m > (1 << 22) or (B > 1 and m > (1 << 16) and B * m * 4 > (48 << 20))
+    big = 0
+    staged = [m for m in (n, k) if is_staged(m)]
     T = (m2 + 2047) // 2048
     tiles = (n + 4095) // 4096 + (k + 4095) // 4096
     phased = kind == "phased"
     # payload arrays per step, by side: (rows side element count, cols side)
     pay_rows = {"fwd": 0, "fwdbwd": B, "phased": B, "gram": B}[kind]  # g (bwd) / z (gram)
-    pay_cols = {"fwd": B, "fwdbwd": 2 * B, "phased": 2 * B, "gram": B}[kind]  # x (fwd, bwd)
     out_rows = {"fwd": B, "fwdbwd": B + 1, "phased": B + 2, "gram": B}[kind]  # y, a_bar, phi_bar / z
     out_cols = {"fwd": 0, "fwdbwd": B + 1, "phased": B + 2, "gram": B}[kind]  # x_bar, b_bar, psi_bar / y
     ch = 2 if phased else 1
@@ -98,16 +102,17 @@ def kernel_model_bytes(name, c):
         "lx_tiledesc": (T + 1) * 32,
         "lx_group_plan": 6 * m2,                            # output positions in, u16 store order out
         "lx_iota": 4 * n,
-        "lx_perm_gather": 12 * ((pay_cols * k if k > big else 0) + ((B if kind != "gram" else 0) * n
-                                                                   if n > big and kind != "fwd" else 0)),
-        "lx_gather_agg": 16 * (pay_cols * k + pay_rows * n) + 8 * m2 * (ch - 1),
+        # x once (the backward reuses the forward's sorted x), g in the backward
+        "lx_perm_gather": 12 * ((B * k if is_staged(k) else 0) + ((B if kind in ("fwdbwd", "phased") else 0) * n
+                                                                if is_staged(n) else 0)),
+        "lx_gather_agg": 16 * (B * k + pay_rows * n) + 8 * m2 * (ch - 1),
         "lx_carry": 2 * 2 * 4 * ch * max(B, 1) * T * 4,
         "lx_main_fwd": 4 * m2 + B * 4 * k + 6 * n + B * 4 * n,
         "lx_main_fwd_phased": 4 * m2 + 16 * m2 + B * 4 * k + 6 * n + B * 4 * n,
         "lx_main_trn": 4 * m2 + B * 4 * n + 6 * k + B * 4 * k,
         "lx_main_bwd": 4 * m2 + B * (4 * n + 4 * k) + 6 * m2 + B * 4 * k + 4 * n + 4 * k,
         "lx_main_bwd_phased": 4 * m2 + 16 * m2 + B * (4 * n + 4 * k) + 6 * m2 + B * 4 * k + 8 * n + 8 * k,
-        "lx_perm_scatter": 12 * ((out_rows * n if n > big else 0) + (out_cols * k if k > big else 0)),
+        "lx_perm_scatter": 12 * ((out_rows * n if is_staged(n) else 0) + (out_cols * k if is_staged(k) else 0)),
     }
     v = model.get(name)
     return v if v else None

@@ -256,7 +256,8 @@ struct Side {
     // dst[q] = caller index at bucketed position q (caller-index buckets of
     // 2^shift elements, so each bucket's caller range is an L2-sized window)
     DBuf spos, sdst;
-    bool staged = false;
+    bool staged = false;     // large side: every call permutes through the plan
+    bool has_splan = false;  // spos / sdst exist (large side, or built for a large batch)
     uint32_t m = 0;
 };
 
@@ -285,6 +286,7 @@ struct Core {
     DBuf ranks[4];  // [side*2 + strict]
     bool has_ranks[4] = {false, false, false, false};
     cudaEvent_t built[2] = {nullptr, nullptr};  // [0]: plan created; [1]: role-swapped data (lazy)
+    cudaEvent_t splan_ev[2] = {nullptr, nullptr};  // permutation plan of a small side built for a batch
     // x of the last forward kept for its backward (LAPLEX_SAVE_X / LAPLEX_REUSE_X):
     // the sorted payload and its tile aggregates (inclusive + strict), i.e.
     // exactly what the backward's x gather would recompute
@@ -323,7 +325,7 @@ struct Core {
             if (rel != u.first) cudaStreamWaitEvent(rel, u.second, 0);
             cudaEventDestroy(u.second);
         }
-        for (cudaEvent_t e : {built[0], built[1], saved.ready})
+        for (cudaEvent_t e : {built[0], built[1], saved.ready, splan_ev[0], splan_ev[1]})
             if (e) {
                 if (uses.size() != 1) cudaStreamWaitEvent(rel, e, 0);
                 cudaEventDestroy(e);
@@ -419,9 +421,24 @@ void build_partition(Core& c, int which, cudaStream_t st) {
         });
 }
 
+void build_splan(Side& sd, cudaStream_t st);
+
+// Batches whose rows x side footprint exceeds this permute a small side (one
+// that fits L2 and is permuted directly for single rows) through its plan too:
+// the main pass stores a row's outputs at perm positions, and with many rows
+// those random stores span rows x m elements, far beyond L2 (measured: the C4
+// transpose, 32 rows x 3.1M, at 0.23 TB/s writing direct).
+constexpr size_t kBatchStageBytes = size_t(48) << 20;
+
+// rows: batch rows of the call the view is for (selects the batch staging).
 template <class R>
-View<R> view(Core& c, bool swapped, cudaStream_t st) {
+View<R> view(Core& c, bool swapped, cudaStream_t st, size_t rows = 1) {
     const int ia = swapped ? 1 : 0;
+    bool use[2];
+    for (int sd = 0; sd < 2; ++sd) {
+        const Side& x = c.side[sd];
+        use[sd] = x.staged || (rows > 1 && x.m > (1u << 16) && rows * x.m * sizeof(R) > kBatchStageBytes);
+    }
     {
         // The role-swapped orientation is built on first use, on the first
         // caller's stream; every caller (any stream) orders itself after it.
@@ -433,6 +450,14 @@ View<R> view(Core& c, bool swapped, cudaStream_t st) {
         }
         if (c.built[0]) ck(cudaStreamWaitEvent(st, c.built[0], 0), "cudaStreamWaitEvent");
         if (ia && c.built[1]) ck(cudaStreamWaitEvent(st, c.built[1], 0), "cudaStreamWaitEvent");
+        for (int sd = 0; sd < 2; ++sd) {
+            if (use[sd] && !c.side[sd].has_splan) {  // lazily, once per side, on this stream
+                build_splan(c.side[sd], st);
+                if (!c.splan_ev[sd]) ck(cudaEventCreateWithFlags(&c.splan_ev[sd], cudaEventDisableTiming), "cudaEventCreate");
+                ck(cudaEventRecord(c.splan_ev[sd], st), "cudaEventRecord");
+            }
+            if (use[sd] && c.splan_ev[sd]) ck(cudaStreamWaitEvent(st, c.splan_ev[sd], 0), "cudaStreamWaitEvent");
+        }
     }
     View<R> v;
     const Side& a = c.side[ia];
@@ -453,10 +478,10 @@ View<R> view(Core& c, bool swapped, cudaStream_t st) {
     v.s_last = c.slast[ia].as<R>();
     v.T = c.T[ia];
     v.inv_t = R(1) / R(c.t);
-    v.pos_a = a.staged ? a.spos.as<uint32_t>() : nullptr;
-    v.dst_a = a.staged ? a.sdst.as<uint32_t>() : nullptr;
-    v.pos_b = b.staged ? b.spos.as<uint32_t>() : nullptr;
-    v.dst_b = b.staged ? b.sdst.as<uint32_t>() : nullptr;
+    v.pos_a = use[ia] ? a.spos.as<uint32_t>() : nullptr;
+    v.dst_a = use[ia] ? a.sdst.as<uint32_t>() : nullptr;
+    v.pos_b = use[1 - ia] ? b.spos.as<uint32_t>() : nullptr;
+    v.dst_b = use[1 - ia] ? b.sdst.as<uint32_t>() : nullptr;
     v.gm_a = c.gmap[ia][0].as<uint16_t>();
     v.gm_b = c.gmap[ia][1].as<uint16_t>();
     return v;
@@ -585,7 +610,7 @@ void build_splan(Side& sd, cudaStream_t st) {
             sd.perm.p, nullptr, sd.sdst.p, sd.spos.as<uint32_t>(), m, 1.0f, shift, nullptr,
             look.as<unsigned long long>(), ctr.as<uint32_t>(), 1u, offs);
     });
-    sd.staged = true;
+    sd.has_splan = true;
 }
 
 template <class R>
@@ -607,7 +632,10 @@ void build_side(Side& sd, const R* raw, uint32_t m, R t, const R* phase, int* ba
             cos_sin_kernel<R><<<(m + 255) / 256, 256, 0, st>>>(ph.as<R>(), m, sd.cph.as<R>(), sd.sph.as<R>());
         });
     }
-    if (m > kDirectMax) build_splan(sd, st);
+    if (m > kDirectMax) {
+        build_splan(sd, st);
+        sd.staged = true;
+    }
 }
 
 // ---- permutation application ------------------------------------------------
@@ -646,8 +674,8 @@ void stage_scatter_one(const uint32_t* dst, uint32_t m, const R* s1, R* o1, size
     const uint32_t chunks = (m + kPermChunk - 1) / kPermChunk;
     if (!g_out_hook) {
         launch("lx_perm_scatter", st, [&] {
-            lx_perm_stage_scatter<R><<<chunks, kPermThreads, 0, st>>>(dst, m, s1, o1, ld1, rows1, nullptr, nullptr,
-                                                                      nullptr, nullptr, 0u);
+            lx_perm_stage_scatter<R><<<dim3(chunks, rows1), kPermThreads, 0, st>>>(dst, m, s1, o1, ld1, rows1, nullptr,
+                                                                                 nullptr, nullptr, nullptr, 0u);
         });
         return;
     }
@@ -662,8 +690,9 @@ void stage_scatter_one(const uint32_t* dst, uint32_t m, const R* s1, R* o1, size
         if (u1 <= u0) continue;
         const uint32_t b0 = (uint32_t)(u0 / kPermChunk), b1 = (uint32_t)((u1 + kPermChunk - 1) / kPermChunk);
         launch("lx_perm_scatter", st, [&] {
-            lx_perm_stage_scatter<R><<<b1 - b0, kPermThreads, 0, st>>>(dst, m, s1, o1, ld1, rows1, nullptr, nullptr,
-                                                                       nullptr, nullptr, b0);
+            lx_perm_stage_scatter<R><<<dim3(b1 - b0, rows1), kPermThreads, 0, st>>>(dst, m, s1, o1, ld1, rows1,
+                                                                                  nullptr, nullptr, nullptr, nullptr,
+                                                                                  b0);
         });
         g_out_hook->fn(o1, u0, u1, rows1, ld1, st);
     }
@@ -1170,7 +1199,7 @@ void do_apply(laplex_plan_s* p, unsigned flags, const R* X, size_t rows, R* Y, c
     if (trn && ph) fail(LAPLEX_E_INVALID_ARGUMENT, "phased transpose is not part of the reference API");
     if (rows == 0) return;
     if (rows > 0x7fffffff) fail(LAPLEX_E_INVALID_SIZE, "too many rows");
-    View<R> v = view<R>(c, p->swapped, st);
+    View<R> v = view<R>(c, p->swapped, st, rows);
     Core* save = (flags & LAPLEX_SAVE_X) && !trn ? &c : nullptr;
     if (trn)
         apply_trn<R>(v, X, (int)rows, Y, st);
@@ -1188,7 +1217,7 @@ void do_backward(laplex_plan_s* p, unsigned flags, const R* X, const R* G, size_
     const bool ph = flags & LAPLEX_PHASED;
     if (ph && !c.phased) fail(LAPLEX_E_PHASE_ABSENT, "phased_matvec_vjp: operator has no phases");
     if (!ph && c.phased) fail(LAPLEX_E_PHASE_PRESENT, "matvec_vjp: use phased_matvec_vjp");
-    View<R> v = view<R>(c, p->swapped, st);
+    View<R> v = view<R>(c, p->swapped, st, rows);
     if (rows == 0) {
         if (before_g) before_g();
         ck(cudaMemsetAsync(abar, 0, (size_t)v.n * sizeof(R), st), "memset");
@@ -1233,7 +1262,7 @@ void do_gram_apply(laplex_plan_s* p, const R* X, size_t rows, R* Y, cudaStream_t
     if (c.phased) fail(LAPLEX_E_PHASE_PRESENT, "gram_apply: operator has phases (matvec is unphased)");
     if (rows == 0) return;
     if (rows > 0x7fffffff) fail(LAPLEX_E_INVALID_SIZE, "too many rows");
-    View<R> v = view<R>(c, p->swapped, st);
+    View<R> v = view<R>(c, p->swapped, st, rows);
     const int nr = (int)rows;
     DBuf zs((size_t)rows * v.n * sizeof(R) + kTmaPad, st);  // Z in sorted-row order
     {
@@ -1319,7 +1348,8 @@ void do_gram(laplex_plan_s* p, unsigned flags, const R* D, R* M, cudaStream_t st
 template <class R>
 void do_gram_vjp(laplex_plan_s* p, const R* Gbar, R* Dbar, cudaStream_t st) {
     Core& c = *p->core;
-    View<R> v = view<R>(c, p->swapped, st);
+    const int ia0 = p->swapped ? 1 : 0;
+    View<R> v = view<R>(c, p->swapped, st, c.side[ia0].m);
     DBuf Y((size_t)v.n * v.k * sizeof(R), st);
     apply_trn<R>(v, Gbar, (int)v.n, Y.as<R>(), st);
     DBuf pa((size_t)v.n * 4, st), pb((size_t)v.k * 4, st);

@@ -176,9 +176,18 @@ __device__ __forceinline__ void issue_tile(MainStage<R, NC>& S, const MainArgs<R
 #ifndef LX_OS_SMEM
 #define LX_OS_SMEM 0
 #endif
+// phased (256-thread) kernels: resident CTAs per SM the register budget targets
+#ifndef LX_PH_FWD_CTAS
+#define LX_PH_FWD_CTAS 2  // 3 spilled (72 registers): C3 forward 3.37 -> 2.42 ms with 2
+#endif
+#ifndef LX_PH_BWD_CTAS
+#define LX_PH_BWD_CTAS 2
+#endif
 template <class R, bool BWD, int TPB>
 constexpr int main_min_blocks() {
-    return sizeof(R) != 4 ? 1 : TPB == 256 ? (BWD ? 2 : 3) : (BWD ? LX_BWD_CTAS : LX_MAIN_CTAS) / TPB;
+    return sizeof(R) != 4 ? 1
+           : TPB == 256   ? (BWD ? LX_PH_BWD_CTAS : LX_PH_FWD_CTAS)
+                          : (BWD ? LX_BWD_CTAS : LX_MAIN_CTAS) / TPB;
 }
 
 // Channel layout: g channels first (c < NG), then x channels.  Strict prefix
@@ -339,6 +348,24 @@ __global__ void __launch_bounds__(TPB + 32, main_min_blocks<R, BWD, TPB>()) lx_m
 
         const bool first_t = tid == 0, last_t = tid == TPB - 1;
 
+        // phased: cos / sin of each element's phase (rows: phi, cols: psi),
+        // loaded once per tile instead of once per batch row and use
+        R mc[PHASED ? IPT : 1], ms[PHASED ? IPT : 1];
+        if constexpr (PHASED) {
+            int ia = ia0, ib = ib0;
+#pragma unroll
+            for (int q = 0; q < IPT; ++q) {
+                const bool isr = (rowm >> q) & 1, val = (valm >> q) & 1;
+                const R* cs = isr ? cphi + g.a0 + ia : cpsi + g.b0 + ib;
+                const R* sn = isr ? sphi + g.a0 + ia : spsi + g.b0 + ib;
+                const bool has = val && (isr ? (NG == 2 || !BWD) : NX == 2);
+                mc[q] = has ? *cs : R(1);
+                ms[q] = has ? *sn : R(0);
+                ia += isr;
+                ib += !isr;
+            }
+        }
+
         for (int r = 0; r < rows; ++r) {
             mbar_wait(&S.barp, (use * (uint32_t)rows + (uint32_t)r) & 1u);
             // ---- payloads: modulated channel values of each element ----
@@ -360,23 +387,13 @@ __global__ void __launch_bounds__(TPB + 32, main_min_blocks<R, BWD, TPB>()) lx_m
                     } else {
                         v = (val && !isr) ? pB[li] : R(0);
                     }
-                    R m0 = R(1), m1 = R(0);
-                    if constexpr (NG == 2) {
-                        if (val && isr) {
-                            m0 = cphi[g.a0 + li];
-                            m1 = sphi[g.a0 + li];
-                        }
-                    }
-                    if constexpr (NX == 2) {
-                        if (val && !isr) {
-                            m0 = cpsi[g.b0 + li];
-                            m1 = spsi[g.b0 + li];
-                        }
-                    }
                     if constexpr (PHASED) {
+                        // payload channels: the side's own modulation (rows: phi in the
+                        // backward; cols: psi); the forward's rows carry no payload
+                        const bool mod = isr ? NG == 2 : NX == 2;
                         raw[q] = v;
-                        pay[0][q] = xmul(m0, v);
-                        pay[1][q] = xmul(m1, v);
+                        pay[0][q] = mod ? xmul(mc[q], v) : v;
+                        pay[1][q] = mod ? xmul(ms[q], v) : R(0);
                     } else {
                         pay[0][q] = v;
                     }
@@ -708,19 +725,15 @@ __global__ void __launch_bounds__(TPB + 32, main_min_blocks<R, BWD, TPB>()) lx_m
                         const int li = ia++;
                         if constexpr (!BWD && NX > 0) {
                             R out = xadd(a[0], OS(0, q));
-                            if constexpr (NX == 2) {
-                                const uint32_t i = g.a0 + li;
-                                out = xadd(xmul(cphi[i], out), xmul(sphi[i], xadd(a[1], OS(1, q))));
-                            }
+                            if constexpr (NX == 2) out = xadd(xmul(mc[q], out), xmul(ms[q], xadd(a[1], OS(1, q))));
                             stg[li] = out;
                         } else if constexpr (BWD) {
                             if constexpr (!PHASED) {
                                 const R gg = pay[0][q];
                                 acc1 = xfma(xmul(gg, p.inv_t), xsub(OS(0, q), a[1]), acc1);
                             } else {
-                                const uint32_t i = g.a0 + li;
                                 const R gg = raw[q];
-                                const R m0 = cphi[i], m1 = sphi[i];
+                                const R m0 = mc[q], m1 = ms[q];
                                 const R in0 = xsub(OS(2, q), a[NG]);  // sum_{b>a} - sum_{b<a}
                                 const R in1 = xsub(OS(3, q), a[NG + 1]);
                                 acc1 = xfma(xmul(xmul(m0, gg), p.inv_t), in0, acc1);
@@ -740,9 +753,8 @@ __global__ void __launch_bounds__(TPB + 32, main_min_blocks<R, BWD, TPB>()) lx_m
                                 const R x = pay[0][q];
                                 acc1 = xfma(xmul(x, p.inv_t), xsub(OS(0, q), b[0]), acc1);
                             } else {
-                                const uint32_t j = g.b0 + li;
                                 const R x = raw[q];
-                                const R m0 = cpsi[j], m1 = spsi[j];
+                                const R m0 = mc[q], m1 = ms[q];
                                 const R xb1 = xadd(a[1], OS(1, q));
                                 stg[li] = xadd(xmul(m0, xb0), xmul(m1, xb1));
                                 acc2 = xfma(x, xadd(xmul(-m1, xb0), xmul(m0, xb1)), acc2);

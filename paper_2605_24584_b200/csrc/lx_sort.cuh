@@ -567,7 +567,11 @@ __global__ void __launch_bounds__(kPermThreads) lx_perm_stage_gather(const R* __
 }
 
 // scatter (sorted order -> caller order), second half: out[r][dst[q]] = stage[r][q]
-// for up to three arrays sharing the permutation (s2/s3 may be null).
+// for up to three arrays sharing the permutation (s2/s3 may be null, row 0
+// only).  One batch row per blockIdx.y: CTAs launch row by row, so the random
+// writes in flight stay inside one row's caller window (a CTA looping over 64
+// rows kept 64 windows -- 1 GB at n = 2^24 -- live in the 126 MB L2 and ran at
+// a third of the single-row rate).  dst is re-read per row (+4 B/element-row).
 template <class R>
 __global__ void __launch_bounds__(kPermThreads) lx_perm_stage_scatter(const uint32_t* __restrict__ dst, uint32_t m,
                                                                      const R* __restrict__ s1, R* __restrict__ o1,
@@ -575,25 +579,27 @@ __global__ void __launch_bounds__(kPermThreads) lx_perm_stage_scatter(const uint
                                                                      R* __restrict__ o2, const R* __restrict__ s3,
                                                                      R* __restrict__ o3, uint32_t block0) {
     const size_t q0 = (size_t)(blockIdx.x + block0) * kPermChunk + threadIdx.x;
+    const size_t r = blockIdx.y;
     uint32_t u[kPermItems];
 #pragma unroll
     for (int j = 0; j < kPermItems; ++j) {
         const size_t q = q0 + (size_t)j * kPermThreads;
         u[j] = q < m ? dst[q] : 0u;
     }
-    for (int r = 0; r < rows1; ++r) {
-#pragma unroll
-        for (int j = 0; j < kPermItems; ++j) {
-            const size_t q = q0 + (size_t)j * kPermThreads;
-            if (q < m) o1[(size_t)r * ld1 + u[j]] = s1[(size_t)r * m + q];
-        }
-    }
 #pragma unroll
     for (int j = 0; j < kPermItems; ++j) {
         const size_t q = q0 + (size_t)j * kPermThreads;
-        if (q < m) {
-            if (s2) o2[u[j]] = s2[q];
-            if (s3) o3[u[j]] = s3[q];
+        if (q < m) o1[r * ld1 + u[j]] = s1[r * m + q];
+    }
+    (void)rows1;
+    if (r == 0) {
+#pragma unroll
+        for (int j = 0; j < kPermItems; ++j) {
+            const size_t q = q0 + (size_t)j * kPermThreads;
+            if (q < m) {
+                if (s2) o2[u[j]] = s2[q];
+                if (s3) o3[u[j]] = s3[q];
+            }
         }
     }
 }

@@ -60,6 +60,10 @@ class AsymmetricCotangent(Error):
     pass
 
 
+class NumericalBreakdown(Error):
+    """errors.hpp:36 (raised by host-side callers such as FactorGaussian)."""
+
+
 class InvalidSize(Error):
     pass
 
@@ -396,6 +400,22 @@ class DeviceOperator:
         flags = (TRANSPOSE if transpose else 0) | (PHASED if self.phased else 0) | (SAVE_X if save_x else 0)
         _check(lib().laplex_apply_dev(self._h, flags, X.data_ptr(), rows, out.data_ptr(), self._stream(stream)))
         return out
+
+    def transposed(self) -> "DeviceOperator":
+        """Role-swapped operator sharing the device plan (operator.hpp:157-159; no re-sort)."""
+        h = C.c_void_p()
+        _check(lib().laplex_plan_transposed(self._h, C.byref(h)))
+        t = DeviceOperator.__new__(DeviceOperator)
+        t.torch, t.dtype, t._h, t.phased = self.torch, self.dtype, h, self.phased
+        t.n, t.k = self.k, self.n
+        return t
+
+    def weighted_gram(self, D, stream=None):
+        """M = A diag(D) A^T (n x n; phased_gram for a phased operator), operator.hpp:191-248."""
+        M = self.torch.empty((self.n, self.n), dtype=self.dtype, device=D.device)
+        _check(lib().laplex_gram_dev(self._h, PHASED if self.phased else 0, D.data_ptr(), M.data_ptr(),
+                                     self._stream(stream)))
+        return M
 
     def gram_vjp_weights(self, G_bar, stream=None):
         """D_bar (k) of gram_vjp_weights (gradients.hpp:190-219) for a symmetric
