@@ -508,27 +508,29 @@ void radix_sort(const R* raw, uint32_t m, R t, R* vals_out, uint32_t* perm_out, 
     DBuf v0((size_t)m * 4, st), v1((size_t)m * 4, st);
     DBuf look(kSortRts ? 8 : (size_t)tiles * kRadix * 8, st);
     DBuf cnt(kSortRts ? (size_t)tiles * kRadix * 4 : 4, st);
-    ck(cudaMemsetAsync(hist.p, 0, (size_t)P * kRadix * 4, st), "memset");
+    DBuf totals(kSortRts ? (size_t)P * kRadix * 4 : 4, st);
+    if (!kSortRts) ck(cudaMemsetAsync(hist.p, 0, (size_t)P * kRadix * 4, st), "memset");
     ck(cudaMemsetAsync(counters.p, 0, (size_t)P * 4, st), "memset");
     if (!kSortRts) ck(cudaMemsetAsync(look.p, 0, (size_t)tiles * kRadix * 8, st), "memset");
     const int sms = num_sms();
     const uint32_t per_block = kHistThreads * kHistItems;
     const uint32_t hgrid = std::max(1u, std::min<uint32_t>((m + per_block - 1) / per_block, (uint32_t)sms * 4));
     const size_t hsmem = (size_t)kHistSub * P * kRadix * sizeof(uint32_t);
-    if (kSortRts) {  // histograms + pass 1's per-tile counts in one read of the keys
+    if (kSortRts) {  // pass 1's per-tile counts (and the finiteness check) in one read of the keys;
+                     // the digit bases of every pass come from the scans' totals
         const uint32_t g0 = (tiles + kHistTilesPerCta - 1) / kHistTilesPerCta;
         launch("lx_sort_hist", st, [&] {
-            lx_sort_hist_count0<R><<<g0, kThreads, 0, st>>>(raw, m, t, hist.as<uint32_t>(), bad, cnt.as<uint32_t>(),
-                                                            tiles);
+            lx_sort_hist_count0<R, false><<<g0, kThreads, 0, st>>>(raw, m, t, hist.as<uint32_t>(), bad,
+                                                                   cnt.as<uint32_t>(), tiles);
         });
     } else {
         launch("lx_sort_hist", st, [&] {
             lx_sort_hist<R><<<hgrid, kHistThreads, hsmem, st>>>(raw, m, t, hist.as<uint32_t>(), bad);
         });
+        launch("lx_sort_bases", st, [&] {
+            lx_sort_bases<P><<<P, kRadix, 0, st>>>(hist.as<uint32_t>(), bases.as<uint32_t>());
+        });
     }
-    launch("lx_sort_bases", st, [&] {
-        lx_sort_bases<P><<<P, kRadix, 0, st>>>(hist.as<uint32_t>(), bases.as<uint32_t>());
-    });
     const size_t smem = sizeof(PassSmem<R>);
     smem_attr(lx_sort_pass<R, true, false>, smem);
     smem_attr(lx_sort_pass<R, false, false>, smem);
@@ -552,20 +554,22 @@ void radix_sort(const R* raw, uint32_t m, R t, R* vals_out, uint32_t* perm_out, 
                                                                                cnt.as<uint32_t>(), tiles);
                 });
             launch("lx_sort_scan", st, [&] {
-                lx_sort_scan<<<kRadix, kScanThreads, 0, st>>>(cnt.as<uint32_t>(), tiles, bptr, 0);
+                lx_sort_scan<<<kRadix, kScanThreads, 0, st>>>(cnt.as<uint32_t>(), tiles, nullptr, -1,
+                                                              totals.as<uint32_t>() + pass * kRadix);
             });
             offs = cnt.as<uint32_t>();
         }
+        const uint32_t* tots = kSortRts ? totals.as<uint32_t>() + pass * kRadix : nullptr;
         launch("lx_sort_pass", st, [&] {
             if (pass == 0)
                 lx_sort_pass<R, true, false><<<tiles, kThreads, smem, st>>>(in, inv, out, outv, m, t, pass * kBits,
-                                                                           bptr, lb, ctr, epoch, offs);
+                                                                           bptr, lb, ctr, epoch, offs, tots);
             else if (!last)
                 lx_sort_pass<R, false, false><<<tiles, kThreads, smem, st>>>(in, inv, out, outv, m, t, pass * kBits,
-                                                                            bptr, lb, ctr, epoch, offs);
+                                                                            bptr, lb, ctr, epoch, offs, tots);
             else
                 lx_sort_pass<R, false, true><<<tiles, kThreads, smem, st>>>(in, inv, out, outv, m, t, pass * kBits,
-                                                                           bptr, lb, ctr, epoch, offs);
+                                                                           bptr, lb, ctr, epoch, offs, tots);
         });
         in = out;
         inv = outv;

@@ -113,7 +113,9 @@ __global__ void __launch_bounds__(kHistThreads) lx_sort_hist(const R* __restrict
 #endif
 constexpr int kHistTilesPerCta = LX_HIST_TILES;
 
-template <class R>
+// HIST = false: only pass 1's per-tile counts (and the finiteness flag); the
+// global digit bases then come from the per-digit totals of lx_sort_scan.
+template <class R, bool HIST = true>
 __global__ void __launch_bounds__(kThreads) lx_sort_hist_count0(const R* __restrict__ raw, size_t n, R t,
                                                                uint32_t* __restrict__ hist, int* __restrict__ bad,
                                                                uint32_t* __restrict__ cnt, uint32_t tiles) {
@@ -145,8 +147,11 @@ __global__ void __launch_bounds__(kThreads) lx_sort_hist_count0(const R* __restr
             if (!isfinite(v[q])) any_bad = 1;
             const K key = radix_key<R>(xdiv(v[q], t));
             atomicAdd(&wt[warp][(int)(key & (kRadix - 1))], 1u);
+            if constexpr (HIST) {
 #pragma unroll
-            for (int p = 0; p < P; ++p) atomicAdd(&mine[p * kRadix + (int)((key >> (p * kBits)) & (kRadix - 1))], 1u);
+                for (int p = 0; p < P; ++p)
+                    atomicAdd(&mine[p * kRadix + (int)((key >> (p * kBits)) & (kRadix - 1))], 1u);
+            }
         }
         __syncthreads();
         if (tid < kRadix) {
@@ -161,11 +166,13 @@ __global__ void __launch_bounds__(kThreads) lx_sort_hist_count0(const R* __restr
         __syncthreads();
     }
     if (any_bad) atomicOr(bad, 1);
-    for (int i = tid; i < P * kRadix; i += kThreads) {
-        uint32_t c = 0;
+    if constexpr (HIST) {
+        for (int i = tid; i < P * kRadix; i += kThreads) {
+            uint32_t c = 0;
 #pragma unroll
-        for (int sub = 0; sub < SUB; ++sub) c += (&gh[sub][0][0])[i];
-        if (c) atomicAdd(&hist[i], c);
+            for (int sub = 0; sub < SUB; ++sub) c += (&gh[sub][0][0])[i];
+            if (c) atomicAdd(&hist[i], c);
+        }
     }
 }
 
@@ -195,6 +202,7 @@ struct PassSmem {
     uint32_t dstart[kRadix];
     uint32_t gbase[kRadix];
     uint32_t scan[kWarps];
+    uint32_t tscan[kWarps];
     uint32_t tile;
     alignas(16) K ik[kTile];         // input tile keys (raw values in the first pass)
     alignas(16) uint32_t iv[kTile];  // input payload
@@ -222,7 +230,8 @@ __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict_
                                                         int shift, const uint32_t* __restrict__ bases,
                                                         unsigned long long* __restrict__ lookback,
                                                         uint32_t* __restrict__ tile_counter, uint32_t epoch,
-                                                        const uint32_t* __restrict__ offs = nullptr) {
+                                                        const uint32_t* __restrict__ offs = nullptr,
+                                                        const uint32_t* __restrict__ totals = nullptr) {
     using K = typename Traits<R>::Key;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     PassSmem<R>& sm = *reinterpret_cast<PassSmem<R>*>(smem_raw);
@@ -285,6 +294,8 @@ __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict_
     __syncthreads();
 #endif
     const int d = tid;  // kThreads == kRadix
+    // digit totals of the whole pass (reduce-then-scan without upfront histogram)
+    const uint32_t tot = (offs && totals) ? totals[d] : 0u;
     uint32_t count = 0;
     unsigned long long* my_status = lookback + (size_t)tile * kRadix + d;
 #if !defined(LX_SORT_LATE)
@@ -341,23 +352,25 @@ __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict_
 #endif
 
     // block exclusive scan of counts over digits -> shared-memory positions
-    uint32_t incl = count;
+    uint32_t incl = count, tincl = tot;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
         const uint32_t v = __shfl_up_sync(FULL, incl, off);
-        if (lane >= off) incl += v;
+        const uint32_t tv = __shfl_up_sync(FULL, tincl, off);
+        if (lane >= off) incl += v, tincl += tv;
     }
-    if (lane == 31) sm.scan[warp] = incl;
+    if (lane == 31) sm.scan[warp] = incl, sm.tscan[warp] = tincl;
     __syncthreads();
-    uint32_t wpre = 0;
+    uint32_t wpre = 0, tpre = 0;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w)
-        if (w < warp) wpre += sm.scan[w];
+        if (w < warp) wpre += sm.scan[w], tpre += sm.tscan[w];
     const uint32_t dstart = wpre + incl - count;
+    const uint32_t dbase = tpre + tincl - tot;  // global start of digit d (0 without totals)
 
     if (offs) {  // reduce-then-scan: the offset is known
         sm.dstart[d] = dstart;
-        sm.gbase[d] = offs[(size_t)d * gridDim.x + tile] - dstart;
+        sm.gbase[d] = dbase + offs[(size_t)d * gridDim.x + tile] - dstart;
         __syncthreads();
         goto scatter;
     }
@@ -491,14 +504,19 @@ __global__ void __launch_bounds__(kThreads) lx_sort_count(const void* __restrict
 // d << shift for the plan pass (every caller bucket holds exactly 2^shift).
 // Coalesced: the CTA walks the digit's row in chunks of 4 * kScanThreads.
 constexpr int kScanThreads = 1024;
+// With bases == nullptr and shift < 0 the offsets are relative to the digit's
+// own start and the digit's total goes to totals[d]; the pass adds the global
+// base (the exclusive scan of the totals, formed in every pass CTA), so no
+// upfront histogram of the keys is needed.
 __global__ void __launch_bounds__(kScanThreads) lx_sort_scan(uint32_t* __restrict__ cnt, uint32_t tiles,
-                                                            const uint32_t* __restrict__ bases, int shift) {
+                                                            const uint32_t* __restrict__ bases, int shift,
+                                                            uint32_t* __restrict__ totals = nullptr) {
     constexpr int NW = kScanThreads / 32;
     __shared__ uint32_t ws[NW];
     __shared__ uint32_t carry;
     const int d = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     uint32_t* c = cnt + (size_t)d * tiles;
-    if (tid == 0) carry = bases ? bases[d] : ((uint32_t)d << shift);
+    if (tid == 0) carry = bases ? bases[d] : (shift >= 0 ? ((uint32_t)d << shift) : 0u);
     __syncthreads();
     for (uint32_t base = 0; base < tiles; base += 4 * kScanThreads) {
         const uint32_t i0 = base + 4 * (uint32_t)tid;
@@ -526,6 +544,7 @@ __global__ void __launch_bounds__(kScanThreads) lx_sort_scan(uint32_t* __restric
         if (tid == kScanThreads - 1) carry = run;
         __syncthreads();
     }
+    if (totals && tid == 0) totals[d] = carry;
 }
 
 // ---- permutation plans: the two L2-window passes --------------------------
@@ -586,10 +605,16 @@ __global__ void __launch_bounds__(kPermThreads) lx_perm_stage_scatter(const uint
         const size_t q = q0 + (size_t)j * kPermThreads;
         u[j] = q < m ? dst[q] : 0u;
     }
+    R v[kPermItems];  // all loads in flight before the random stores
 #pragma unroll
     for (int j = 0; j < kPermItems; ++j) {
         const size_t q = q0 + (size_t)j * kPermThreads;
-        if (q < m) o1[r * ld1 + u[j]] = s1[r * m + q];
+        v[j] = q < m ? s1[r * m + q] : R(0);
+    }
+#pragma unroll
+    for (int j = 0; j < kPermItems; ++j) {
+        const size_t q = q0 + (size_t)j * kPermThreads;
+        if (q < m) o1[r * ld1 + u[j]] = v[j];
     }
     (void)rows1;
     if (r == 0) {
