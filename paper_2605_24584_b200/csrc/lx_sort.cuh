@@ -24,12 +24,6 @@
 
 #include "lx_common.cuh"
 
-// digit counts published after ranking (measured faster on B200 than the
-// early-count variant: 64.8 vs 66.4 ms for the 8 passes at 2^30)
-#if !defined(LX_SORT_EARLY) && !defined(LX_SORT_LATE)
-#define LX_SORT_LATE
-#endif
-
 namespace lx {
 namespace sort {
 
@@ -194,6 +188,75 @@ __global__ void __launch_bounds__(kRadix) lx_sort_bases(const uint32_t* __restri
     bases[p * kRadix + d] = s[d] - hist[p * kRadix + d];
 }
 
+// Digit of a key in this pass.  Sort passes take whole bytes (one PRMT for
+// 32-bit keys); the permutation-plan pass (SPLAN) takes 8 bits at any shift.
+template <bool SPLAN, class K>
+__device__ __forceinline__ uint32_t digit_of(K key, int shift) {
+    if constexpr (!SPLAN && sizeof(K) == 4)
+        return __byte_perm((uint32_t)key, 0u, 0x4440u | (uint32_t)(shift >> 3));
+    else
+        return (uint32_t)(key >> shift) & (kRadix - 1);
+}
+
+// Lanes of the warp whose 8-bit digit equals this lane's, within `peers`:
+// per bit one predicate (LOP3), one ballot, one select and one LOP3.
+__device__ __forceinline__ unsigned match_digit8(unsigned peers, uint32_t dk) {
+    static_assert(kBits == 8, "match_digit8 covers 8 digit bits");
+    asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 t, m, s;\n\t"
+            "and.b32 t, %1, 1;\n\t"
+            "setp.ne.u32 p, t, 0;\n\t"
+            "vote.sync.ballot.b32 m, p, 0xffffffff;\n\t"
+            "selp.b32 s, 0, -1, p;\n\t"
+            "xor.b32 m, m, s;\n\t"
+            "and.b32 %0, %0, m;\n\t"
+            "and.b32 t, %1, 2;\n\t"
+            "setp.ne.u32 p, t, 0;\n\t"
+            "vote.sync.ballot.b32 m, p, 0xffffffff;\n\t"
+            "selp.b32 s, 0, -1, p;\n\t"
+            "xor.b32 m, m, s;\n\t"
+            "and.b32 %0, %0, m;\n\t"
+            "and.b32 t, %1, 4;\n\t"
+            "setp.ne.u32 p, t, 0;\n\t"
+            "vote.sync.ballot.b32 m, p, 0xffffffff;\n\t"
+            "selp.b32 s, 0, -1, p;\n\t"
+            "xor.b32 m, m, s;\n\t"
+            "and.b32 %0, %0, m;\n\t"
+            "and.b32 t, %1, 8;\n\t"
+            "setp.ne.u32 p, t, 0;\n\t"
+            "vote.sync.ballot.b32 m, p, 0xffffffff;\n\t"
+            "selp.b32 s, 0, -1, p;\n\t"
+            "xor.b32 m, m, s;\n\t"
+            "and.b32 %0, %0, m;\n\t"
+            "and.b32 t, %1, 16;\n\t"
+            "setp.ne.u32 p, t, 0;\n\t"
+            "vote.sync.ballot.b32 m, p, 0xffffffff;\n\t"
+            "selp.b32 s, 0, -1, p;\n\t"
+            "xor.b32 m, m, s;\n\t"
+            "and.b32 %0, %0, m;\n\t"
+            "and.b32 t, %1, 32;\n\t"
+            "setp.ne.u32 p, t, 0;\n\t"
+            "vote.sync.ballot.b32 m, p, 0xffffffff;\n\t"
+            "selp.b32 s, 0, -1, p;\n\t"
+            "xor.b32 m, m, s;\n\t"
+            "and.b32 %0, %0, m;\n\t"
+            "and.b32 t, %1, 64;\n\t"
+            "setp.ne.u32 p, t, 0;\n\t"
+            "vote.sync.ballot.b32 m, p, 0xffffffff;\n\t"
+            "selp.b32 s, 0, -1, p;\n\t"
+            "xor.b32 m, m, s;\n\t"
+            "and.b32 %0, %0, m;\n\t"
+            "and.b32 t, %1, 128;\n\t"
+            "setp.ne.u32 p, t, 0;\n\t"
+            "vote.sync.ballot.b32 m, p, 0xffffffff;\n\t"
+            "selp.b32 s, 0, -1, p;\n\t"
+            "xor.b32 m, m, s;\n\t"
+            "and.b32 %0, %0, m;\n\t"
+            "}"
+            : "+r"(peers)
+            : "r"(dk));
+    return peers;
+}
+
 template <class R>
 struct PassSmem {
     using K = typename Traits<R>::Key;
@@ -282,74 +345,39 @@ __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict_
     }
     // warp-striped item layout: item k of lane l is tile element w*32*kItems + k*32 + l
     const int wbase = warp * 32 * kItems;
-
-#if !defined(LX_SORT_LATE)
-    // ---- early counts: per-warp digit histogram (order-free smem atomics),
-    // published before ranking so successors' look-back overlaps our ranking ----
-#pragma unroll
-    for (int k = 0; k < kItems; ++k) {
-        const int li = wbase + k * 32 + lane;
-        if (li < tile_n) atomicAdd(&sm.whist[warp][(int)((sm.ik[li] >> shift) & (kRadix - 1))], 1u);
-    }
-    __syncthreads();
-#endif
-    const int d = tid;  // kThreads == kRadix
+    const bool full = tile_n == kTile;  // every tile but the last: no bounds checks
+    const int d = tid;                  // kThreads == kRadix
     // digit totals of the whole pass (reduce-then-scan without upfront histogram)
     const uint32_t tot = (offs && totals) ? totals[d] : 0u;
-    uint32_t count = 0;
     unsigned long long* my_status = lookback + (size_t)tile * kRadix + d;
-#if !defined(LX_SORT_LATE)
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-        const uint32_t c = sm.whist[w][d];
-        sm.whist[w][d] = count;
-        count += c;
-    }
-    st_relaxed_u64(my_status, status(tile == 0 ? kFlagInc : kFlagAgg, epoch, count));
-    __syncthreads();  // warp-exclusive offsets visible before the cursors start
-#endif
 
-    // ---- stable in-warp ranks: peer mask per key (8 ballots) and a running
-    // per-warp digit cursor ----
-    uint32_t rank[kItems];
+    // ---- stable in-warp ranks.  Per item: the mask of lanes holding the same
+    // digit (8 ballots), rank = the warp's running cursor of the digit + lower
+    // peers.  All peers read the cursor (one warp-wide LDS) and the highest
+    // peer advances it.  Rank and digit stay packed in one register per item.
+    uint32_t rd[kItems];  // rank | digit << 16
     const unsigned lt = lanemask_lt();
+    uint32_t* wh = sm.whist[warp];
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
-        // invalid tail items use digit 255 and are never counted: they follow
-        // every valid item of the warp, so they never shift a valid rank
         const int li = wbase + k * 32 + lane;
-        const bool valid = li < tile_n;
-        const int dk = valid ? (int)((sm.ik[li] >> shift) & (kRadix - 1)) : kRadix - 1;
-#if defined(LX_SORT_MATCH_ANY)
-        const unsigned peers = __match_any_sync(FULL, valid ? dk : kRadix);
-#else
-        unsigned peers = __ballot_sync(FULL, valid);
-        if (!valid) peers = ~peers;
-#pragma unroll
-        for (int b = 0; b < kBits; ++b) {
-            const bool bit = (dk >> b) & 1;
-            const unsigned m = __ballot_sync(FULL, bit);
-            peers &= bit ? m : ~m;
-        }
-#endif
-        const int leader = __ffs(peers) - 1;
-        uint32_t cnt = 0;
-        if (lane == leader) cnt = sm.whist[warp][dk];
-        cnt = __shfl_sync(FULL, cnt, leader);
-        if (lane == leader && valid) sm.whist[warp][dk] = cnt + __popc(peers);
-        rank[k] = cnt + __popc(peers & lt);
+        const bool valid = full || li < tile_n;
+        const uint32_t dk = digit_of<SPLAN>(sm.ik[li], shift);  // tail slots: stale, masked
+        // invalid tail lanes sit above every valid lane of the item: they are
+        // masked out of the peers and never advance a cursor
+        const unsigned peers = match_digit8(full ? FULL : __ballot_sync(FULL, valid), dk);
+        const uint32_t cnt = wh[dk];
+        const uint32_t r = cnt + __popc(peers & lt);
+        __syncwarp();
+        if (valid && (peers >> lane) == 1u) wh[dk] = r + 1u;
+        rd[k] = r | (dk << 16);
         __syncwarp();
     }
-#if defined(LX_SORT_LATE)
     __syncthreads();
+    uint32_t count = 0;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) {  // per digit: warp-exclusive offsets, tile count
-        const uint32_t c = sm.whist[w][d];
-        sm.whist[w][d] = count;
-        count += c;
-    }
+    for (int w = 0; w < kWarps; ++w) count += sm.whist[w][d];
     if (!offs) st_relaxed_u64(my_status, status(tile == 0 ? kFlagInc : kFlagAgg, epoch, count));
-#endif
 
     // block exclusive scan of counts over digits -> shared-memory positions
     uint32_t incl = count, tincl = tot;
@@ -367,9 +395,17 @@ __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict_
         if (w < warp) wpre += sm.scan[w], tpre += sm.tscan[w];
     const uint32_t dstart = wpre + incl - count;
     const uint32_t dbase = tpre + tincl - tot;  // global start of digit d (0 without totals)
+    {   // per (warp, digit): shared-memory start of the warp's keys of the digit
+        uint32_t run = dstart;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const uint32_t c = sm.whist[w][d];
+            sm.whist[w][d] = run;
+            run += c;
+        }
+    }
 
     if (offs) {  // reduce-then-scan: the offset is known
-        sm.dstart[d] = dstart;
         sm.gbase[d] = dbase + offs[(size_t)d * gridDim.x + tile] - dstart;
         __syncthreads();
         goto scatter;
@@ -390,7 +426,6 @@ __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict_
         }
         st_relaxed_u64(my_status, status(kFlagInc, epoch, excl + count));
     }
-    sm.dstart[d] = dstart;
     if constexpr (SPLAN)
         sm.gbase[d] = ((uint32_t)d << shift) + excl - dstart;
     else
@@ -403,15 +438,10 @@ scatter:
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
         const int li = wbase + k * 32 + lane;
-        if (li < tile_n) {
-            const K key = sm.ik[li];
-            const int dk = (int)((key >> shift) & (kRadix - 1));
-#if !defined(LX_SORT_LATE)
-            const uint32_t pos = sm.dstart[dk] + rank[k];  // rank includes the warp offset
-#else
-            const uint32_t pos = sm.dstart[dk] + sm.whist[warp][dk] + rank[k];
-#endif
-            sm.ok[pos] = key;
+        if (full || li < tile_n) {
+            const uint32_t dk = rd[k] >> 16;
+            const uint32_t pos = wh[dk] + (rd[k] & 0xffffu);
+            sm.ok[pos] = sm.ik[li];
             if constexpr (SPLAN)
                 out_vals[tile_start + li] = sm.gbase[dk] + pos;
             else
@@ -421,10 +451,9 @@ scatter:
     __syncthreads();
 
     // ---- digit-contiguous global writes ----
-    for (int i = tid; i < tile_n; i += kThreads) {
+    auto put = [&](int i) {
         const K kk = sm.ok[i];
-        const int dk = (int)((kk >> shift) & (kRadix - 1));
-        const uint32_t o = sm.gbase[dk] + (uint32_t)i;
+        const uint32_t o = sm.gbase[digit_of<SPLAN>(kk, shift)] + (uint32_t)i;
         if constexpr (SPLAN) {
             reinterpret_cast<K*>(out_keys)[o] = kk;
         } else if constexpr (LAST) {
@@ -435,6 +464,12 @@ scatter:
             reinterpret_cast<K*>(out_keys)[o] = kk;
             out_vals[o] = sm.ov[i];
         }
+    };
+    if (full) {
+#pragma unroll
+        for (int j = 0; j < kItems; ++j) put(j * kThreads + tid);
+    } else {
+        for (int i = tid; i < tile_n; i += kThreads) put(i);
     }
 }
 
