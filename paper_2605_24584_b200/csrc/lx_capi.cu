@@ -282,6 +282,7 @@ struct Core {
     DBuf part[2];  // merge-path tiles with side 0 (resp. 1) as the "A" operand, A-first
     DBuf desc[2], sfirst[2], slast[2];  // per-tile descriptors and edge anchors
     DBuf gmap[2][2];  // per orientation: store order of the A / B side in every tile (lx_group_plan)
+    DBuf mwd[2];      // per orientation: merge words of every tile (lx_group_plan)
     uint32_t T[2] = {0, 0};
     DBuf ranks[4];  // [side*2 + strict]
     bool has_ranks[4] = {false, false, false, false};
@@ -291,9 +292,9 @@ struct Core {
     // the sorted payload and its tile aggregates (inclusive + strict), i.e.
     // exactly what the backward's x gather would recompute
     struct SavedX {
-        const void* X = nullptr;
+        const void* X = nullptr;  // device pointer, or the caller's host pointer (host API)
         size_t rows = 0;
-        bool swapped = false, phased = false;
+        bool swapped = false, phased = false, host = false;
         DBuf xs, aggp, aggq;
         size_t ldxs = 0, agg_count = 0;
         cudaEvent_t ready = nullptr;
@@ -310,7 +311,7 @@ struct Core {
         for (Side& sd : side)
             for (DBuf* b : {&sd.vals, &sd.perm, &sd.cph, &sd.sph, &sd.spos, &sd.sdst}) f(*b);
         for (int o = 0; o < 2; ++o)
-            for (DBuf* b : {&part[o], &desc[o], &sfirst[o], &slast[o], &gmap[o][0], &gmap[o][1]}) f(*b);
+            for (DBuf* b : {&part[o], &desc[o], &sfirst[o], &slast[o], &gmap[o][0], &gmap[o][1], &mwd[o]}) f(*b);
         for (DBuf& b : ranks) f(b);
         f(saved.xs), f(saved.aggp), f(saved.aggq);
     }
@@ -376,6 +377,7 @@ struct View {
     R inv_t;
     const uint32_t *pos_a, *dst_a, *pos_b, *dst_b;  // null = direct permutation
     const uint16_t *gm_a, *gm_b;                      // per-tile store order (lx_group_plan)
+    const uint32_t* mw;                               // per-tile merge words (lx_group_plan)
 };
 
 // ≤256 caller-index buckets of 2^shift elements (permutation plans, store grouping)
@@ -406,6 +408,7 @@ void build_partition(Core& c, int which, cudaStream_t st) {
             c.desc[which].as<lx::ms::TileDesc<R>>(), c.sfirst[which].as<R>(), c.slast[which].as<R>());
     });
     c.T[which] = T;
+    c.mwd[which] = DBuf((size_t)T * lx::ms::kMergeWords * 4 + 16, st);
     // per-tile store order of both sides (output positions: plan pos or perm)
     const uint32_t* pa = a.staged ? a.spos.as<uint32_t>() : a.perm.as<uint32_t>();
     const uint32_t* pb = b.staged ? b.spos.as<uint32_t>() : b.perm.as<uint32_t>();
@@ -417,7 +420,8 @@ void build_partition(Core& c, int which, cudaStream_t st) {
         launch("lx_group_plan", st, [&] {
             lx::ms::lx_group_plan<R><<<T, lx::ms::kGroupBuckets, gsm, st>>>(
                 c.desc[which].as<lx::ms::TileDesc<R>>(), T, pa, bucket_shift(a.m), pb, bucket_shift(b.m),
-                c.gmap[which][0].as<uint16_t>(), c.gmap[which][1].as<uint16_t>());
+                c.gmap[which][0].as<uint16_t>(), c.gmap[which][1].as<uint16_t>(), a.vals.as<R>(), b.vals.as<R>(),
+                c.mwd[which].as<uint32_t>());
         });
 }
 
@@ -484,6 +488,7 @@ View<R> view(Core& c, bool swapped, cudaStream_t st, size_t rows = 1) {
     v.dst_b = use[1 - ia] ? b.sdst.as<uint32_t>() : nullptr;
     v.gm_a = c.gmap[ia][0].as<uint16_t>();
     v.gm_b = c.gmap[ia][1].as<uint16_t>();
+    v.mw = c.mwd[ia].as<uint32_t>();
     return v;
 }
 
@@ -816,6 +821,7 @@ lx::ms::MainArgs<R> main_args(const View<R>& v, int rows) {
     a.perm_b = v.pb;
     a.part = v.part;
     a.desc = v.desc;
+    a.mwords = v.mw;
     a.s_last = v.s_last;
     a.s_first = v.s_first;
     a.n = v.n;
@@ -1059,6 +1065,7 @@ void apply_fwd(const View<R>& v, const R* X, int rows, R* Y, cudaStream_t st, Co
     std::lock_guard<std::mutex> g(save->saved_mu);
     auto& sv = save->saved;
     sv.X = X;
+    sv.host = false;
     sv.rows = (size_t)rows;
     sv.swapped = swapped;
     sv.phased = NX == 2;
@@ -1214,9 +1221,12 @@ void do_apply(laplex_plan_s* p, unsigned flags, const R* X, size_t rows, R* Y, c
     touch(c, st);
 }
 
+// host_x: X is the caller's host pointer of a host-API call that reuses the
+// x saved by a host-API apply (never dereferenced then).
 template <class R>
 void do_backward(laplex_plan_s* p, unsigned flags, const R* X, const R* G, size_t rows, R* xbar, R* abar, R* bbar,
-                 R* phibar, R* psibar, cudaStream_t st, const std::function<void()>& before_g = {}) {
+                 R* phibar, R* psibar, cudaStream_t st, const std::function<void()>& before_g = {},
+                 bool host_x = false) {
     Core& c = *p->core;
     const bool ph = flags & LAPLEX_PHASED;
     if (ph && !c.phased) fail(LAPLEX_E_PHASE_ABSENT, "phased_matvec_vjp: operator has no phases");
@@ -1236,7 +1246,7 @@ void do_backward(laplex_plan_s* p, unsigned flags, const R* X, const R* G, size_
     std::unique_lock<std::mutex> lk(c.saved_mu);
     Core* reuse = nullptr;
     if ((flags & LAPLEX_REUSE_X) && c.saved.xs.p && c.saved.X == (const void*)X && c.saved.rows == rows &&
-        c.saved.swapped == p->swapped && c.saved.phased == ph)
+        c.saved.swapped == p->swapped && c.saved.phased == ph && c.saved.host == host_x)
         reuse = &c;
     else
         lk.unlock();
@@ -1978,7 +1988,14 @@ int laplex_apply(laplex_plan plan, unsigned flags, const void* X, size_t rows, s
             dl.add(dy.p, Y, out_len, (int)rows);
             {
                 HookScope hs(&dl.hook);
-                do_apply<R>(plan, flags & ~LAPLEX_SAVE_X, dx.get(), rows, dy.as<R>(), st);
+                do_apply<R>(plan, flags, dx.get(), rows, dy.as<R>(), st);
+            }
+            if ((flags & LAPLEX_SAVE_X) && !trn) {  // the saved x is keyed by the caller's host pointer
+                std::lock_guard<std::mutex> g(c.saved_mu);
+                if (c.saved.X == (const void*)dx.get()) {
+                    c.saved.X = X;
+                    c.saved.host = true;
+                }
             }
             dl.finish(st);
         };
@@ -2064,15 +2081,26 @@ int laplex_backward(laplex_plan plan, unsigned flags, const void* X, size_t rows
         if (gcols != n) fail(LAPLEX_E_DIMENSION_MISMATCH, "matvec_vjp: g length");
         cudaStream_t st = host_stream();
         const size_t rs = rsize(c.dtype);
+        // LAPLEX_REUSE_X after a host-API apply with LAPLEX_SAVE_X of the same
+        // X, rows and orientation: x is neither uploaded nor checked again (the
+        // caller asserts it is unchanged; the apply checked it)
+        bool reuse;
+        {
+            std::lock_guard<std::mutex> g(c.saved_mu);
+            reuse = (flags & LAPLEX_REUSE_X) && c.saved.xs.p && c.saved.host && c.saved.X == X &&
+                    c.saved.rows == rows && c.saved.swapped == plan->swapped && c.saved.phased == ph;
+        }
         auto run = [&](auto zero) {
             using R = decltype(zero);
             // x first: its gather runs while g is still uploading
-            HostUp<R> dx(X, rows * k, st);
+            HostUp<R> dx(reuse ? nullptr : X, reuse ? 0 : rows * k, st);
             HostUp<R> dg(G, rows * n, st);
             DBuf xb(rows * k * rs, st), ab(n * rs, st), bb(k * rs, st), pb(ph ? n * rs : 0, st), qb(ph ? k * rs : 0, st);
             Flags f(2, st);
-            dx.wait(st);
-            launch_finite<R>(dx.get(), rows * k, f.at(0), st);
+            if (!reuse) {
+                dx.wait(st);
+                launch_finite<R>(dx.get(), rows * k, f.at(0), st);
+            }
             Downloader dl(rs);
             dl.check = [&] {
                 const int* h = f.wait();
@@ -2088,12 +2116,14 @@ int laplex_backward(laplex_plan plan, unsigned flags, const void* X, size_t rows
             }
             {
                 HookScope hs(&dl.hook);
-                do_backward<R>(plan, flags, dx.get(), dg.get(), rows, xb.as<R>(), ab.as<R>(), bb.as<R>(),
-                               pb.as<R>(), qb.as<R>(), st, [&] {
+                do_backward<R>(plan, reuse ? flags : flags & ~LAPLEX_REUSE_X, reuse ? (const R*)X : dx.get(),
+                               dg.get(), rows, xb.as<R>(), ab.as<R>(), bb.as<R>(), pb.as<R>(), qb.as<R>(), st,
+                               [&] {
                                    dg.wait(st);
                                    launch_finite<R>(dg.get(), rows * n, f.at(1), st);
                                    f.snapshot(st);
-                               });
+                               },
+                               reuse);
             }
             dl.finish(st);
         };

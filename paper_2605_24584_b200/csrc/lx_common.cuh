@@ -146,6 +146,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
+// order this thread's generic-proxy shared-memory accesses before later
+// async-proxy (TMA) accesses of the same bytes (buffer refills)
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 // element-wise async gather global -> shared (LDGSTS)
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {

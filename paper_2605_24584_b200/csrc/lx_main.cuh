@@ -52,6 +52,7 @@ struct MainStage {
     alignas(16) R pay[kTile + 8 * kPad];  // row payloads, same layout
     alignas(16) uint32_t oidx[kTile + 16];  // output index ranges: A at [offIA], B at [baseIB + offIB]
     alignas(16) uint16_t gm[kTile + 32];    // store order (lx_group_plan): A at [offGA], B at [baseGB]
+    alignas(16) uint32_t mw[kMergeWords];   // the tile's merge words (lx_merge_words)
 };
 
 #ifndef LX_MAIN_STAGES
@@ -140,7 +141,9 @@ __device__ __forceinline__ void issue_tile(MainStage<R, NC>& S, const MainArgs<R
     S.s_last = dt.s_last;
     S.SL = SL;
     S.SR = dn.s_first;
-    mbar_expect_tx(&S.bar, g.bytesA + g.bytesB + g.ibytesA + g.ibytesB + g.gbytesA + g.gbytesB);
+    constexpr uint32_t kMW = SEQ ? 0u : (uint32_t)(kMergeWords * 4);
+    mbar_expect_tx(&S.bar, g.bytesA + g.bytesB + g.ibytesA + g.ibytesB + g.gbytesA + g.gbytesB + kMW);
+    if (kMW) bulk_g2s(S.mw, p.mwords + (size_t)t * kMergeWords, kMW, &S.bar);
     if (g.bytesA) bulk_g2s(S.anch, p.A + g.a0al, g.bytesA, &S.bar);
     if (g.bytesB) bulk_g2s(S.anch + (g.bytesA / sizeof(R)) + MainStage<R, NC>::kPad, p.B + g.b0al, g.bytesB, &S.bar);
     if (g.ibytesA) bulk_g2s(S.oidx, p.perm_a + g.a0i, g.ibytesA, &S.bar);
@@ -286,12 +289,6 @@ __global__ void __launch_bounds__(TPB + 32, main_min_blocks<R, BWD, TPB>()) lx_m
         const R SR = t + 1 < T ? S.SR : ext_qa;
         R* sA = S.anch + g.offA;
         R* sB = S.anch + g.baseB;
-        const R kInf = R(__int_as_float(0x7f800000));
-        if (tid == 0) {  // +inf behind both ranges: the merge reads past an exhausted side
-            sA[na] = kInf;
-            sB[nb] = kInf;
-        }
-        cbar<TPB>();
         const R* pA = S.pay + g.offA;
         const R* pB = S.pay + g.baseB;
         const uint32_t* iA = S.oidx + g.offIA;
@@ -299,31 +296,34 @@ __global__ void __launch_bounds__(TPB + 32, main_min_blocks<R, BWD, TPB>()) lx_m
         const uint16_t* gmA = S.gm + g.offGA;  // store order of the tile rows / cols
         const uint16_t* gmB = S.gm + g.baseGB;
 
-        // ---- merge: anchors and kinds of this thread's IPT elements ----
+        // ---- this thread's IPT merged elements: kinds from the plan's merge
+        // words, anchors by independent shared-memory loads ----
+        static_assert(kMergeGroup % IPT == 0, "a thread's elements lie in one merge word");
         R s[IPT];
-        unsigned rowm = 0;  // bit q: element q is a row
+        unsigned rowm;  // bit q: element q is a row
         int ia0, ib0, nval;
         {
             const int dd = min(tid * IPT, len);
             nval = min(IPT, len - dd);
-            int ia = merge_path<true, R, int>(sA, na, sB, nb, dd);
+            int ia;
+            if constexpr (SEQ) {  // one sequence: every element is a "row"
+                rowm = (1u << IPT) - 1u;
+                ia = dd;
+            } else {
+                const uint32_t w = S.mw[(tid * IPT) / kMergeGroup];
+                const int sh = (tid * IPT) % kMergeGroup;
+                rowm = (w >> sh) & ((1u << IPT) - 1u);
+                ia = (int)(w >> 16) + __popc(w & ((1u << sh) - 1u));
+            }
             int ib = dd - ia;
             ia0 = ia;
             ib0 = ib;
-            R av = sA[ia], bv = sB[ib];  // +inf sentinels behind both ranges
-            // branch-free: one compare and one shared load per element; anchors
-            // are finite, so an exhausted side (+inf) is never taken while the
-            // other has elements
 #pragma unroll
             for (int q = 0; q < IPT; ++q) {
-                const bool takeA = av <= bv;
-                s[q] = takeA ? av : bv;
-                rowm |= (unsigned)takeA << q;
-                ia += takeA;
-                ib += !takeA;
-                const R nx = takeA ? sA[ia] : sB[ib];
-                av = takeA ? nx : av;
-                bv = takeA ? bv : nx;
+                const bool r = (rowm >> q) & 1u;
+                s[q] = r ? sA[ia] : sB[ib];  // past the tile end: stale, replaced below
+                ia += r;
+                ib += !r;
             }
 #pragma unroll
             for (int q = 0; q < IPT; ++q)
@@ -792,6 +792,7 @@ __global__ void __launch_bounds__(TPB + 32, main_min_blocks<R, BWD, TPB>()) lx_m
                     }
                 }
             }
+            fence_proxy_async_smem();  // staging writes before any TMA refill of this stage
             cbar<TPB>();  // (C) staging row and warp totals free for the next row / tile
         }
         if constexpr (BWD) {  // anchor cotangents summed over rows (complete after (C))

@@ -126,6 +126,18 @@ __global__ void lx_tiledesc(const R* __restrict__ A, uint32_t n, const R* __rest
 }
 
 // ---------------------------------------------------------------------------
+// Merge words (built by lx_group_plan, once per plan orientation): word g of a
+// tile covers merged elements [16g, 16g + 16) (rows first on ties, the order
+// lx_main consumes); bit q = element 16g + q is a row, bits 16..31 = rows of
+// the tile before element 16g.  The main pass then reads its elements' anchors
+// with independent shared-memory loads instead of a merge-path search and a
+// serial merge.
+// ---------------------------------------------------------------------------
+constexpr int kMergeGroup = 16;
+constexpr int kMergeWords = kTile / kMergeGroup;  // words per tile
+static_assert(kItems * 2 == kMergeGroup, "two merge threads per word");
+
+// ---------------------------------------------------------------------------
 // co-ranks (accessor path): AFIRST gives J<[i] and R<=[j]; !AFIRST gives
 // J<=[i] and R<[j]  (operator.hpp:110-120 are the two tie-inclusive ones).
 // ---------------------------------------------------------------------------
@@ -183,6 +195,7 @@ struct MainArgs {
     const uint16_t* gmap_a;
     const uint16_t* gmap_b;
     const TileDesc<R>* desc;  // T+1 tile descriptors
+    const uint32_t* mwords;   // lx_merge_words: kMergeWords per tile (null: single-sequence SEQ pass)
     uint32_t n, k, T;
     int rows;
     // payloads in SORTED order (lx_gather_agg output), rows x ld (ld % (16/sizeof(R)) == 0)
@@ -307,26 +320,30 @@ __device__ __forceinline__ void group_tile(uint16_t (&gmap)[2][kTile], uint32_t 
     if (SB) gcnt[1][tid] = 0u;
 }
 
-// Plan-time store order of every merge tile (both sides), consumed by lx_main:
-// the grouping depends only on the plan (positions and tiles), so it is built
-// once per plan orientation instead of in every apply / backward.
+// Plan-time per-tile data consumed by lx_main, built once per plan orientation
+// (it depends only on the plan): the store order of both sides (grouping by
+// output bucket) and the tile's merge words (see lx_merge_words).
 template <class R>
 constexpr size_t group_plan_smem() {
     return sizeof(uint32_t) * 2 * kTile + sizeof(uint16_t) * 2 * kTile + sizeof(uint32_t) * 2 * kGroupBuckets +
-           sizeof(uint32_t) * 2 * (kGroupBuckets / 32) + 16;
+           sizeof(uint32_t) * 2 * (kGroupBuckets / 32) + sizeof(R) * (kTile + 2) + 16;
 }
 
 template <class R>
 __global__ void __launch_bounds__(kGroupBuckets) lx_group_plan(const TileDesc<R>* __restrict__ desc, uint32_t T,
                                                                const uint32_t* __restrict__ posA, int shA,
                                                                const uint32_t* __restrict__ posB, int shB,
-                                                               uint16_t* __restrict__ gA, uint16_t* __restrict__ gB) {
+                                                               uint16_t* __restrict__ gA, uint16_t* __restrict__ gB,
+                                                               const R* __restrict__ A, const R* __restrict__ B,
+                                                               uint32_t* __restrict__ words) {
     constexpr int TPB = kGroupBuckets, NW = TPB / 32;
+    static_assert(TPB == kThreads, "one merge thread per grouping thread");
     struct Smem {
         uint32_t sA[kTile], sB[kTile];
         uint16_t gmap[2][kTile];
         uint32_t gcnt[2][kGroupBuckets];
         uint32_t gwarp[2][NW];
+        R anc[kTile + 2];
     };
     extern __shared__ __align__(16) unsigned char smem_group[];  // dynamic: > 48 KB for large tiles
     Smem& sm = *reinterpret_cast<Smem*>(smem_group);
@@ -340,11 +357,43 @@ __global__ void __launch_bounds__(kGroupBuckets) lx_group_plan(const TileDesc<R>
     const TileDesc<R> dt = desc[t], dn = desc[t + 1];
     const uint32_t a0 = dt.a0, b0 = dt.b0;
     const int na = (int)(dn.a0 - a0), nb = (int)(dn.b0 - b0);
-    for (int i = tid; i < na; i += TPB) sA[i] = posA[a0 + i];
-    for (int i = tid; i < nb; i += TPB) sB[i] = posB[b0 + i];
+    R* mA = sm.anc;
+    R* mB = sm.anc + na + 1;
+    for (int i = tid; i < na; i += TPB) {
+        sA[i] = posA[a0 + i];
+        mA[i] = A[a0 + i];
+    }
+    for (int i = tid; i < nb; i += TPB) {
+        sB[i] = posB[b0 + i];
+        mB[i] = B[b0 + i];
+    }
+    if (tid == 0) {  // +inf behind both ranges: the merge reads past an exhausted side
+        const R inf = R(__int_as_float(0x7f800000));
+        mA[na] = inf;
+        mB[nb] = inf;
+    }
     gcnt[0][tid] = 0u;
     gcnt[1][tid] = 0u;
     __syncthreads();
+    {   // merge words (rows first on ties), kItems merged elements per thread
+        const int len = na + nb;
+        const int dd = min(tid * kItems, len);
+        const int nval = min(kItems, len - dd);
+        int ia = merge_path<true, R, int>(mA, na, mB, nb, dd), ib = dd - ia;
+        const int ia0 = ia;
+        uint32_t m = 0;
+        R av = mA[ia], bv = mB[ib];
+        for (int q = 0; q < nval; ++q) {
+            const bool takeA = av <= bv;
+            m |= (uint32_t)takeA << q;
+            if (takeA)
+                av = mA[++ia];
+            else
+                bv = mB[++ib];
+        }
+        const uint32_t hi = __shfl_down_sync(FULL, m, 1);
+        if ((tid & 1) == 0) words[(size_t)t * kMergeWords + tid / 2] = m | (hi << kItems) | ((uint32_t)ia0 << 16);
+    }
     group_tile<TPB, NW, true, true, 0>(gmap, gcnt, gwarp, sA, na, shA, sB, nb, shB, tid);
     for (int k = tid; k < na; k += TPB) gA[a0 + k] = gmap[0][k];
     for (int k = tid; k < nb; k += TPB) gB[b0 + k] = gmap[1][k];

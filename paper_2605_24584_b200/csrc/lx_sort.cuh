@@ -261,17 +261,25 @@ template <class R>
 struct PassSmem {
     using K = typename Traits<R>::Key;
     unsigned long long bar;
-    uint32_t whist[kWarps][kRadix];
-    uint32_t dstart[kRadix];
+    uint32_t whist[kWarps][kRadix];  // per-warp digit cursors, then per-warp digit starts
     uint32_t gbase[kRadix];
     uint32_t scan[kWarps];
     uint32_t tscan[kWarps];
     uint32_t tile;
-    alignas(16) K ik[kTile];         // input tile keys (raw values in the first pass)
-    alignas(16) uint32_t iv[kTile];  // input payload
-    alignas(16) K ok[kTile];         // digit-ordered staging for coalesced writes
-    alignas(16) uint32_t ov[kTile];
+    // the input tile; reordered in place into digit order before the global
+    // writes (keys, then payload, each through registers)
+    alignas(16) K ik[kTile];
+    alignas(16) uint32_t iv[kTile];
 };
+
+// CTAs per SM the 32-bit-key pass is built for (64 registers, ~42 KB of shared
+// memory; 4 measured 2% faster than 3 at 2^30).  A persistent double-buffered
+// form (next tile's TMA in flight during ranking) measured 7% slower.
+#ifndef LX_SORT_CTAS
+#define LX_SORT_CTAS 4
+#endif
+template <class R>
+constexpr int sort_min_blocks() { return sizeof(typename Traits<R>::Key) == 4 ? LX_SORT_CTAS : 2; }
 
 // One digit pass.  FIRST reads the raw anchors and builds keys+payload on the
 // fly; LAST writes sorted values (Real) and perm (u32) instead of key/payload.
@@ -286,7 +294,7 @@ struct PassSmem {
 // then read from shared memory where needed, so no thread holds its 16 keys
 // across the load latency (register pressure, hence occupancy).
 template <class R, bool FIRST, bool LAST, bool SPLAN = false>
-__global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict__ in_keys,
+__global__ void __launch_bounds__(kThreads, sort_min_blocks<R>()) lx_sort_pass(const void* __restrict__ in_keys,
                                                         const uint32_t* __restrict__ in_vals,
                                                         void* __restrict__ out_keys,
                                                         uint32_t* __restrict__ out_vals, size_t n, R t,
@@ -434,35 +442,52 @@ __global__ void __launch_bounds__(kThreads) lx_sort_pass(const void* __restrict_
     }
 scatter:
 
-    // ---- scatter into shared memory in digit order ----
+    // ---- reorder the tile in place into digit order: keys, then payload ----
+    {
+        K kv[kItems];
 #pragma unroll
-    for (int k = 0; k < kItems; ++k) {
-        const int li = wbase + k * 32 + lane;
-        if (full || li < tile_n) {
-            const uint32_t dk = rd[k] >> 16;
-            const uint32_t pos = wh[dk] + (rd[k] & 0xffffu);
-            sm.ok[pos] = sm.ik[li];
-            if constexpr (SPLAN)
-                out_vals[tile_start + li] = sm.gbase[dk] + pos;
-            else
-                sm.ov[pos] = sm.iv[li];
+        for (int k = 0; k < kItems; ++k) {
+            const int li = wbase + k * 32 + lane;
+            kv[k] = sm.ik[li];  // tail slots: stale, never stored
+            rd[k] = (wh[rd[k] >> 16] + (rd[k] & 0xffffu)) | (rd[k] & 0xffff0000u);  // shared position | digit
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+            const int li = wbase + k * 32 + lane;
+            if (full || li < tile_n) {
+                const uint32_t pos = rd[k] & 0xffffu;
+                sm.ik[pos] = kv[k];
+                if constexpr (SPLAN) out_vals[tile_start + li] = sm.gbase[rd[k] >> 16] + pos;
+            }
+        }
+    }
+    if constexpr (!SPLAN) {
+        uint32_t vv[kItems];
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) vv[k] = sm.iv[wbase + k * 32 + lane];
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+            const int li = wbase + k * 32 + lane;
+            if (full || li < tile_n) sm.iv[rd[k] & 0xffffu] = vv[k];
         }
     }
     __syncthreads();
 
     // ---- digit-contiguous global writes ----
     auto put = [&](int i) {
-        const K kk = sm.ok[i];
+        const K kk = sm.ik[i];
         const uint32_t o = sm.gbase[digit_of<SPLAN>(kk, shift)] + (uint32_t)i;
         if constexpr (SPLAN) {
             reinterpret_cast<K*>(out_keys)[o] = kk;
         } else if constexpr (LAST) {
-            const uint32_t v = sm.ov[i];
+            const uint32_t v = sm.iv[i];
             reinterpret_cast<R*>(out_keys)[o] = radix_value<R>(kk, (v >> 31) != 0);
             out_vals[o] = v & 0x7fffffffu;
         } else {
             reinterpret_cast<K*>(out_keys)[o] = kk;
-            out_vals[o] = sm.ov[i];
+            out_vals[o] = sm.iv[i];
         }
     };
     if (full) {

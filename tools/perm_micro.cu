@@ -118,6 +118,26 @@ __global__ void make_li(uint16_t* li, size_t m, int wbits) {
     }
 }
 
+// digit-run writes of a radix pass: tile t (RK keys) writes RK/256 consecutive
+// keys (+ values) into each of 256 digit regions, like a uniform-digit pass
+template <int RK>
+__global__ void __launch_bounds__(256) runs(const uint2* __restrict__ in, uint32_t* __restrict__ ok,
+                                            uint32_t* __restrict__ ov, size_t m) {
+    constexpr int RUN = RK / 256;
+    const size_t tiles = m / RK;
+    const size_t t = blockIdx.x;
+    const size_t region = m / 256;
+    for (int j = 0; j < RK / 256; ++j) {
+        const int i = j * 256 + threadIdx.x;  // position in the tile, digit-major
+        const uint2 kv = in[t * RK + i];
+        const int d = i / RUN, r = i % RUN;
+        const size_t o = (size_t)d * region + t * RUN + r;
+        ok[o] = kv.x;
+        ov[o] = kv.y;
+    }
+    (void)tiles;
+}
+
 template <class F>
 float timeit(F f, int reps = 5) {
     cudaEvent_t a, b;
@@ -161,6 +181,18 @@ int main(int argc, char** argv) {
                wb, (4.0 * (1 << wb)) / 1048576.0, t[0], t[1], t[2], t[3], t[4], t[5]);
     }
     {
+        uint32_t *k2, *v2;
+        CK(cudaMalloc(&k2, m * 4));
+        CK(cudaMalloc(&v2, m * 4));
+        const uint2* in = reinterpret_cast<const uint2*>(dst);  // m/2 pairs: reuse 2 buffers as 8 B input
+        const size_t mm = m / 2;
+        printf("digit runs (8 B in, 4+4 B out) of %zu keys: tile 2048 %.3f | 4096 %.3f | 8192 %.3f | 16384 %.3f ms\n", mm,
+               timeit([&] { runs<2048><<<(unsigned)(mm / 2048), 256>>>(in, k2, v2, mm); }),
+               timeit([&] { runs<4096><<<(unsigned)(mm / 4096), 256>>>(in, k2, v2, mm); }),
+               timeit([&] { runs<8192><<<(unsigned)(mm / 8192), 256>>>(in, k2, v2, mm); }),
+               timeit([&] { runs<16384><<<(unsigned)(mm / 16384), 256>>>(in, k2, v2, mm); }));
+        printf("copy of the same bytes (8 B in, 8 B out): %.3f ms\n",
+               timeit([&] { copyk<<<148 * 16, 256>>>(s, o, m); }));
         make_li<<<2048, 256>>>(li, m, 15);
         CK(cudaFuncSetAttribute(smem_win<15>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << 15));
         printf("smem window 2^15 (val 4 B + idx 2 B in, 4 B out): %.3f ms\n",
