@@ -30,6 +30,7 @@ sys.path.insert(0, ROOT)
 METRIC = "elements/sec and % HBM roofline, LAPLEX fwd+bwd n=2^30, 1/2/4/8 B200 vs CPU ref"
 UNIT = "elements/s"
 SPEC_PEAK_GBS = 8000.0  # B200 HBM3e spec (report beside the measured copy peak)
+REUSE_X, SAVE_X = 4, 8  # include/laplex_c.h flags
 
 # BASELINE.json configs: shape, the timed work unit and
 # what counts as an "element".
@@ -766,11 +767,15 @@ def run_e2e(args, torch, lib, c):
             rc = lib.laplex_gram_apply(hp, h["X"].data_ptr(), B, k, o["Y"].data_ptr())
             assert rc == 0, lib.laplex_last_error()
         else:
-            rc = lib.laplex_apply(hp, flags, h["X"].data_ptr(), B, k, o["Y"].data_ptr())
+            # fwd+bwd: the apply keeps its sorted x (LAPLEX_SAVE_X) and the
+            # backward of the same host X reuses it (LAPLEX_REUSE_X): x crosses
+            # PCIe once; results are bitwise those of separate calls
+            fb = kind != "fwd"
+            rc = lib.laplex_apply(hp, flags | (SAVE_X if fb else 0), h["X"].data_ptr(), B, k, o["Y"].data_ptr())
             assert rc == 0, lib.laplex_last_error()
-            if kind != "fwd":
-                rc = lib.laplex_backward(hp, flags, h["X"].data_ptr(), B, k, h["G"].data_ptr(), n, P("xb"),
-                                         P("ab"), P("bb"), P("pb"), P("qb"))
+            if fb:
+                rc = lib.laplex_backward(hp, flags | REUSE_X, h["X"].data_ptr(), B, k, h["G"].data_ptr(), n,
+                                         P("xb"), P("ab"), P("bb"), P("pb"), P("qb"))
                 assert rc == 0, lib.laplex_last_error()
         lib.laplex_plan_release(hp)
 
@@ -782,13 +787,13 @@ def run_e2e(args, torch, lib, c):
         times.append(time.perf_counter() - t0)
     sec = statistics.median(times)
     # bytes crossing PCIe per step: every input once per call that takes it
-    uploads = {"fwd": ["a", "b", "X"], "fwdbwd": ["a", "b", "X", "X", "G"],
-               "phased": ["a", "b", "phi", "psi", "X", "X", "G"], "gram": ["a", "b", "X"]}[kind]
+    uploads = {"fwd": ["a", "b", "X"], "fwdbwd": ["a", "b", "X", "G"],
+               "phased": ["a", "b", "phi", "psi", "X", "G"], "gram": ["a", "b", "X"]}[kind]
     h2d = sum(h[key].numel() * 4 for key in uploads)
     d2h = sum(v.numel() * 4 for v in o.values())
-    calls = {"fwd": "laplex_plan_create + laplex_apply", "fwdbwd": "laplex_plan_create + laplex_apply + "
-             "laplex_backward", "phased": "laplex_plan_create(phases) + laplex_apply(PHASED) + "
-             "laplex_backward(PHASED)", "gram": "laplex_plan_create + laplex_gram_apply"}[kind]
+    calls = {"fwd": "laplex_plan_create + laplex_apply", "fwdbwd": "laplex_plan_create + laplex_apply(SAVE_X) + "
+             "laplex_backward(REUSE_X)", "phased": "laplex_plan_create(phases) + laplex_apply(PHASED|SAVE_X) + "
+             "laplex_backward(PHASED|REUSE_X)", "gram": "laplex_plan_create + laplex_gram_apply"}[kind]
     return {"value": units_of(c) / sec, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "ms_per_step": 1000 * sec,
             "path": f"{calls} (host pointers, pinned torch buffers; inputs checked for finiteness in the "

@@ -843,16 +843,16 @@ lx::ms::MainArgs<R> main_args(const View<R>& v, int rows) {
 // overheads per element; measured best at 2^30); the phased kernels carry
 // twice the channels and keep 256 x 8.  The transpose and the backward share
 // a shape, so x_bar of the VJP is bitwise the transpose.
-template <bool BWD, bool PHASED>
+template <bool GCH, bool PHASED>  // GCH: the kernel carries g channels (transpose, backward)
 struct MainShape {
-    static constexpr int TPB = PHASED ? 256 : (BWD ? LX_BWD_TPB : LX_FWD_TPB);
+    static constexpr int TPB = PHASED ? 256 : (GCH ? LX_BWD_TPB : LX_FWD_TPB);
     static constexpr int IPT = lx::ms::kTile / TPB;
 };
 
 template <class R, int NG, int NX, bool BWD, bool SEQ = false>
 void launch_main(const char* name, const lx::ms::MainArgs<R>& a, cudaStream_t st) {
     using namespace lx::ms;
-    constexpr int TPB = MainShape<BWD, (NG == 2 || NX == 2)>::TPB, IPT = MainShape<BWD, (NG == 2 || NX == 2)>::IPT;
+    constexpr int TPB = MainShape<(NG > 0), (NG == 2 || NX == 2)>::TPB, IPT = MainShape<(NG > 0), (NG == 2 || NX == 2)>::IPT;
     auto kern = lx_main<R, NG, NX, BWD, SEQ, TPB, IPT>;
     constexpr bool os_smem = LX_OS_SMEM && BWD && NG != 2 && sizeof(R) == 4;
     const size_t smem = sizeof(MainShared<R, NG + NX, TPB / 32, BWD ? (NG == 2 ? 2 : 1) : 0, os_smem ? kTile : 0>);

@@ -483,6 +483,11 @@ __global__ void __launch_bounds__(kAggThreads) lx_gather_agg(GatherAggArgs<R> g)
         for (int j = 0; j < NT; ++j)
 #pragma unroll
             for (int c = 0; c < NCH; ++c) pi[j][c] = ps[j][c] = qi[j][c] = qs[j][c] = R(0);
+        // row / range base pointers: 32-bit element offsets below
+        const R* __restrict__ srow = src + (size_t)r * g.ld_src;
+        R* __restrict__ orow = out + (size_t)r * g.ld_out + s0;
+        const R* __restrict__ Vs = V + s0;
+        const uint32_t* __restrict__ ixs = idx ? idx + s0 : nullptr;
         for (int base = 0; base < ns; base += kSpan) {  // one round unless the side dominates
             // all loads of the thread's (up to) kGI elements are issued before use
             uint32_t ix[kGI];
@@ -490,25 +495,30 @@ __global__ void __launch_bounds__(kAggThreads) lx_gather_agg(GatherAggArgs<R> g)
 #pragma unroll
             for (int q = 0; q < kGI; ++q) {
                 const int i = base + tid + q * kAggThreads;
-                const uint32_t e = s0 + (uint32_t)i;
-                ix[q] = i < ns ? (idx ? idx[e] : e) : 0u;
-                sv[q] = i < ns ? V[e] : R(0);
+                ix[q] = i < ns ? (ixs ? ixs[i] : s0 + (uint32_t)i) : 0u;
+                sv[q] = i < ns ? Vs[i] : R(0);
             }
 #pragma unroll
             for (int q = 0; q < kGI; ++q) {
                 const int i = base + tid + q * kAggThreads;
-                v[q] = i < ns ? src[(size_t)r * g.ld_src + ix[q]] : R(0);
+                v[q] = i < ns ? srow[ix[q]] : R(0);
             }
 #pragma unroll
             for (int q = 0; q < kGI; ++q) {
                 const int i = base + tid + q * kAggThreads;
                 if (i >= ns) continue;
                 const uint32_t e = s0 + (uint32_t)i;
-                out[(size_t)r * g.ld_out + e] = v[q];
+                orow[i] = v[q];
                 const R s = sv[q];
+                // the element's tile: one branch target per tile (static
+                // accumulator registers, one exp pair per element; the tile of
+                // an element is uniform across a warp except at tile edges)
+                int jj = 0;
+#pragma unroll
+                for (int j = 1; j < NT; ++j) jj += e >= sb[j];
 #pragma unroll
                 for (int j = 0; j < NT; ++j) {
-                    if (e < sb[j] || e >= sb[j + 1]) continue;  // element of tile t0 + j
+                    if (j != jj) continue;  // element of tile t0 + j
                     const R S_first = Sf[j], S_last = Sl[j];
                     const R e1 = xexp(xsub(s, S_last)), e2 = xexp(xsub(S_first, s));
                     R pay[NCH];

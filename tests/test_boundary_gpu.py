@@ -195,3 +195,30 @@ def test_saved_forward_x_reuse_is_bitwise(torch, phased, n):
     want3 = dop.backward(X2, G)
     for w, gg in zip(want3, got3):
         assert (w is None and gg is None) or torch.equal(w, gg)
+
+
+@pytest.mark.parametrize("phased,n", [(False, 6000), (True, 5000), (False, (1 << 21) + 5)])
+def test_host_api_saved_x_reuse_is_bitwise(torch, phased, n):
+    """Host-pointer API: laplex_apply(SAVE_X) + laplex_backward(REUSE_X) of the
+    same host X skips the second upload of x and gives bitwise the results of
+    a plain backward; a different host X is uploaded and recomputed."""
+    from paper_2605_24584_b200 import laplex as LX
+    rng = np.random.default_rng(n)
+    k = n + 17
+    a, b = rng.uniform(-30, 30, n).astype(np.float32), rng.uniform(-30, 30, k).astype(np.float32)
+    ph = (rng.uniform(0, 6, n).astype(np.float32), rng.uniform(0, 6, k).astype(np.float32)) if phased else (None, None)
+    X = rng.uniform(-1, 1, (2, k)).astype(np.float32)
+    X2 = rng.uniform(-1, 1, (2, k)).astype(np.float32)
+    G = rng.uniform(-1, 1, (2, n)).astype(np.float32)
+    op = L.LaplexOperator(a, b, 1.0, *ph, dtype=np.float32)
+    base = LX.PHASED if phased else 0
+    want = LX._vjp(op, X, G, base)
+    op._apply(base | LX.SAVE_X, X, 2, k, n)
+    fields = ("x_bar", "a_bar", "b_bar", "phi_bar", "psi_bar")
+    got = LX._vjp(op, X, G, base | LX.REUSE_X)
+    for f in fields:
+        assert np.array_equal(getattr(want, f), getattr(got, f)), f
+    op._apply(base | LX.SAVE_X, X2, 2, k, n)
+    got2 = LX._vjp(op, X, G, base | LX.REUSE_X)  # not the saved host x: uploaded again
+    for f in fields:
+        assert np.array_equal(getattr(want, f), getattr(got2, f)), f
