@@ -523,10 +523,12 @@ void radix_sort(const R* raw, uint32_t m, R t, R* vals_out, uint32_t* perm_out, 
     const size_t hsmem = (size_t)kHistSub * P * kRadix * sizeof(uint32_t);
     if (kSortRts) {  // pass 1's per-tile counts (and the finiteness check) in one read of the keys;
                      // the digit bases of every pass come from the scans' totals
-        const uint32_t g0 = (tiles + kHistTilesPerCta - 1) / kHistTilesPerCta;
+        const uint32_t tpc = std::max<uint32_t>(
+            1u, std::min<uint32_t>(kHistTilesPerCta, tiles / (uint32_t)(num_sms() * 4)));
+        const uint32_t g0 = (tiles + tpc - 1) / tpc;
         launch("lx_sort_hist", st, [&] {
             lx_sort_hist_count0<R, false><<<g0, kThreads, 0, st>>>(raw, m, t, hist.as<uint32_t>(), bad,
-                                                                   cnt.as<uint32_t>(), tiles);
+                                                                   cnt.as<uint32_t>(), tiles, tpc);
         });
     } else {
         launch("lx_sort_hist", st, [&] {

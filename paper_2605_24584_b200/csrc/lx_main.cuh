@@ -70,6 +70,7 @@ struct MainShared {
     // accumulated over the batch rows by the element's owning thread
     R acc[NACC > 0 ? NACC : 1][kTile];
     R wsl[NW], wsf[NW];                 // warp last / first anchors (per tile)
+    R cr[2][4][NC];                     // tile carries of batch rows >= 1 (prefetched a row ahead)
     R pv[NC][NW], pw[NC][NW];           // warp prefix totals (inclusive, strict)
     R qv[NC][NW], qw[NC][NW];           // warp suffix totals
 };
@@ -368,6 +369,31 @@ __global__ void __launch_bounds__(TPB + 32, main_min_blocks<R, BWD, TPB>()) lx_m
 
         for (int r = 0; r < rows; ++r) {
             mbar_wait(&S.barp, (use * (uint32_t)rows + (uint32_t)r) & 1u);
+            // phased kernels: the next batch row's tile carries are copied
+            // global -> shared asynchronously now and read after barrier (A)
+            // of that row (row 0's come with the producer's staging; C3 bwd
+            // 5.43 -> 4.71 ms).  The unphased kernels load them at use: the
+            // prefetch's registers cost the single-row C5 kernels more than
+            // it saves the batched C2 ones.
+            constexpr bool PF = PHASED;
+            const bool pf = PF && r + 1 < rows && tid < 4 * NC;
+            if (pf) {
+                const int c = tid % NC, kind = tid / NC;  // kind: prefix, strict prefix, suffix, strict suffix
+                const bool strict = kind & 1;
+                const size_t sl = ((size_t)(2 * c + (strict ? 1 : 0)) * rows + r + 1);
+                const bool ok = (kind < 2 ? t > 0 : t + 1 < T) && (!strict || (kind < 2 ? C::pst(c) : C::qst(c)));
+                R* d = &sm.cr[(r + 1) & 1][kind][c];
+                if (ok) {
+                    const R* src = kind < 2 ? p.cp + sl * T + t - 1 : p.cq + sl * T + t + 1;
+                    if constexpr (sizeof(R) == 4)
+                        cp_async4(d, src);
+                    else
+                        cp_async8(d, src);
+                } else {
+                    *d = R(0);
+                }
+                asm volatile("cp.async.commit_group;" ::: "memory");
+            }
             // ---- payloads: modulated channel values of each element ----
             R pay[NP][IPT];
             R raw[PHASED ? IPT : 1];
@@ -475,7 +501,13 @@ __global__ void __launch_bounds__(TPB + 32, main_min_blocks<R, BWD, TPB>()) lx_m
                     sm.qw[c][warp] = wq[c];
                 }
             }
-            cbar<TPB>();  // (A) warp totals; every merge of this tile is done
+            if (PF && r > 0 && tid < 4 * NC) {  // this row's prefetched carries have landed
+                if (pf)
+                    asm volatile("cp.async.wait_group 1;" ::: "memory");
+                else
+                    asm volatile("cp.async.wait_group 0;" ::: "memory");
+            }
+            cbar<TPB>();  // (A) warp totals; every merge of this tile is done; row carries in shared memory
             if (tid == 0 && r + 1 < rows) {  // next batch row's payloads into this stage
                 const R* srcA = SEQ ? p.Xs : p.Gs;
                 const size_t ldA = SEQ ? p.ldxs : p.ldgs;
@@ -565,6 +597,11 @@ __global__ void __launch_bounds__(TPB + 32, main_min_blocks<R, BWD, TPB>()) lx_m
                     cps[c] = S.c0[1][c];
                     cqv[c] = S.c0[2][c];
                     cqs[c] = S.c0[3][c];
+                } else if constexpr (PF) {
+                    cpv[c] = sm.cr[r & 1][0][c];
+                    cps[c] = sm.cr[r & 1][1][c];
+                    cqv[c] = sm.cr[r & 1][2][c];
+                    cqs[c] = sm.cr[r & 1][3][c];
                 } else {
                     cpv[c] = t > 0 ? p.cp[sl0 * T + t - 1] : R(0);
                     cps[c] = (t > 0 && C::pst(c)) ? p.cp[sl1 * T + t - 1] : R(0);

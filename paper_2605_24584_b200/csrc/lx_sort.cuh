@@ -100,8 +100,9 @@ __global__ void __launch_bounds__(kHistThreads) lx_sort_hist(const R* __restrict
 
 // Reduce-then-scan form of the histogram: the same single read of the raw
 // keys also yields pass 1's per-tile digit counts (its tiles are the raw
-// order), so pass 1 needs no count kernel.  kHistTilesPerCta consecutive pass
-// tiles per CTA keep the global-histogram atomics few.
+// order), so pass 1 needs no count kernel.  Up to kHistTilesPerCta consecutive
+// pass tiles per CTA keep the global-histogram atomics few; small inputs take
+// fewer per CTA so that every SM gets work (2^20 keys: 256 tiles).
 #ifndef LX_HIST_TILES
 #define LX_HIST_TILES 64
 #endif
@@ -112,7 +113,8 @@ constexpr int kHistTilesPerCta = LX_HIST_TILES;
 template <class R, bool HIST = true>
 __global__ void __launch_bounds__(kThreads) lx_sort_hist_count0(const R* __restrict__ raw, size_t n, R t,
                                                                uint32_t* __restrict__ hist, int* __restrict__ bad,
-                                                               uint32_t* __restrict__ cnt, uint32_t tiles) {
+                                                               uint32_t* __restrict__ cnt, uint32_t tiles,
+                                                               uint32_t tiles_per_cta) {
     using K = typename Traits<R>::Key;
     constexpr int P = Traits<R>::kPasses;
     constexpr int SUB = 4;
@@ -124,8 +126,8 @@ __global__ void __launch_bounds__(kThreads) lx_sort_hist_count0(const R* __restr
     __syncthreads();
     uint32_t* mine = &gh[warp % SUB][0][0];
     int any_bad = 0;
-    const uint32_t t_lo = blockIdx.x * kHistTilesPerCta;
-    const uint32_t t_hi = min(tiles, t_lo + kHistTilesPerCta);
+    const uint32_t t_lo = blockIdx.x * tiles_per_cta;
+    const uint32_t t_hi = min(tiles, t_lo + tiles_per_cta);
     for (uint32_t tile = t_lo; tile < t_hi; ++tile) {
         const size_t base = (size_t)tile * kTile;
         R v[kItems];
