@@ -101,18 +101,20 @@ def kernel_model_bytes(name, c):
         "cos_sin": 12 * m2 if phased else 0,
         "lx_partition": 4 * (T + 1),
         "lx_tiledesc": (T + 1) * 32,
-        "lx_group_plan": 6 * m2,                            # output positions in, u16 store order out
+        # output positions and anchors in; u16 store order and the merge words (4 B per 16 merged) out
+        "lx_group_plan": 10 * m2 + T * 512,
         "lx_iota": 4 * n,
         # x once (the backward reuses the forward's sorted x), g in the backward
         "lx_perm_gather": 12 * ((B * k if is_staged(k) else 0) + ((B if kind in ("fwdbwd", "phased") else 0) * n
                                                                 if is_staged(n) else 0)),
         "lx_gather_agg": 16 * (B * k + pay_rows * n) + 8 * m2 * (ch - 1),
         "lx_carry": 2 * 2 * 4 * ch * max(B, 1) * T * 4,
-        "lx_main_fwd": 4 * m2 + B * 4 * k + 6 * n + B * 4 * n,
-        "lx_main_fwd_phased": 4 * m2 + 16 * m2 + B * 4 * k + 6 * n + B * 4 * n,
-        "lx_main_trn": 4 * m2 + B * 4 * n + 6 * k + B * 4 * k,
-        "lx_main_bwd": 4 * m2 + B * (4 * n + 4 * k) + 6 * m2 + B * 4 * k + 4 * n + 4 * k,
-        "lx_main_bwd_phased": 4 * m2 + 16 * m2 + B * (4 * n + 4 * k) + 6 * m2 + B * 4 * k + 8 * n + 8 * k,
+        # (+ the tile's merge words, 512 B per 2048 merged elements, T * 512)
+        "lx_main_fwd": 4 * m2 + B * 4 * k + 6 * n + B * 4 * n + T * 512,
+        "lx_main_fwd_phased": 4 * m2 + 16 * m2 + B * 4 * k + 6 * n + B * 4 * n + T * 512,
+        "lx_main_trn": 4 * m2 + B * 4 * n + 6 * k + B * 4 * k + T * 512,
+        "lx_main_bwd": 4 * m2 + B * (4 * n + 4 * k) + 6 * m2 + B * 4 * k + 4 * n + 4 * k + T * 512,
+        "lx_main_bwd_phased": 4 * m2 + 16 * m2 + B * (4 * n + 4 * k) + 6 * m2 + B * 4 * k + 8 * n + 8 * k + T * 512,
         "lx_perm_scatter": 12 * ((out_rows * n if is_staged(n) else 0) + (out_cols * k if is_staged(k) else 0)),
     }
     v = model.get(name)
