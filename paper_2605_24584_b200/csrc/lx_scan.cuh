@@ -69,15 +69,41 @@ __device__ __forceinline__ I merge_path(const R* a, I na, const R* b, I nb, I di
     return lo;
 }
 
+// Merge path restricted to A indices [lo, hi) (the answer must lie there).
+template <bool AFIRST, class R, class I>
+__device__ __forceinline__ I merge_path_in(const R* a, const R* b, I diag, I lo, I hi) {
+    while (lo < hi) {
+        const I mid = (lo + hi) >> 1;
+        const bool take = AFIRST ? (a[mid] <= b[diag - 1 - mid]) : (a[mid] < b[diag - 1 - mid]);
+        if (take)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// Two-level: the first and last boundary of a block's 256 tiles are searched
+// over the whole sequence, then every boundary between them inside that
+// bracket (merge path is monotone in the diagonal), so most probes are short
+// and hit data the block already touched.  blockDim.x == 256.
 template <class R, bool AFIRST>
 __global__ void lx_partition(const R* __restrict__ A, uint32_t n, const R* __restrict__ B, uint32_t k,
                              uint32_t* __restrict__ part, uint32_t T) {
-    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    using I = unsigned long long;
+    __shared__ I bracket[2];
+    const I total = (I)n + k;
+    auto diag_of = [&](uint32_t t) { return min((I)t * kTile, total); };
+    const uint32_t t0 = blockIdx.x * blockDim.x;
+    const uint32_t tl = min(t0 + blockDim.x - 1, T);
+    if (threadIdx.x < 2) bracket[threadIdx.x] = merge_path<AFIRST, R, I>(A, n, B, k, diag_of(threadIdx.x ? tl : t0));
+    __syncthreads();
+    const uint32_t t = t0 + threadIdx.x;
     if (t > T) return;
-    const unsigned long long total = (unsigned long long)n + k;
-    unsigned long long diag = (unsigned long long)t * kTile;
-    if (diag > total) diag = total;
-    part[t] = (uint32_t)merge_path<AFIRST, R, unsigned long long>(A, n, B, k, diag);
+    const I diag = diag_of(t);
+    const I lo = max(bracket[0], diag > k ? diag - k : (I)0);
+    const I hi = min(bracket[1], min(diag, (I)n));
+    part[t] = (uint32_t)merge_path_in<AFIRST, R, I>(A, B, diag, lo, hi);
 }
 
 // Per-tile descriptor, built once per plan orientation: the tile's row/col

@@ -1,0 +1,5 @@
+for v in part it12 it20; do
+  LAPLEX_LIB=$PWD/variants/lib_$v.so timeout 300 python tools/sort_bench.py 30 $v >> gpurun_out/r37_sort.txt 2>&1
+done
+LAPLEX_LIB=$PWD/variants/lib_part.so timeout 900 python -m pytest tests/test_parity_gpu.py tests/test_scale_gpu.py -x -q 2>&1 | tail -3 > gpurun_out/r37_tests.txt
+cat gpurun_out/r37_sort.txt gpurun_out/r37_tests.txt
