@@ -82,7 +82,8 @@ def kernel_model_bytes(name, c):
     big = 0
     staged = [m for m in (n, k) if is_staged(m)]
     T = (m2 + 2047) // 2048
-    tiles = (n + 4095) // 4096 + (k + 4095) // 4096
+    ST = 6144  # radix-sort tile (lx_sort.cuh kTile: 256 threads x 24 keys)
+    tiles = (n + ST - 1) // ST + (k + ST - 1) // ST
     phased = kind == "phased"
     # payload arrays per step, by side: (rows side element count, cols side)
     pay_rows = {"fwd": 0, "fwdbwd": B, "phased": B, "gram": B}[kind]  # g (bwd) / z (gram)
@@ -93,9 +94,9 @@ def kernel_model_bytes(name, c):
         "lx_sort_hist": 4 * m2 + 2 * 4 * 256 * 4,         # keys once; 4 digit histograms per side
         "lx_sort_bases": 2 * 2 * 4 * 256 * 4,
         "lx_sort_count": 3 * 4 * m2 + 3 * tiles * 1024,  # passes 2-4: keys in, per-tile digit counts out
-        "lx_sort_scan": 4 * tiles * 2048 + sum((m + 4095) // 4096 for m in staged) * 2048,
+        "lx_sort_scan": 4 * tiles * 2048 + sum((m + ST - 1) // ST for m in staged) * 2048,
         "lx_sort_pass": (12 + 16 + 16 + 16) * m2,          # pass 1: r4 w8; passes 2-4: r8 w8
-        "lx_splan_count": sum(4 * m + (m + 4095) // 4096 * 1024 for m in staged),
+        "lx_splan_count": sum(4 * m + (m + ST - 1) // ST * 1024 for m in staged),
         "lx_splan": sum(12 * m for m in staged),            # perm in; pos (sequential), dst (bucket streams) out
         "lx_gather_sorted": 8 * m2 if phased else 0,        # phases into sorted order
         "cos_sin": 12 * m2 if phased else 0,

@@ -31,11 +31,14 @@ constexpr int kBits = 8;
 constexpr int kRadix = 256;
 constexpr int kThreads = 256;  // == kRadix: one look-back lane per digit
 constexpr int kWarps = kThreads / 32;
+// keys per thread: 24 measured best at 2^30 (sort + counts + plan pass: 16:
+// 65.3 ms, 20: 62.4, 24: 60.8, 28: 62.1, 32: 63.1) -- larger tiles shrink the
+// per-tile count tables and overheads until registers spill
 #ifndef LX_SORT_ITEMS
-#define LX_SORT_ITEMS 16
+#define LX_SORT_ITEMS 24
 #endif
 constexpr int kItems = LX_SORT_ITEMS;
-constexpr int kTile = kThreads * kItems;  // 4096 keys per tile
+constexpr int kTile = kThreads * kItems;  // 6144 keys per tile
 
 // look-back status word: [63:62] flag (1 aggregate, 2 inclusive prefix),
 // [61:32] pass epoch, [31:0] count
@@ -274,11 +277,12 @@ struct PassSmem {
     alignas(16) uint32_t iv[kTile];
 };
 
-// CTAs per SM the 32-bit-key pass is built for (64 registers, ~42 KB of shared
-// memory; 4 measured 2% faster than 3 at 2^30).  A persistent double-buffered
-// form (next tile's TMA in flight during ranking) measured 7% slower.
+// CTAs per SM the 32-bit-key pass is built for: 3 (80 registers, ~58 KB of
+// shared memory with 24 keys per thread; at 16 keys, 4 CTAs at 64 registers
+// measured 2% faster than 3).  A persistent double-buffered form (next tile's
+// TMA in flight during ranking) measured 7% slower.
 #ifndef LX_SORT_CTAS
-#define LX_SORT_CTAS 4
+#define LX_SORT_CTAS 3
 #endif
 template <class R>
 constexpr int sort_min_blocks() { return sizeof(typename Traits<R>::Key) == 4 ? LX_SORT_CTAS : 2; }

@@ -30,7 +30,7 @@ def instance(rng, n, k, span=5.0, ties=True):
 
 # ---------------------------------------------------------------- sort
 @pytest.mark.parametrize("dt", [F64, F32])
-@pytest.mark.parametrize("m", [1, 2, 3, 31, 4095, 4096, 4097, 8193, 100_003])
+@pytest.mark.parametrize("m", [1, 2, 3, 31, 4095, 4096, 4097, 6143, 6144, 6145, 12289, 100_003])
 def test_sort_bit_exact(dt, m):
     rng = np.random.default_rng(m)
     raw = rng.uniform(-3, 3, m).astype(dt)

@@ -4,7 +4,7 @@ phased forward/backward, Gram-vector, sort and scan (tools/sanitize_driver,
 torch-free).  lx_main is a persistent, warp-specialised mbarrier pipeline and
 lx_sort_pass / lx_gather_agg use shared-memory staging: these tools are what
 proves the barriers and shared-memory hand-offs are race-free.  Sizes cover a
-multi-tile plan (merge tiles of 2048, sort tiles of 4096) and, for memcheck,
+multi-tile plan (merge tiles of 2048, sort tiles of 6144) and, for memcheck,
 the two-pass permutation plans (sides > 2^22)."""
 import os
 import shutil
