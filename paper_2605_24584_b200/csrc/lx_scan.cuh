@@ -468,10 +468,17 @@ struct GatherAggArgs {
 #ifndef LX_AGG_TILES
 #define LX_AGG_TILES 4
 #endif
+// resident CTAs per SM the register budget targets for the two-channel
+// (phased) pass, which is latency-bound at 3 (C3: 3.54 -> 2.52 ms at 4); the
+// one-channel pass keeps its 74-register, 3-CTA form (a 64-register budget
+// spilled and measured 1% slower at 2^30)
+#ifndef LX_AGG_CTAS
+#define LX_AGG_CTAS 4
+#endif
 constexpr int kAggTiles = LX_AGG_TILES;
 
 template <class R, int NCH, bool SIDE_A, bool GFORM, bool STRICT>
-__global__ void __launch_bounds__(kAggThreads) lx_gather_agg(GatherAggArgs<R> g) {
+__global__ void __launch_bounds__(kAggThreads, NCH == 2 ? LX_AGG_CTAS : 3) lx_gather_agg(GatherAggArgs<R> g) {
     constexpr int NW = kAggThreads / 32;
     constexpr int NT = kAggTiles;
     constexpr int kGI = kTile * NT / 2 / kAggThreads;  // slots for ~the side's share of NT tiles
@@ -518,16 +525,21 @@ __global__ void __launch_bounds__(kAggThreads) lx_gather_agg(GatherAggArgs<R> g)
             // all loads of the thread's (up to) kGI elements are issued before use
             uint32_t ix[kGI];
             R v[kGI], sv[kGI];
+            // two channels: the anchors (not on the gather's dependency
+            // chain) are loaded with the gathers, so the plan positions and the
+            // anchors are never live at the same time (registers -> 4 CTAs/SM)
+            constexpr bool LATE_V = NCH == 2;
 #pragma unroll
             for (int q = 0; q < kGI; ++q) {
                 const int i = base + tid + q * kAggThreads;
                 ix[q] = i < ns ? (ixs ? ixs[i] : s0 + (uint32_t)i) : 0u;
-                sv[q] = i < ns ? Vs[i] : R(0);
+                if (!LATE_V) sv[q] = i < ns ? Vs[i] : R(0);
             }
 #pragma unroll
             for (int q = 0; q < kGI; ++q) {
                 const int i = base + tid + q * kAggThreads;
                 v[q] = i < ns ? srow[ix[q]] : R(0);
+                if (LATE_V) sv[q] = i < ns ? Vs[i] : R(0);
             }
 #pragma unroll
             for (int q = 0; q < kGI; ++q) {
