@@ -661,7 +661,7 @@ template <class R>
 DBuf stage_gather(const R* src, size_t ld, const uint32_t* dst, uint32_t m, int rows, cudaStream_t st) {
     DBuf out((size_t)rows * m * sizeof(R), st);
     using namespace lx::sort;
-    const uint32_t chunks = (m + kPermChunk - 1) / kPermChunk;
+    const uint32_t chunks = (m + kGatherChunk - 1) / kGatherChunk;
     launch("lx_perm_gather", st, [&] {
         lx_perm_stage_gather<R><<<dim3(chunks, rows), kPermThreads, 0, st>>>(src, ld, dst, m, out.as<R>());
     });
@@ -682,7 +682,7 @@ thread_local OutHook* g_out_hook = nullptr;
 template <class R>
 void stage_scatter_one(const uint32_t* dst, uint32_t m, const R* s1, R* o1, size_t ld1, int rows1, cudaStream_t st) {
     using namespace lx::sort;
-    const uint32_t chunks = (m + kPermChunk - 1) / kPermChunk;
+    const uint32_t chunks = (m + kScatterChunk - 1) / kScatterChunk;
     if (!g_out_hook) {
         launch("lx_perm_scatter", st, [&] {
             lx_perm_stage_scatter<R><<<dim3(chunks, rows1), kPermThreads, 0, st>>>(dst, m, s1, o1, ld1, rows1, nullptr,
@@ -699,7 +699,7 @@ void stage_scatter_one(const uint32_t* dst, uint32_t m, const R* s1, R* o1, size
         const uint64_t u0 = ((uint64_t)(gi * W / G)) << shift;
         const uint64_t u1 = std::min<uint64_t>(((uint64_t)((gi + 1) * W / G)) << shift, m);
         if (u1 <= u0) continue;
-        const uint32_t b0 = (uint32_t)(u0 / kPermChunk), b1 = (uint32_t)((u1 + kPermChunk - 1) / kPermChunk);
+        const uint32_t b0 = (uint32_t)(u0 / kScatterChunk), b1 = (uint32_t)((u1 + kScatterChunk - 1) / kScatterChunk);
         launch("lx_perm_scatter", st, [&] {
             lx_perm_stage_scatter<R><<<dim3(b1 - b0, rows1), kPermThreads, 0, st>>>(dst, m, s1, o1, ld1, rows1,
                                                                                   nullptr, nullptr, nullptr, nullptr,
