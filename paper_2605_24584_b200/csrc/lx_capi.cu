@@ -679,13 +679,14 @@ thread_local OutHook* g_out_hook = nullptr;
 // One launch per output array: with two arrays in one pass the random writes of
 // both windows thrash L2 (measured at 2^30: 17.5 ms for x_bar + b_bar together
 // vs 7.2 ms for one array, with ~60% DRAM read/write amplification).
-template <class R>
-void stage_scatter_one(const uint32_t* dst, uint32_t m, const R* s1, R* o1, size_t ld1, int rows1, cudaStream_t st) {
+template <class R, int ITEMS>
+void stage_scatter_one_t(const uint32_t* dst, uint32_t m, const R* s1, R* o1, size_t ld1, int rows1, cudaStream_t st) {
     using namespace lx::sort;
-    const uint32_t chunks = (m + kScatterChunk - 1) / kScatterChunk;
+    constexpr uint32_t kChunk = kPermThreads * ITEMS;
+    const uint32_t chunks = (m + kChunk - 1) / kChunk;
     if (!g_out_hook) {
         launch("lx_perm_scatter", st, [&] {
-            lx_perm_stage_scatter<R><<<dim3(chunks, rows1), kPermThreads, 0, st>>>(dst, m, s1, o1, ld1, rows1, nullptr,
+            lx_perm_stage_scatter<R, ITEMS><<<dim3(chunks, rows1), kPermThreads, 0, st>>>(dst, m, s1, o1, ld1, rows1, nullptr,
                                                                                  nullptr, nullptr, nullptr, 0u);
         });
         return;
@@ -699,14 +700,22 @@ void stage_scatter_one(const uint32_t* dst, uint32_t m, const R* s1, R* o1, size
         const uint64_t u0 = ((uint64_t)(gi * W / G)) << shift;
         const uint64_t u1 = std::min<uint64_t>(((uint64_t)((gi + 1) * W / G)) << shift, m);
         if (u1 <= u0) continue;
-        const uint32_t b0 = (uint32_t)(u0 / kScatterChunk), b1 = (uint32_t)((u1 + kScatterChunk - 1) / kScatterChunk);
+        const uint32_t b0 = (uint32_t)(u0 / kChunk), b1 = (uint32_t)((u1 + kChunk - 1) / kChunk);
         launch("lx_perm_scatter", st, [&] {
-            lx_perm_stage_scatter<R><<<dim3(b1 - b0, rows1), kPermThreads, 0, st>>>(dst, m, s1, o1, ld1, rows1,
+            lx_perm_stage_scatter<R, ITEMS><<<dim3(b1 - b0, rows1), kPermThreads, 0, st>>>(dst, m, s1, o1, ld1, rows1,
                                                                                   nullptr, nullptr, nullptr, nullptr,
                                                                                   b0);
         });
         g_out_hook->fn(o1, u0, u1, rows1, ld1, st);
     }
+}
+
+template <class R>
+void stage_scatter_one(const uint32_t* dst, uint32_t m, const R* s1, R* o1, size_t ld1, int rows1, cudaStream_t st) {
+    if (rows1 == 1)
+        stage_scatter_one_t<R, lx::sort::kScatterItemsRow>(dst, m, s1, o1, ld1, rows1, st);
+    else
+        stage_scatter_one_t<R, lx::sort::kScatterItemsBatch>(dst, m, s1, o1, ld1, rows1, st);
 }
 
 template <class R>

@@ -823,29 +823,33 @@ __global__ void __launch_bounds__(TPB + 32, main_min_blocks<R, BWD, TPB>()) lx_m
                     }
                 } else {
                     R* xb = p.xbar + (size_t)r * p.ldxb;
-                    for (int k = tid; k < nb; k += TPB) {
-                        const int li = gmB[k];
-                        xb[LXO(iB[li], g.b0 + li)] = stg[li];
+                    if (r + 1 < rows) {
+                        for (int k = tid; k < nb; k += TPB) {
+                            const int li = gmB[k];
+                            xb[LXO(iB[li], g.b0 + li)] = stg[li];
+                        }
+                    } else {  // last row: the column cotangents (summed over rows in 4b) are complete
+                        for (int k = tid; k < nb; k += TPB) {
+                            const int li = gmB[k];
+                            const uint32_t u = LXO(iB[li], g.b0 + li);
+                            xb[u] = stg[li];
+                            p.bbar[u] = sm.acc[0][na + li];
+                            if constexpr (PHASED) p.psibar[u] = sm.acc[NACC - 1][na + li];
+                        }
                     }
                 }
             }
             fence_proxy_async_smem();  // staging writes before any TMA refill of this stage
             cbar<TPB>();  // (C) staging row and warp totals free for the next row / tile
         }
-        if constexpr (BWD) {  // anchor cotangents summed over rows (complete after (C))
+        if constexpr (BWD) {  // row cotangents summed over rows (complete after (C)); the
+                              // column ones went out with the last row's x_bar
             const uint32_t* iA = S.oidx + g.offIA;
-            const uint32_t* iB = S.oidx + g.baseIB;
             for (int k = tid; k < na; k += TPB) {
                 const int li = gmA[k];
                 const uint32_t u = LXO(iA[li], g.a0 + li);
                 p.abar[u] = sm.acc[0][li];
                 if constexpr (PHASED) p.phibar[u] = sm.acc[NACC - 1][li];
-            }
-            for (int k = tid; k < nb; k += TPB) {
-                const int li = gmB[k];
-                const uint32_t u = LXO(iB[li], g.b0 + li);
-                p.bbar[u] = sm.acc[0][na + li];
-                if constexpr (PHASED) p.psibar[u] = sm.acc[NACC - 1][na + li];
             }
             cbar<TPB>();
         }

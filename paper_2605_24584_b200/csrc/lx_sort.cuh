@@ -106,10 +106,11 @@ __global__ void __launch_bounds__(kHistThreads) lx_sort_hist(const R* __restrict
 // Reduce-then-scan form of the histogram: the same single read of the raw
 // keys also yields pass 1's per-tile digit counts (its tiles are the raw
 // order), so pass 1 needs no count kernel.  Up to kHistTilesPerCta consecutive
-// pass tiles per CTA keep the global-histogram atomics few; small inputs take
-// fewer per CTA so that every SM gets work (2^20 keys: 256 tiles).
+// pass tiles per CTA (8 measured best at 2^30: 1 -> 2.37 ms, 8 -> 2.11, 64 ->
+// 2.32 for both sides); small inputs take fewer per CTA so that every SM gets
+// work (2^20 keys: 171 tiles).
 #ifndef LX_HIST_TILES
-#define LX_HIST_TILES 64
+#define LX_HIST_TILES 8
 #endif
 constexpr int kHistTilesPerCta = LX_HIST_TILES;
 
@@ -636,19 +637,19 @@ __global__ void __launch_bounds__(kScanThreads) lx_sort_scan(uint32_t* __restric
 // random side of each pass stays inside an L2-resident window.
 constexpr int kPermThreads = 256;
 // items per thread: the gather half keeps more independent random reads in
-// flight (16), the scatter half issues fewer random writes per thread (4);
-// measured at 2^30 against 8 for both: gather 4.69 -> 4.58 ms, scatter 7.73
-// -> 7.45 ms per launch
+// flight (16: 4.69 -> 4.58 ms per 2^30 launch against 8).  The scatter half
+// writes at random inside one caller window, and the entries in flight across
+// the GPU (resident threads x items) decide how many windows are live in L2 at
+// once: a single row takes 1 item per thread (7.73 ms at 8 -> 7.45 at 4 ->
+// 7.02 at 2 -> 6.95 at 1 per 2^30 launch); batched calls, whose grid walks
+// the rows, take 4 (C2: 11.2 ms at 4, 12.1 at 2).
 #ifndef LX_PERM_GATHER_ITEMS
 #define LX_PERM_GATHER_ITEMS 16
 #endif
-#ifndef LX_PERM_SCATTER_ITEMS
-#define LX_PERM_SCATTER_ITEMS 4
-#endif
 constexpr int kGatherItems = LX_PERM_GATHER_ITEMS;
 constexpr int kGatherChunk = kPermThreads * kGatherItems;
-constexpr int kScatterItems = LX_PERM_SCATTER_ITEMS;
-constexpr int kScatterChunk = kPermThreads * kScatterItems;
+constexpr int kScatterItemsRow = 1;    // single-row scatters
+constexpr int kScatterItemsBatch = 4;  // batched scatters
 
 // gather (caller order -> sorted order), first half: stage[r][q] = src[r][dst[q]];
 // the consumer then reads stage[r][pos[i]].  grid: (chunks, rows)
@@ -683,35 +684,35 @@ __global__ void __launch_bounds__(kPermThreads) lx_perm_stage_gather(const R* __
 // writes in flight stay inside one row's caller window (a CTA looping over 64
 // rows kept 64 windows -- 1 GB at n = 2^24 -- live in the 126 MB L2 and ran at
 // a third of the single-row rate).  dst is re-read per row (+4 B/element-row).
-template <class R>
+template <class R, int ITEMS>
 __global__ void __launch_bounds__(kPermThreads) lx_perm_stage_scatter(const uint32_t* __restrict__ dst, uint32_t m,
                                                                      const R* __restrict__ s1, R* __restrict__ o1,
                                                                      size_t ld1, int rows1, const R* __restrict__ s2,
                                                                      R* __restrict__ o2, const R* __restrict__ s3,
                                                                      R* __restrict__ o3, uint32_t block0) {
-    const size_t q0 = (size_t)(blockIdx.x + block0) * kScatterChunk + threadIdx.x;
+    const size_t q0 = (size_t)(blockIdx.x + block0) * (kPermThreads * ITEMS) + threadIdx.x;
     const size_t r = blockIdx.y;
-    uint32_t u[kScatterItems];
+    uint32_t u[ITEMS];
 #pragma unroll
-    for (int j = 0; j < kScatterItems; ++j) {
+    for (int j = 0; j < ITEMS; ++j) {
         const size_t q = q0 + (size_t)j * kPermThreads;
         u[j] = q < m ? dst[q] : 0u;
     }
-    R v[kScatterItems];  // all loads in flight before the random stores
+    R v[ITEMS];  // all loads in flight before the random stores
 #pragma unroll
-    for (int j = 0; j < kScatterItems; ++j) {
+    for (int j = 0; j < ITEMS; ++j) {
         const size_t q = q0 + (size_t)j * kPermThreads;
         v[j] = q < m ? s1[r * m + q] : R(0);
     }
 #pragma unroll
-    for (int j = 0; j < kScatterItems; ++j) {
+    for (int j = 0; j < ITEMS; ++j) {
         const size_t q = q0 + (size_t)j * kPermThreads;
         if (q < m) o1[r * ld1 + u[j]] = v[j];
     }
     (void)rows1;
     if (r == 0) {
 #pragma unroll
-        for (int j = 0; j < kScatterItems; ++j) {
+        for (int j = 0; j < ITEMS; ++j) {
             const size_t q = q0 + (size_t)j * kPermThreads;
             if (q < m) {
                 if (s2) o2[u[j]] = s2[q];
