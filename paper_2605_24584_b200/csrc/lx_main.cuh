@@ -197,8 +197,10 @@ constexpr int main_min_blocks() {
 // Channel layout: g channels first (c < NG), then x channels.  Strict prefix
 // variants for g channels and strict suffix variants for x channels, in the
 // backward (BWD) configuration only.  SEQ: one x channel carried by rows.
-template <class R, int NG, int NX, bool BWD, bool SEQ, int TPB, int IPT>
-__global__ void __launch_bounds__(TPB + 32, main_min_blocks<R, BWD, TPB>()) lx_main(MainArgs<R> p) {
+// MB: CTAs per SM the register budget targets, 0 = main_min_blocks (the
+// batched unphased backward runs a 3-CTA instantiation, see launch_main)
+template <class R, int NG, int NX, bool BWD, bool SEQ, int TPB, int IPT, int MB = 0>
+__global__ void __launch_bounds__(TPB + 32, MB ? MB : main_min_blocks<R, BWD, TPB>()) lx_main(MainArgs<R> p) {
     static_assert(TPB * IPT == kTile, "a CTA covers one merge tile");
     constexpr int NW = TPB / 32;
     static_assert(NW <= 32 && (NW & (NW - 1)) == 0, "warps per CTA: power of two");
