@@ -281,7 +281,7 @@ struct Core {
     std::mutex mu;
     DBuf part[2];  // merge-path tiles with side 0 (resp. 1) as the "A" operand, A-first
     DBuf desc[2], sfirst[2], slast[2];  // per-tile descriptors and edge anchors
-    DBuf gmap[2][2];  // per orientation: store order of the A / B side in every tile (lx_group_plan)
+    DBuf gmt[2];      // per orientation: store order of both sides, one kTile slot per tile (lx_group_plan)
     DBuf mwd[2];      // per orientation: merge words of every tile (lx_group_plan)
     uint32_t T[2] = {0, 0};
     DBuf ranks[4];  // [side*2 + strict]
@@ -311,7 +311,7 @@ struct Core {
         for (Side& sd : side)
             for (DBuf* b : {&sd.vals, &sd.perm, &sd.cph, &sd.sph, &sd.spos, &sd.sdst}) f(*b);
         for (int o = 0; o < 2; ++o)
-            for (DBuf* b : {&part[o], &desc[o], &sfirst[o], &slast[o], &gmap[o][0], &gmap[o][1], &mwd[o]}) f(*b);
+            for (DBuf* b : {&part[o], &desc[o], &sfirst[o], &slast[o], &gmt[o], &mwd[o]}) f(*b);
         for (DBuf& b : ranks) f(b);
         f(saved.xs), f(saved.aggp), f(saved.aggq);
     }
@@ -376,7 +376,7 @@ struct View {
     uint32_t T;
     R inv_t;
     const uint32_t *pos_a, *dst_a, *pos_b, *dst_b;  // null = direct permutation
-    const uint16_t *gm_a, *gm_b;                      // per-tile store order (lx_group_plan)
+    const uint16_t* gmt;                              // per-tile store order (lx_group_plan)
     const uint32_t* mw;                               // per-tile merge words (lx_group_plan)
 };
 
@@ -412,16 +412,14 @@ void build_partition(Core& c, int which, cudaStream_t st) {
     // per-tile store order of both sides (output positions: plan pos or perm)
     const uint32_t* pa = a.staged ? a.spos.as<uint32_t>() : a.perm.as<uint32_t>();
     const uint32_t* pb = b.staged ? b.spos.as<uint32_t>() : b.perm.as<uint32_t>();
-    c.gmap[which][0] = DBuf(((size_t)a.m + 16) * 2, st);
-    c.gmap[which][1] = DBuf(((size_t)b.m + 16) * 2, st);
+    c.gmt[which] = DBuf((size_t)T * lx::ms::kTile * 2 + 16, st);
     const size_t gsm = lx::ms::group_plan_smem<R>();
     smem_attr(lx::ms::lx_group_plan<R>, gsm);
     if (T)
         launch("lx_group_plan", st, [&] {
             lx::ms::lx_group_plan<R><<<T, lx::ms::kGroupBuckets, gsm, st>>>(
                 c.desc[which].as<lx::ms::TileDesc<R>>(), T, pa, bucket_shift(a.m), pb, bucket_shift(b.m),
-                c.gmap[which][0].as<uint16_t>(), c.gmap[which][1].as<uint16_t>(), a.vals.as<R>(), b.vals.as<R>(),
-                c.mwd[which].as<uint32_t>());
+                c.gmt[which].as<uint16_t>(), a.vals.as<R>(), b.vals.as<R>(), c.mwd[which].as<uint32_t>());
         });
 }
 
@@ -486,8 +484,7 @@ View<R> view(Core& c, bool swapped, cudaStream_t st, size_t rows = 1) {
     v.dst_a = use[ia] ? a.sdst.as<uint32_t>() : nullptr;
     v.pos_b = use[1 - ia] ? b.spos.as<uint32_t>() : nullptr;
     v.dst_b = use[1 - ia] ? b.sdst.as<uint32_t>() : nullptr;
-    v.gm_a = c.gmap[ia][0].as<uint16_t>();
-    v.gm_b = c.gmap[ia][1].as<uint16_t>();
+    v.gmt = c.gmt[ia].as<uint16_t>();
     v.mw = c.mwd[ia].as<uint32_t>();
     return v;
 }
@@ -844,8 +841,7 @@ lx::ms::MainArgs<R> main_args(const View<R>& v, int rows) {
     a.cpsi = v.cpsi;
     a.spsi = v.spsi;
     a.inv_t = v.inv_t;
-    a.gmap_a = v.gm_a;
-    a.gmap_b = v.gm_b;
+    a.gmt = v.gmt;
     return a;
 }
 
@@ -882,6 +878,8 @@ void launch_main_mb(const char* name, const lx::ms::MainArgs<R>& a, cudaStream_t
 // (128 registers, some spills) for batches, where every tile walks many rows
 // and the extra warps hide more latency than the spills cost (C2 backward
 // 14.9 -> 13.8 ms; C5 20.7 -> 24.2 ms with 3).  Same arithmetic either way.
+// (The forward / transpose gain nothing from it: C2 forward 5.9 -> 7.6 ms at
+// 4 CTAs, 8.2 at 2.)
 template <class R, int NG, int NX, bool BWD, bool SEQ = false>
 void launch_main(const char* name, const lx::ms::MainArgs<R>& a, cudaStream_t st) {
     if constexpr (BWD && NG == 1 && NX == 1 && sizeof(R) == 4) {
@@ -890,6 +888,7 @@ void launch_main(const char* name, const lx::ms::MainArgs<R>& a, cudaStream_t st
             return;
         }
     }
+
     launch_main_mb<R, NG, NX, BWD, SEQ, 0>(name, a, st);
 }
 

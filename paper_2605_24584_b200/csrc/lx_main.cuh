@@ -51,7 +51,7 @@ struct MainStage {
     alignas(16) R anch[kTile + 8 * kPad];
     alignas(16) R pay[kTile + 8 * kPad];  // row payloads, same layout
     alignas(16) uint32_t oidx[kTile + 16];  // output index ranges: A at [offIA], B at [baseIB + offIB]
-    alignas(16) uint16_t gm[kTile + 32];    // store order (lx_group_plan): A at [offGA], B at [baseGB]
+    alignas(16) uint16_t gm[kTile];         // store order (lx_group_plan): rows at [0, na), cols at [na, len)
     alignas(16) uint32_t mw[kMergeWords];   // the tile's merge words (lx_merge_words)
 };
 
@@ -80,9 +80,9 @@ template <class R>
 struct TileGeom {
     uint32_t a0, b0;
     int na, nb;
-    int offA, baseB, offIA, baseIB, offGA, baseGB;  // element offsets inside anch/pay, oidx, gm
-    uint32_t bytesA, bytesB, ibytesA, ibytesB, gbytesA, gbytesB;
-    uint32_t a0al, b0al, a0i, b0i, a0g, b0g;
+    int offA, baseB, offIA, baseIB;  // element offsets inside anch/pay, oidx
+    uint32_t bytesA, bytesB, ibytesA, ibytesB, gbytes;
+    uint32_t a0al, b0al, a0i, b0i;
     __device__ __forceinline__ void init(uint32_t a0_, uint32_t b0_, int na_, int nb_, bool outA, bool outB) {
         constexpr int kPad = 16 / sizeof(R);
         a0 = a0_;
@@ -103,13 +103,8 @@ struct TileGeom {
         ibytesA = (outA && na) ? (uint32_t)(((offIA + na + 3) / 4) * 16) : 0u;
         ibytesB = (outB && nb) ? (uint32_t)(((offIB + nb + 3) / 4) * 16) : 0u;
         baseIB = (int)(ibytesA / 4) + offIB;
-        a0g = a0 & ~7u;  // u16 store order: 8-element alignment
-        b0g = b0 & ~7u;
-        offGA = (int)(a0 - a0g);
-        const int offGB = (int)(b0 - b0g);
-        gbytesA = (outA && na) ? (uint32_t)(((offGA + na + 7) / 8) * 16) : 0u;
-        gbytesB = (outB && nb) ? (uint32_t)(((offGB + nb + 7) / 8) * 16) : 0u;
-        baseGB = (int)(gbytesA / 2) + offGB;
+        // the tile's store-order slot (16-byte aligned): rows then cols
+        gbytes = (outA || outB) ? (uint32_t)(((na + nb + 7) / 8) * 16) : 0u;
     }
 };
 
@@ -143,14 +138,13 @@ __device__ __forceinline__ void issue_tile(MainStage<R, NC>& S, const MainArgs<R
     S.SL = SL;
     S.SR = dn.s_first;
     constexpr uint32_t kMW = SEQ ? 0u : (uint32_t)(kMergeWords * 4);
-    mbar_expect_tx(&S.bar, g.bytesA + g.bytesB + g.ibytesA + g.ibytesB + g.gbytesA + g.gbytesB + kMW);
+    mbar_expect_tx(&S.bar, g.bytesA + g.bytesB + g.ibytesA + g.ibytesB + g.gbytes + kMW);
     if (kMW) bulk_g2s(S.mw, p.mwords + (size_t)t * kMergeWords, kMW, &S.bar);
     if (g.bytesA) bulk_g2s(S.anch, p.A + g.a0al, g.bytesA, &S.bar);
     if (g.bytesB) bulk_g2s(S.anch + (g.bytesA / sizeof(R)) + MainStage<R, NC>::kPad, p.B + g.b0al, g.bytesB, &S.bar);
     if (g.ibytesA) bulk_g2s(S.oidx, p.perm_a + g.a0i, g.ibytesA, &S.bar);
     if (g.ibytesB) bulk_g2s(S.oidx + g.ibytesA / 4, p.perm_b + g.b0i, g.ibytesB, &S.bar);
-    if (g.gbytesA) bulk_g2s(S.gm, p.gmap_a + g.a0g, g.gbytesA, &S.bar);
-    if (g.gbytesB) bulk_g2s(S.gm + g.gbytesA / 2, p.gmap_b + g.b0g, g.gbytesB, &S.bar);
+    if (g.gbytes) bulk_g2s(S.gm, p.gmt + (size_t)t * kTile, g.gbytes, &S.bar);
     const R* srcA = SEQ ? p.Xs : p.Gs;
     mbar_expect_tx(&S.barp, (PAY_A ? g.bytesA : 0u) + (PAY_B ? g.bytesB : 0u));
     if (PAY_A && g.bytesA) bulk_g2s(S.pay, srcA + g.a0al, g.bytesA, &S.barp);
@@ -296,8 +290,8 @@ __global__ void __launch_bounds__(TPB + 32, MB ? MB : main_min_blocks<R, BWD, TP
         const R* pB = S.pay + g.baseB;
         const uint32_t* iA = S.oidx + g.offIA;
         const uint32_t* iB = S.oidx + g.baseIB;
-        const uint16_t* gmA = S.gm + g.offGA;  // store order of the tile rows / cols
-        const uint16_t* gmB = S.gm + g.baseGB;
+        const uint16_t* gmA = S.gm;  // store order of the tile rows / cols
+        const uint16_t* gmB = S.gm + na;
 
         // ---- this thread's IPT merged elements: kinds from the plan's merge
         // words, anchors by independent shared-memory loads ----

@@ -216,10 +216,9 @@ struct MainArgs {
     const uint32_t* perm_b;
     const uint32_t* part;  // T+1 row offsets of the merged tiles
     uint32_t* tile_ctr;    // zeroed tile counter (lx_main's in-order tile schedule)
-    // per-tile store order (lx_group_plan): gmap_a[a0 + k] = row-local index of
-    // the k-th tile row in output-bucket order (likewise gmap_b for cols)
-    const uint16_t* gmap_a;
-    const uint16_t* gmap_b;
+    // per-tile store order (lx_group_plan): gmt[t * kTile + k] = row-local index
+    // of the k-th tile row in output-bucket order (k < na), then the cols
+    const uint16_t* gmt;
     const TileDesc<R>* desc;  // T+1 tile descriptors
     const uint32_t* mwords;   // lx_merge_words: kMergeWords per tile (null: single-sequence SEQ pass)
     uint32_t n, k, T;
@@ -349,60 +348,73 @@ __device__ __forceinline__ void group_tile(uint16_t (&gmap)[2][kTile], uint32_t 
 // Plan-time per-tile data consumed by lx_main, built once per plan orientation
 // (it depends only on the plan): the store order of both sides (grouping by
 // output bucket) and the tile's merge words (see lx_merge_words).
+// Shared memory of lx_group_plan: both sides' output positions and anchors
+// arrive by TMA (each range at a 16-byte aligned-down start), the store order
+// is built in one per-tile array [rows | cols] and leaves with 16-byte stores.
+template <class R>
+struct GroupSmem {
+    static constexpr int kPadU = 4, kPadR = 16 / sizeof(R);
+    unsigned long long bar;
+    uint32_t gcnt[2][kGroupBuckets];
+    uint32_t gwarp[2][kGroupBuckets / 32];
+    alignas(16) uint32_t sA[kTile + 2 * kPadU], sB[kTile + 2 * kPadU];
+    alignas(16) R mA[kTile + 2 * kPadR], mB[kTile + 2 * kPadR];  // + room for the +inf sentinels
+    alignas(16) uint16_t gm[kTile];
+};
 template <class R>
 constexpr size_t group_plan_smem() {
-    return sizeof(uint32_t) * 2 * kTile + sizeof(uint16_t) * 2 * kTile + sizeof(uint32_t) * 2 * kGroupBuckets +
-           sizeof(uint32_t) * 2 * (kGroupBuckets / 32) + sizeof(R) * (kTile + 2) + 16;
+    return sizeof(GroupSmem<R>);
 }
 
+// Per merge tile: the merge words and the store order of both sides.  The
+// store order lives in a per-tile slot gm[t * kTile + e]: the tile's rows at
+// e < na (row-local indices ranked by output bucket), its cols at na + k.
 template <class R>
 __global__ void __launch_bounds__(kGroupBuckets) lx_group_plan(const TileDesc<R>* __restrict__ desc, uint32_t T,
                                                                const uint32_t* __restrict__ posA, int shA,
                                                                const uint32_t* __restrict__ posB, int shB,
-                                                               uint16_t* __restrict__ gA, uint16_t* __restrict__ gB,
-                                                               const R* __restrict__ A, const R* __restrict__ B,
-                                                               uint32_t* __restrict__ words) {
+                                                               uint16_t* __restrict__ gmt, const R* __restrict__ A,
+                                                               const R* __restrict__ B, uint32_t* __restrict__ words) {
     constexpr int TPB = kGroupBuckets, NW = TPB / 32;
     static_assert(TPB == kThreads, "one merge thread per grouping thread");
-    struct Smem {
-        uint32_t sA[kTile], sB[kTile];
-        uint16_t gmap[2][kTile];
-        uint32_t gcnt[2][kGroupBuckets];
-        uint32_t gwarp[2][NW];
-        R anc[kTile + 2];
-    };
-    extern __shared__ __align__(16) unsigned char smem_group[];  // dynamic: > 48 KB for large tiles
-    Smem& sm = *reinterpret_cast<Smem*>(smem_group);
-    uint32_t* sA = sm.sA;
-    uint32_t* sB = sm.sB;
-    auto& gmap = sm.gmap;
-    auto& gcnt = sm.gcnt;
-    auto& gwarp = sm.gwarp;
-    const int tid = threadIdx.x;
+    using SM = GroupSmem<R>;
+    extern __shared__ __align__(16) unsigned char smem_group[];  // dynamic: > 48 KB
+    SM& sm = *reinterpret_cast<SM*>(smem_group);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t t = blockIdx.x;
     const TileDesc<R> dt = desc[t], dn = desc[t + 1];
     const uint32_t a0 = dt.a0, b0 = dt.b0;
-    const int na = (int)(dn.a0 - a0), nb = (int)(dn.b0 - b0);
-    R* mA = sm.anc;
-    R* mB = sm.anc + na + 1;
-    for (int i = tid; i < na; i += TPB) {
-        sA[i] = posA[a0 + i];
-        mA[i] = A[a0 + i];
+    const int na = (int)(dn.a0 - a0), nb = (int)(dn.b0 - b0), len = na + nb;
+    // 16-byte aligned-down starts of the four ranges
+    const int oPA = (int)(a0 & (SM::kPadU - 1)), oPB = (int)(b0 & (SM::kPadU - 1));
+    const int oMA = (int)(a0 & (SM::kPadR - 1)), oMB = (int)(b0 & (SM::kPadR - 1));
+    auto rb = [](int off, int cnt, int esz) { return cnt ? (uint32_t)(((off + cnt) * esz + 15) & ~15) : 0u; };
+    const uint32_t bPA = rb(oPA, na, 4), bPB = rb(oPB, nb, 4);
+    const uint32_t bMA = rb(oMA, na, (int)sizeof(R)), bMB = rb(oMB, nb, (int)sizeof(R));
+    if (tid == 0) {
+        mbar_init(&sm.bar, 1);
+        fence_mbar_init();
+        mbar_expect_tx(&sm.bar, bPA + bPB + bMA + bMB);
+        if (bPA) bulk_g2s(sm.sA, posA + (a0 - oPA), bPA, &sm.bar);
+        if (bPB) bulk_g2s(sm.sB, posB + (b0 - oPB), bPB, &sm.bar);
+        if (bMA) bulk_g2s(sm.mA, A + (a0 - oMA), bMA, &sm.bar);
+        if (bMB) bulk_g2s(sm.mB, B + (b0 - oMB), bMB, &sm.bar);
     }
-    for (int i = tid; i < nb; i += TPB) {
-        sB[i] = posB[b0 + i];
-        mB[i] = B[b0 + i];
-    }
+    sm.gcnt[0][tid] = 0u;
+    sm.gcnt[1][tid] = 0u;
+    __syncthreads();  // barrier initialised before anyone waits on it
+    mbar_wait(&sm.bar, 0);
+    const uint32_t* sA = sm.sA + oPA;
+    const uint32_t* sB = sm.sB + oPB;
+    R* mA = sm.mA + oMA;
+    R* mB = sm.mB + oMB;
     if (tid == 0) {  // +inf behind both ranges: the merge reads past an exhausted side
         const R inf = R(__int_as_float(0x7f800000));
         mA[na] = inf;
         mB[nb] = inf;
     }
-    gcnt[0][tid] = 0u;
-    gcnt[1][tid] = 0u;
     __syncthreads();
     {   // merge words (rows first on ties), kItems merged elements per thread
-        const int len = na + nb;
         const int dd = min(tid * kItems, len);
         const int nval = min(kItems, len - dd);
         int ia = merge_path<true, R, int>(mA, na, mB, nb, dd), ib = dd - ia;
@@ -420,9 +432,43 @@ __global__ void __launch_bounds__(kGroupBuckets) lx_group_plan(const TileDesc<R>
         const uint32_t hi = __shfl_down_sync(FULL, m, 1);
         if ((tid & 1) == 0) words[(size_t)t * kMergeWords + tid / 2] = m | (hi << kItems) | ((uint32_t)ia0 << 16);
     }
-    group_tile<TPB, NW, true, true, 0>(gmap, gcnt, gwarp, sA, na, shA, sB, nb, shB, tid);
-    for (int k = tid; k < na; k += TPB) gA[a0 + k] = gmap[0][k];
-    for (int k = tid; k < nb; k += TPB) gB[b0 + k] = gmap[1][k];
+    // store order: counting sort of each side's elements by output bucket
+    for (int li = tid; li < na; li += TPB) atomicAdd(&sm.gcnt[0][sA[li] >> shA], 1u);
+    for (int li = tid; li < nb; li += TPB) atomicAdd(&sm.gcnt[1][sB[li] >> shB], 1u);
+    __syncthreads();
+    {
+        const uint32_t c0 = sm.gcnt[0][tid], c1 = sm.gcnt[1][tid];
+        uint32_t x0 = c0, x1 = c1;  // inclusive warp scans
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y0 = __shfl_up_sync(FULL, x0, o), y1 = __shfl_up_sync(FULL, x1, o);
+            if (lane >= o) {
+                x0 += y0;
+                x1 += y1;
+            }
+        }
+        if (lane == 31) {
+            sm.gwarp[0][warp] = x0;
+            sm.gwarp[1][warp] = x1;
+        }
+        __syncthreads();
+        uint32_t w0 = 0, w1 = (uint32_t)na;  // the cols follow the rows in the tile's slot
+#pragma unroll
+        for (int w = 0; w < NW; ++w)
+            if (w < warp) {
+                w0 += sm.gwarp[0][w];
+                w1 += sm.gwarp[1][w];
+            }
+        sm.gcnt[0][tid] = w0 + x0 - c0;  // exclusive offsets
+        sm.gcnt[1][tid] = w1 + x1 - c1;
+    }
+    __syncthreads();
+    for (int li = tid; li < na; li += TPB) sm.gm[atomicAdd(&sm.gcnt[0][sA[li] >> shA], 1u)] = (uint16_t)li;
+    for (int li = tid; li < nb; li += TPB) sm.gm[atomicAdd(&sm.gcnt[1][sB[li] >> shB], 1u)] = (uint16_t)li;
+    __syncthreads();
+    // the whole slot, 8 entries per 16-byte store (entries past len are don't-care)
+    for (int v = tid; v * 8 < len; v += TPB)
+        reinterpret_cast<uint4*>(gmt + (size_t)t * kTile)[v] = reinterpret_cast<const uint4*>(sm.gm)[v];
 }
 
 // ---------------------------------------------------------------------------
