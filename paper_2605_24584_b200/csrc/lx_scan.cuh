@@ -554,6 +554,26 @@ __global__ void __launch_bounds__(kAggThreads, NCH == 2 ? LX_AGG_CTAS : 3) lx_ga
     const R* __restrict__ V = g.V;
     R* __restrict__ out = g.out;
     __shared__ R red[NT][4 * NCH][NW];
+    // The plan positions of the CTA's range arrive by one TMA bulk copy (16-byte
+    // aligned-down start), so the gathers depend on a shared load instead of
+    // a per-thread global load, and batch rows reuse them.
+    constexpr int kIdxCap = NT * kTile + 8;
+    __shared__ alignas(16) uint32_t six[kIdxCap];
+    __shared__ unsigned long long ibar;
+    const int oI = (int)(s0 & 3u);
+    const bool tma_idx = idx != nullptr && ns > 0;
+    if (tma_idx) {
+        if (tid == 0) {
+            mbar_init(&ibar, 1);
+            fence_mbar_init();
+            const uint32_t bytes = (uint32_t)(((oI + ns) * 4 + 15) & ~15);
+            mbar_expect_tx(&ibar, bytes);
+            bulk_g2s(six, idx + (s0 - (uint32_t)oI), bytes, &ibar);
+        }
+        __syncthreads();  // barrier initialised before anyone waits on it
+        mbar_wait(&ibar, 0);
+    }
+    const uint32_t* __restrict__ sx = six + oI;
     // batch rows are split over blockIdx.y (row groups of g.rows_per_cta)
     const int r_lo = (int)blockIdx.y * g.rows_per_cta, r_hi = min(g.rows, r_lo + g.rows_per_cta);
     for (int r = r_lo; r < r_hi; ++r) {
@@ -566,26 +586,15 @@ __global__ void __launch_bounds__(kAggThreads, NCH == 2 ? LX_AGG_CTAS : 3) lx_ga
         const R* __restrict__ srow = src + (size_t)r * g.ld_src;
         R* __restrict__ orow = out + (size_t)r * g.ld_out + s0;
         const R* __restrict__ Vs = V + s0;
-        const uint32_t* __restrict__ ixs = idx ? idx + s0 : nullptr;
         for (int base = 0; base < ns; base += kSpan) {  // one round unless the side dominates
             // all loads of the thread's (up to) kGI elements are issued before use
-            uint32_t ix[kGI];
             R v[kGI], sv[kGI];
-            // two channels: the anchors (not on the gather's dependency
-            // chain) are loaded with the gathers, so the plan positions and the
-            // anchors are never live at the same time (registers -> 4 CTAs/SM)
-            constexpr bool LATE_V = NCH == 2;
 #pragma unroll
             for (int q = 0; q < kGI; ++q) {
                 const int i = base + tid + q * kAggThreads;
-                ix[q] = i < ns ? (ixs ? ixs[i] : s0 + (uint32_t)i) : 0u;
-                if (!LATE_V) sv[q] = i < ns ? Vs[i] : R(0);
-            }
-#pragma unroll
-            for (int q = 0; q < kGI; ++q) {
-                const int i = base + tid + q * kAggThreads;
-                v[q] = i < ns ? srow[ix[q]] : R(0);
-                if (LATE_V) sv[q] = i < ns ? Vs[i] : R(0);
+                const uint32_t x = i < ns ? (tma_idx ? sx[i] : s0 + (uint32_t)i) : 0u;
+                v[q] = i < ns ? srow[x] : R(0);
+                sv[q] = i < ns ? Vs[i] : R(0);
             }
 #pragma unroll
             for (int q = 0; q < kGI; ++q) {
