@@ -48,5 +48,28 @@ lib.laplex_plan_create(0, ha.data_ptr(), n, hb.data_ptr(), k, 1.0, None, None, C
 print("apply ms", tm(lambda: lib.laplex_apply(h, 0, hx.data_ptr(), 1, k, hy.data_ptr())))
 print("backward ms", tm(lambda: lib.laplex_backward(h, 0, hx.data_ptr(), 1, k, hg.data_ptr(), n, hxb.data_ptr(),
                                                    hab.data_ptr(), hbb.data_ptr(), None, None)))
+
+
+def fwd_bwd_reuse():  # the bench's e2e pair: apply(SAVE_X) + backward(REUSE_X)
+    lib.laplex_apply(h, 8, hx.data_ptr(), 1, k, hy.data_ptr())
+    lib.laplex_backward(h, 4, hx.data_ptr(), 1, k, hg.data_ptr(), n, hxb.data_ptr(), hab.data_ptr(), hbb.data_ptr(),
+                        None, None)
+
+
+print("apply(SAVE_X)+backward(REUSE_X) ms", tm(fwd_bwd_reuse))
+s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+d2 = torch.empty(n, device="cuda")
+
+
+def duplex():  # H2D and D2H at once on two streams
+    with torch.cuda.stream(s1):
+        d.copy_(ha, non_blocking=True)
+    with torch.cuda.stream(s2):
+        hy.copy_(d2, non_blocking=True)
+    s1.synchronize()
+    s2.synchronize()
+
+
+print("h2d || d2h 4 B x n each ms", tm(duplex))
 import os
 print("cpus", os.cpu_count())
