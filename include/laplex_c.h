@@ -57,13 +57,16 @@ extern "C" {
 /* apply / backward / gram flags */
 #define LAPLEX_TRANSPOSE 1u /* apply: y = A^T g (matvec_transpose) */
 #define LAPLEX_PHASED 2u    /* phased_matvec / phased_matvec_vjp / phased_gram */
-/* laplex_apply_dev: keep the forward's sorted x (and its tile aggregates) in
+/* laplex_apply[_dev]: keep the forward's sorted x (and its tile aggregates) in
  * the plan for the backward -- the autograd "save for backward" of x; one x
- * per plan, replaced by the next save, released when consumed. */
+ * per plan, replaced by the next save, released when consumed.  The host-
+ * pointer laplex_apply keys the saved x by the caller's host pointer. */
 #define LAPLEX_SAVE_X 8u
-/* laplex_backward_dev / laplex_sharded_backward_dev: reuse the x saved by the
+/* laplex_backward[_dev] / laplex_sharded_backward_dev: reuse the x saved by the
  * preceding forward (same X pointer, rows and orientation; the caller asserts X
- * is unchanged) instead of gathering it again.  Results are bitwise identical. */
+ * is unchanged) instead of gathering it again -- for the host-pointer
+ * laplex_backward, x is then neither uploaded nor re-checked.  Results are
+ * bitwise identical; a non-matching X is simply gathered (and uploaded). */
 #define LAPLEX_REUSE_X 4u
 
 /* error codes (reference exception types) */
