@@ -2421,10 +2421,15 @@ int laplex_gather_dev(int dtype, const void* src, size_t ld_src, const uint32_t*
         cudaStream_t st = as_stream(stream);
         auto run = [&](auto zero) {
             using R = decltype(zero);
-            launch("lx_gather_idx", st, [&] {
-                lx::shard::lx_gather_idx<R><<<grid_for(m * rows), 256, 0, st>>>((const R*)src, ld_src, idx, m,
-                                                                                 (int)rows, (R*)dst);
-            });
+            using namespace lx::shard;
+            const uint32_t chunks = (uint32_t)((m + kRouteChunk - 1) / kRouteChunk);
+            for (size_t r0 = 0; r0 < rows; r0 += 65535) {  // grid.y limit
+                const uint32_t nr = (uint32_t)std::min<size_t>(65535, rows - r0);
+                launch("lx_gather_idx", st, [&] {
+                    lx_gather_idx<R><<<dim3(chunks, nr), kRouteThreads, 0, st>>>(
+                        (const R*)src + r0 * ld_src, ld_src, idx, m, (R*)dst + r0 * m);
+                });
+            }
         };
         if (dtype == LAPLEX_F64)
             run(0.0);
@@ -2441,10 +2446,15 @@ int laplex_scatter_dev(int dtype, const void* src, const uint32_t* idx, size_t m
         cudaStream_t st = as_stream(stream);
         auto run = [&](auto zero) {
             using R = decltype(zero);
-            launch("lx_scatter_idx", st, [&] {
-                lx::shard::lx_scatter_idx<R><<<grid_for(m * rows), 256, 0, st>>>((const R*)src, idx, m, (int)rows,
-                                                                                  (R*)dst, ld_dst);
-            });
+            using namespace lx::shard;
+            const uint32_t chunks = (uint32_t)((m + kRouteChunk - 1) / kRouteChunk);
+            for (size_t r0 = 0; r0 < rows; r0 += 65535) {  // grid.y limit
+                const uint32_t nr = (uint32_t)std::min<size_t>(65535, rows - r0);
+                launch("lx_scatter_idx", st, [&] {
+                    lx_scatter_idx<R><<<dim3(chunks, nr), kRouteThreads, 0, st>>>(
+                        (const R*)src + r0 * m, idx, m, (R*)dst + r0 * ld_dst, ld_dst);
+                });
+            }
         };
         if (dtype == LAPLEX_F64)
             run(0.0);

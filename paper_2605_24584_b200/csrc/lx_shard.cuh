@@ -180,62 +180,61 @@ __global__ void lx_collect_totals(const R* __restrict__ cp, const R* __restrict_
     }
 }
 
-// Routing by index list (partition order <-> caller order).  Each thread
-// moves kRouteItems elements per round with every index load, then every
-// payload load, issued before use (the index list is a few increasing runs,
-// so both sides are near-sequential streams).
+// Routing by index list (partition order <-> caller order).  The index list
+// of a stable partition is a few increasing runs (one per destination shard),
+// so blocks take contiguous chunks of the partition order in launch order:
+// the runs then advance together through the caller array and every region of
+// it is read (or written) by all runs within a short window -- L2-resident --
+// instead of grid-strided positions spread over the whole array (measured on
+// the simulated 8-rank step at 2^27 per rank: 65 ms -> see DESIGN.md 7).
+// grid: (chunks, rows of this launch)
+constexpr int kRouteThreads = 256;
 constexpr int kRouteItems = 8;
+constexpr int kRouteChunk = kRouteThreads * kRouteItems;
 
 template <class R>
-__global__ void lx_gather_idx(const R* __restrict__ src, size_t ld_src, const uint32_t* __restrict__ idx, size_t m,
-                              int rows, R* __restrict__ dst) {
-    const size_t total = m * rows;
-    const size_t stride = (size_t)gridDim.x * blockDim.x;
-    for (size_t e0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < total; e0 += stride * kRouteItems) {
-        uint32_t u[kRouteItems];
-        size_t rr[kRouteItems];
+__global__ void __launch_bounds__(kRouteThreads) lx_gather_idx(const R* __restrict__ src, size_t ld_src,
+                                                              const uint32_t* __restrict__ idx, size_t m,
+                                                              R* __restrict__ dst) {
+    const size_t r = blockIdx.y;
+    const size_t p0 = (size_t)blockIdx.x * kRouteChunk + threadIdx.x;
+    uint32_t u[kRouteItems];
 #pragma unroll
-        for (int q = 0; q < kRouteItems; ++q) {
-            const size_t e = e0 + (size_t)q * stride;
-            const size_t r = (rows == 1 || e >= total) ? 0 : e / m;  // no 64-bit division for one row
-            const size_t j = e < total ? e - r * m : 0;
-            rr[q] = r;
-            u[q] = e < total ? idx[j] : 0u;
-        }
-        R v[kRouteItems];
+    for (int q = 0; q < kRouteItems; ++q) {
+        const size_t p = p0 + (size_t)q * kRouteThreads;
+        u[q] = p < m ? idx[p] : 0u;
+    }
+    R v[kRouteItems];
 #pragma unroll
-        for (int q = 0; q < kRouteItems; ++q) {
-            const size_t e = e0 + (size_t)q * stride;
-            v[q] = e < total ? src[rr[q] * ld_src + u[q]] : R(0);
-        }
+    for (int q = 0; q < kRouteItems; ++q) {
+        const size_t p = p0 + (size_t)q * kRouteThreads;
+        v[q] = p < m ? src[r * ld_src + u[q]] : R(0);
+    }
 #pragma unroll
-        for (int q = 0; q < kRouteItems; ++q) {
-            const size_t e = e0 + (size_t)q * stride;
-            if (e < total) dst[e] = v[q];
-        }
+    for (int q = 0; q < kRouteItems; ++q) {
+        const size_t p = p0 + (size_t)q * kRouteThreads;
+        if (p < m) dst[r * m + p] = v[q];
     }
 }
 
 template <class R>
-__global__ void lx_scatter_idx(const R* __restrict__ src, const uint32_t* __restrict__ idx, size_t m, int rows,
-                               R* __restrict__ dst, size_t ld_dst) {
-    const size_t total = m * rows;
-    const size_t stride = (size_t)gridDim.x * blockDim.x;
-    for (size_t e0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < total; e0 += stride * kRouteItems) {
-        uint32_t u[kRouteItems];
-        R v[kRouteItems];
+__global__ void __launch_bounds__(kRouteThreads) lx_scatter_idx(const R* __restrict__ src,
+                                                               const uint32_t* __restrict__ idx, size_t m,
+                                                               R* __restrict__ dst, size_t ld_dst) {
+    const size_t r = blockIdx.y;
+    const size_t p0 = (size_t)blockIdx.x * kRouteChunk + threadIdx.x;
+    uint32_t u[kRouteItems];
+    R v[kRouteItems];
 #pragma unroll
-        for (int q = 0; q < kRouteItems; ++q) {
-            const size_t e = e0 + (size_t)q * stride;
-            const size_t j = e >= total ? 0 : (rows == 1 ? e : e % m);
-            u[q] = e < total ? idx[j] : 0u;
-            v[q] = e < total ? src[e] : R(0);
-        }
+    for (int q = 0; q < kRouteItems; ++q) {
+        const size_t p = p0 + (size_t)q * kRouteThreads;
+        u[q] = p < m ? idx[p] : 0u;
+        v[q] = p < m ? src[r * m + p] : R(0);
+    }
 #pragma unroll
-        for (int q = 0; q < kRouteItems; ++q) {
-            const size_t e = e0 + (size_t)q * stride;
-            if (e < total) dst[(rows == 1 ? 0 : e / m) * ld_dst + u[q]] = v[q];
-        }
+    for (int q = 0; q < kRouteItems; ++q) {
+        const size_t p = p0 + (size_t)q * kRouteThreads;
+        if (p < m) dst[r * ld_dst + u[q]] = v[q];
     }
 }
 
