@@ -52,7 +52,7 @@ struct MainStage {
     alignas(16) R pay[kTile + 8 * kPad];  // row payloads, same layout
     alignas(16) uint32_t oidx[kTile + 16];  // output index ranges: A at [offIA], B at [baseIB + offIB]
     alignas(16) uint16_t gm[kTile];         // store order (lx_group_plan): rows at [0, na), cols at [na, len)
-    alignas(16) uint32_t mw[kMergeWords];   // the tile's merge words (lx_merge_words)
+    alignas(16) uint32_t mw[kMergeWords];   // the tile's merge words (lx_group_plan)
 };
 
 #ifndef LX_MAIN_STAGES

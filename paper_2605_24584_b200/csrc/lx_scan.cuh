@@ -220,7 +220,7 @@ struct MainArgs {
     // of the k-th tile row in output-bucket order (k < na), then the cols
     const uint16_t* gmt;
     const TileDesc<R>* desc;  // T+1 tile descriptors
-    const uint32_t* mwords;   // lx_merge_words: kMergeWords per tile (null: single-sequence SEQ pass)
+    const uint32_t* mwords;   // merge words (lx_group_plan): kMergeWords per tile (null: single-sequence SEQ pass)
     uint32_t n, k, T;
     int rows;
     // payloads in SORTED order (lx_gather_agg output), rows x ld (ld % (16/sizeof(R)) == 0)
@@ -283,71 +283,9 @@ __device__ __forceinline__ void cbar() {
     asm volatile("bar.sync 1, %0;" ::"n"(TPB) : "memory");
 }
 
-// barrier of the grouping helpers: BAR 0 = whole CTA, BAR 1 = the TPB consumer threads
-template <int TPB, int BAR>
-__device__ __forceinline__ void gbar() {
-    if constexpr (BAR == 0)
-        __syncthreads();
-    else
-        cbar<TPB>();
-}
-
-// Access grouping (stores of lx_main, loads of lx_gather_agg).  The outputs of a tile go to perm / plan positions that are
-// spread over up to 256 caller-index buckets (2 MB pages apart at 2^30); a
-// warp storing 32 consecutive sorted elements would touch ~32 pages per
-// instruction.  Instead the tile's elements of each side are ranked by bucket
-// (counting sort in shared memory; order inside a bucket is irrelevant since
-// every element carries its exact position), and accesses walk that order:
-// one or two runs per warp instruction.  gcnt must be zero on entry and is
-// zero again on exit.  NS sides (0: rows via idx0, 1: cols via idx1).
-template <int TPB, int NW, bool SA, bool SB, int BAR>
-__device__ __forceinline__ void group_tile(uint16_t (&gmap)[2][kTile], uint32_t (&gcnt)[2][kGroupBuckets],
-                                           uint32_t (&gwarp)[2][NW], const uint32_t* idx0, int n0, int sh0,
-                                           const uint32_t* idx1, int n1, int sh1, int tid) {
-    static_assert(TPB == kGroupBuckets, "one bucket per consumer thread");
-    const int lane = tid & 31, warp = tid >> 5;
-    if (SA)
-        for (int li = tid; li < n0; li += TPB) atomicAdd(&gcnt[0][idx0[li] >> sh0], 1u);
-    if (SB)
-        for (int li = tid; li < n1; li += TPB) atomicAdd(&gcnt[1][idx1[li] >> sh1], 1u);
-    gbar<TPB, BAR>();
-    uint32_t c0 = SA ? gcnt[0][tid] : 0u, c1 = SB ? gcnt[1][tid] : 0u;
-    uint32_t x0 = c0, x1 = c1;  // inclusive warp scans
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y0 = __shfl_up_sync(FULL, x0, o), y1 = __shfl_up_sync(FULL, x1, o);
-        if (lane >= o) {
-            x0 += y0;
-            x1 += y1;
-        }
-    }
-    if (lane == 31) {
-        gwarp[0][warp] = x0;
-        gwarp[1][warp] = x1;
-    }
-    gbar<TPB, BAR>();
-    uint32_t b0 = 0, b1 = 0;
-#pragma unroll
-    for (int w = 0; w < NW; ++w)
-        if (w < warp) {
-            b0 += gwarp[0][w];
-            b1 += gwarp[1][w];
-        }
-    if (SA) gcnt[0][tid] = b0 + x0 - c0;  // exclusive offsets
-    if (SB) gcnt[1][tid] = b1 + x1 - c1;
-    gbar<TPB, BAR>();
-    if (SA)
-        for (int li = tid; li < n0; li += TPB) gmap[0][atomicAdd(&gcnt[0][idx0[li] >> sh0], 1u)] = (uint16_t)li;
-    if (SB)
-        for (int li = tid; li < n1; li += TPB) gmap[1][atomicAdd(&gcnt[1][idx1[li] >> sh1], 1u)] = (uint16_t)li;
-    gbar<TPB, BAR>();
-    if (SA) gcnt[0][tid] = 0u;  // ready for the next tile (read again only after later barriers)
-    if (SB) gcnt[1][tid] = 0u;
-}
-
 // Plan-time per-tile data consumed by lx_main, built once per plan orientation
 // (it depends only on the plan): the store order of both sides (grouping by
-// output bucket) and the tile's merge words (see lx_merge_words).
+// output bucket) and the tile's merge words (see above).
 // Shared memory of lx_group_plan: both sides' output positions and anchors
 // arrive by TMA (each range at a 16-byte aligned-down start), the store order
 // is built in one per-tile array [rows | cols] and leaves with 16-byte stores.
