@@ -459,10 +459,13 @@ struct GatherAggArgs {
 #ifndef LX_AGG_CTAS
 #define LX_AGG_CTAS 4
 #endif
+#ifndef LX_AGG1_CTAS
+#define LX_AGG1_CTAS 3  // 4 (62 registers, no spills) measured slower: C5 14.6 -> 16.7 ms
+#endif
 constexpr int kAggTiles = LX_AGG_TILES;
 
 template <class R, int NCH, bool SIDE_A, bool GFORM, bool STRICT>
-__global__ void __launch_bounds__(kAggThreads, NCH == 2 ? LX_AGG_CTAS : 3) lx_gather_agg(GatherAggArgs<R> g) {
+__global__ void __launch_bounds__(kAggThreads, NCH == 2 ? LX_AGG_CTAS : LX_AGG1_CTAS) lx_gather_agg(GatherAggArgs<R> g) {
     constexpr int NW = kAggThreads / 32;
     constexpr int NT = kAggTiles;
     constexpr int kGI = kTile * NT / 2 / kAggThreads;  // slots for ~the side's share of NT tiles
