@@ -498,8 +498,11 @@ constexpr bool kSortRts = false;
 #else
 constexpr bool kSortRts = true;
 #endif
+// after_hist: enqueued right behind the histogram kernel (whose read of the
+// raw keys sets the finiteness flag)
 template <class R>
-void radix_sort(const R* raw, uint32_t m, R t, R* vals_out, uint32_t* perm_out, int* bad, cudaStream_t st) {
+void radix_sort(const R* raw, uint32_t m, R t, R* vals_out, uint32_t* perm_out, int* bad, cudaStream_t st,
+                const std::function<void()>& after_hist = {}) {
     using namespace lx::sort;
     using K = typename lx::Traits<R>::Key;
     constexpr int P = lx::Traits<R>::kPasses;
@@ -527,6 +530,7 @@ void radix_sort(const R* raw, uint32_t m, R t, R* vals_out, uint32_t* perm_out, 
             lx_sort_hist_count0<R, false><<<g0, kThreads, 0, st>>>(raw, m, t, hist.as<uint32_t>(), bad,
                                                                    cnt.as<uint32_t>(), tiles, tpc);
         });
+        if (after_hist) after_hist();
     } else {
         launch("lx_sort_hist", st, [&] {
             lx_sort_hist<R><<<hgrid, kHistThreads, hsmem, st>>>(raw, m, t, hist.as<uint32_t>(), bad);
@@ -622,12 +626,16 @@ void build_splan(Side& sd, cudaStream_t st) {
 }
 
 template <class R>
-void build_side(Side& sd, const R* raw, uint32_t m, R t, const R* phase, int* bad, cudaStream_t st) {
+void build_side(Side& sd, const R* raw, uint32_t m, R t, const R* phase, int* bad, cudaStream_t st,
+                const std::function<void()>& after_hist = {}) {
     sd.m = m;
     sd.vals = DBuf((size_t)m * sizeof(R) + kTmaPad, st);  // TMA reads round up to 16 B
     sd.perm = DBuf((size_t)m * 4 + 16, st);
-    if (m == 0) return;  // empty side of a range shard
-    radix_sort<R>(raw, m, t, sd.vals.as<R>(), sd.perm.as<uint32_t>(), bad, st);
+    if (m == 0) {  // empty side of a range shard
+        if (after_hist) after_hist();
+        return;
+    }
+    radix_sort<R>(raw, m, t, sd.vals.as<R>(), sd.perm.as<uint32_t>(), bad, st, after_hist);
     if (phase) {
         DBuf ph((size_t)m * sizeof(R), st);
         launch("lx_gather_sorted", st, [&] {
@@ -794,21 +802,49 @@ laplex_plan create_plan(const R* a, uint32_t n, const R* b, uint32_t k, double t
     core->phased = phi != nullptr;
     DBuf bad(sizeof(int) * 4, st);
     ck(cudaMemsetAsync(bad.p, 0, sizeof(int) * 4, st), "memset");
+    // Host-pointer API (ready != null): the call returns as soon as the
+    // finiteness flags are known -- right behind the histogram of the second
+    // side -- and the rest of the build runs on behind it, overlapping the
+    // next call's upload (its kernels queue behind the build on the same
+    // stream).  NonFinite is still raised synchronously, in the reference's order.
+    const bool early = ready && sync;
+    thread_local int* hflags = [] {
+        int* q = nullptr;
+        ck(cudaMallocHost(&q, 4 * sizeof(int)), "cudaMallocHost");
+        return q;
+    }();
+    cudaEvent_t fev = nullptr;
+    auto flags_out = [&] {
+        if (phi) {
+            launch_finite<R>(phi, n, bad.as<int>() + 2, st);
+            launch_finite<R>(psi, k, bad.as<int>() + 2, st);
+        }
+        ck(cudaMemcpyAsync(hflags, bad.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+        ck(cudaEventCreateWithFlags(&fev, cudaEventDisableTiming), "cudaEventCreate");
+        ck(cudaEventRecord(fev, st), "cudaEventRecord");
+    };
     if (ready) ck(cudaStreamWaitEvent(st, ready[0], 0), "cudaStreamWaitEvent");
     build_side<R>(core->side[0], a, n, R(t), phi, bad.as<int>() + 0, st);
     if (ready) ck(cudaStreamWaitEvent(st, ready[1], 0), "cudaStreamWaitEvent");
-    build_side<R>(core->side[1], b, k, R(t), psi, bad.as<int>() + 1, st);
-    if (phi) {
+    build_side<R>(core->side[1], b, k, R(t), psi, bad.as<int>() + 1, st,
+                  early ? std::function<void()>(flags_out) : std::function<void()>());
+    if (!early && phi) {
         launch_finite<R>(phi, n, bad.as<int>() + 2, st);
         launch_finite<R>(psi, k, bad.as<int>() + 2, st);
     }
     build_partition<R>(*core, 0, st);
-    ck(cudaMemcpyAsync(core->bad_host, bad.p, sizeof(core->bad_host), cudaMemcpyDeviceToHost, st),
-       "cudaMemcpyAsync");
+    if (!early)
+        ck(cudaMemcpyAsync(core->bad_host, bad.p, sizeof(core->bad_host), cudaMemcpyDeviceToHost, st),
+           "cudaMemcpyAsync");
     touch(*core, st);
     ck(cudaEventCreateWithFlags(&core->built[0], cudaEventDisableTiming), "cudaEventCreate");
     ck(cudaEventRecord(core->built[0], st), "cudaEventRecord");
-    if (sync) {
+    if (early) {
+        ck(cudaEventSynchronize(fev), "cudaEventSynchronize");
+        cudaEventDestroy(fev);
+        std::memcpy(core->bad_host, hflags, sizeof(core->bad_host));
+        raise_bad(*core);  // the plan (released) still frees its buffers behind the build
+    } else if (sync) {
         ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
         raise_bad(*core);
     }
@@ -1548,26 +1584,30 @@ cudaStream_t upload_stream() {
     return s;
 }
 
+// A host buffer uploaded on the per-thread upload stream.  The device copy is
+// allocated on the upload stream too, so the copy starts at once, even while
+// the consumer stream still runs earlier work (e.g. the tail of a plan build);
+// the consumer waits on `done` (wait()) before use and frees the copy in its
+// own stream order (the destructor orders the free after the upload).
 template <class R>
 struct HostUp {
     DBuf d;
+    cudaStream_t cons;
     cudaEvent_t done = nullptr;
-    HostUp(const void* h, size_t count, cudaStream_t st) : d(count * sizeof(R), st) {
+    HostUp(const void* h, size_t count, cudaStream_t st) : d(count * sizeof(R), upload_stream()), cons(st) {
         if (!count) return;
-        cudaStream_t up = upload_stream();
-        cudaEvent_t alloc;
-        ck(cudaEventCreateWithFlags(&alloc, cudaEventDisableTiming), "cudaEventCreate");
-        ck(cudaEventRecord(alloc, st), "cudaEventRecord");  // the allocation is ordered on st
-        ck(cudaStreamWaitEvent(up, alloc, 0), "cudaStreamWaitEvent");
-        cudaEventDestroy(alloc);
-        ck(cudaMemcpyAsync(d.p, h, count * sizeof(R), cudaMemcpyHostToDevice, up), "H2D");
+        ck(cudaMemcpyAsync(d.p, h, count * sizeof(R), cudaMemcpyHostToDevice, d.st), "H2D");
         ck(cudaEventCreateWithFlags(&done, cudaEventDisableTiming), "cudaEventCreate");
-        ck(cudaEventRecord(done, up), "cudaEventRecord");
+        ck(cudaEventRecord(done, d.st), "cudaEventRecord");
     }
     HostUp(const HostUp&) = delete;
     HostUp& operator=(const HostUp&) = delete;
     ~HostUp() {
-        if (done) cudaEventDestroy(done);
+        if (done) {
+            cudaStreamWaitEvent(cons, done, 0);  // free after the upload, in the consumer's order
+            d.st = cons;
+            cudaEventDestroy(done);
+        }
     }
     void wait(cudaStream_t st) const {
         if (done) ck(cudaStreamWaitEvent(st, done, 0), "cudaStreamWaitEvent");
@@ -2185,6 +2225,7 @@ int laplex_gram(laplex_plan plan, unsigned flags, const void* D, size_t dlen, vo
             using R = decltype(zero);
             if (!host_finite((const R*)D, dlen)) fail(LAPLEX_E_NON_FINITE, "weighted_gram D: non-finite entry");
             HostUp<R> dd(D, k, st);
+            dd.wait(st);
             DBuf dm(n * n * sizeof(R), st);
             do_gram<R>(plan, flags, dd.get(), dm.as<R>(), st);
             d2h<R>(M, dm, n * n, st);
@@ -2223,6 +2264,7 @@ int laplex_gram_vjp_weights(laplex_plan plan, const void* D, size_t dlen, const 
             if (max_asym > R(1e-9) * std::max(R(1), max_abs))
                 fail(LAPLEX_E_ASYMMETRIC_COTANGENT, "gram_vjp_weights: G_bar is not symmetric");
             HostUp<R> dg(G_bar, n * n, st);
+            dg.wait(st);
             DBuf dd(k * sizeof(R), st);
             do_gram_vjp<R>(plan, dg.get(), dd.as<R>(), st);
             d2h<R>(D_bar, dd, k, st);
@@ -2246,6 +2288,7 @@ int laplex_sort(int dtype, const void* raw, size_t m, void* values, uint64_t* pe
             using R = decltype(zero);
             if (!host_finite((const R*)raw, m)) fail(LAPLEX_E_NON_FINITE, "sort_anchors: non-finite entry");
             HostUp<R> dr(raw, m, st);
+            dr.wait(st);
             DBuf vals(m * sizeof(R), st), pm(m * 4, st), bad(sizeof(int), st), dec(m > 1 ? (m - 1) * sizeof(R) : 0, st);
             ck(cudaMemsetAsync(bad.p, 0, sizeof(int), st), "memset");
             radix_sort<R>(dr.get(), (uint32_t)m, R(1), vals.as<R>(), pm.as<uint32_t>(), bad.as<int>(), st);
