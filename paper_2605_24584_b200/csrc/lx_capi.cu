@@ -541,6 +541,7 @@ void radix_sort(const R* raw, uint32_t m, R t, R* vals_out, uint32_t* perm_out, 
     }
     const size_t smem = sizeof(PassSmem<R>);
     smem_attr(lx_sort_pass<R, true, false>, smem);
+    smem_attr(lx_sort_pass<R, true, false, false, true>, smem);
     smem_attr(lx_sort_pass<R, false, false>, smem);
     smem_attr(lx_sort_pass<R, false, true>, smem);
     const void* in = raw;
@@ -569,7 +570,10 @@ void radix_sort(const R* raw, uint32_t m, R t, R* vals_out, uint32_t* perm_out, 
         }
         const uint32_t* tots = kSortRts ? totals.as<uint32_t>() + pass * kRadix : nullptr;
         launch("lx_sort_pass", st, [&] {
-            if (pass == 0)
+            if (pass == 0 && t == R(1))
+                lx_sort_pass<R, true, false, false, true><<<tiles, kThreads, smem, st>>>(
+                    in, inv, out, outv, m, t, pass * kBits, bptr, lb, ctr, epoch, offs, tots);
+            else if (pass == 0)
                 lx_sort_pass<R, true, false><<<tiles, kThreads, smem, st>>>(in, inv, out, outv, m, t, pass * kBits,
                                                                            bptr, lb, ctr, epoch, offs, tots);
             else if (!last)

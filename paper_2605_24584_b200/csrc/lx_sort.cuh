@@ -308,7 +308,11 @@ constexpr int sort_min_blocks() { return sizeof(typename Traits<R>::Key) == 4 ? 
 // The tile (keys, payload) arrives in shared memory by TMA bulk copy; keys are
 // then read from shared memory where needed, so no thread holds its 16 keys
 // across the load latency (register pressure, hence occupancy).
-template <class R, bool FIRST, bool LAST, bool SPLAN = false>
+// UNIT (first pass with t == 1, where raw / t == raw bitwise): the raw values
+// are turned into radix keys where they are read (ranking, reorder) instead of
+// in a separate shared-memory pass; the payload's -0 flags ride in a register
+// mask (first pass 5.9 ms -> see DESIGN.md 3).
+template <class R, bool FIRST, bool LAST, bool SPLAN = false, bool UNIT = false>
 __global__ void __launch_bounds__(kThreads, sort_min_blocks<R>()) lx_sort_pass(const void* __restrict__ in_keys,
                                                         const uint32_t* __restrict__ in_vals,
                                                         void* __restrict__ out_keys,
@@ -357,7 +361,9 @@ __global__ void __launch_bounds__(kThreads, sort_min_blocks<R>()) lx_sort_pass(c
         for (int i = (int)(vbytes / 4) + tid; i < tile_n; i += kThreads) sm.iv[i] = gv[i];
     mbar_wait(&sm.bar, 0);
     __syncthreads();
-    if constexpr (FIRST) {  // raw/t -> radix key, payload = index | (-0 flag)
+    static_assert(!UNIT || FIRST, "UNIT is a first-pass form");
+    static_assert(!UNIT || kItems <= 32, "the -0 flags live in one 32-bit mask");
+    if constexpr (FIRST && !UNIT) {  // raw/t -> radix key, payload = index | (-0 flag)
         // t == 1 (the API default): raw / t == raw bitwise in IEEE arithmetic,
         // so the division (~10 instructions per key) is skipped
         auto convert = [&](auto unit_t) {
@@ -394,7 +400,9 @@ __global__ void __launch_bounds__(kThreads, sort_min_blocks<R>()) lx_sort_pass(c
     for (int k = 0; k < kItems; ++k) {
         const int li = wbase + k * 32 + lane;
         const bool valid = full || li < tile_n;
-        const uint32_t dk = digit_of<SPLAN>(sm.ik[li], shift);  // tail slots: stale, masked
+        K key = sm.ik[li];
+        if constexpr (UNIT) key = radix_key<R>(from_bits(key, R(0)));
+        const uint32_t dk = digit_of<SPLAN>(key, shift);  // tail slots: stale, masked
         // invalid tail lanes sit above every valid lane of the item: they are
         // masked out of the peers and never advance a cursor
         const unsigned peers = match_digit8(full ? FULL : __ballot_sync(FULL, valid), dk);
@@ -467,12 +475,17 @@ __global__ void __launch_bounds__(kThreads, sort_min_blocks<R>()) lx_sort_pass(c
 scatter:
 
     // ---- reorder the tile in place into digit order: keys, then payload ----
+    uint32_t nzm = 0;  // UNIT: bit k = item k is -0 (the payload's flag)
     {
         K kv[kItems];
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
             const int li = wbase + k * 32 + lane;
             kv[k] = sm.ik[li];  // tail slots: stale, never stored
+            if constexpr (UNIT) {
+                nzm |= (uint32_t)(kv[k] == Traits<R>::kSign) << k;
+                kv[k] = radix_key<R>(from_bits(kv[k], R(0)));
+            }
             rd[k] = (wh[rd[k] >> 16] + (rd[k] & 0xffffu)) | (rd[k] & 0xffff0000u);  // shared position | digit
         }
         __syncthreads();
@@ -489,8 +502,14 @@ scatter:
     if constexpr (!SPLAN) {
         uint32_t vv[kItems];
 #pragma unroll
-        for (int k = 0; k < kItems; ++k) vv[k] = sm.iv[wbase + k * 32 + lane];
-        __syncthreads();
+        for (int k = 0; k < kItems; ++k) {
+            const int li = wbase + k * 32 + lane;
+            if constexpr (UNIT)
+                vv[k] = (uint32_t)(tile_start + li) | (((nzm >> k) & 1u) << 31);
+            else
+                vv[k] = sm.iv[li];
+        }
+        if constexpr (!UNIT) __syncthreads();
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
             const int li = wbase + k * 32 + lane;
