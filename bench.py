@@ -17,6 +17,7 @@ from __future__ import annotations
 import argparse
 import ctypes as C
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -71,6 +72,23 @@ STEP_MODEL_TEXT = {"fwd": "84n+80k+B(4n+4k)", "fwdbwd": "100n+96k+B(8n+12k)", "p
 # Algorithmic bytes per kernel over one step (summed over its launches),
 # what each kernel must read and write at minimum for its
 # role in this pipeline (fp32 values, u32 indices, u16 store order).
+def row_split(T, B, phased):
+    """Row chunks of a batched main-kernel launch (launch_main_mb, lx_capi.cu): the chunk count
+    minimising rounds of the resident CTA slots per chunk (phased kernels only; 148 SMs x 2 CTAs)."""
+    slots = 148 * 2
+    if not phased or B < 16 or T >= 4 * slots:
+        return 1
+    best, rc = math.ceil(T / slots), 1
+    for c in range(2, 9):
+        if c * 4 > B:
+            break
+        m = math.ceil(T * c / slots) / c
+        if m < best - 1e-9:
+            best, rc = m, c
+    chunk = (B + rc - 1) // rc
+    return (B + chunk - 1) // chunk
+
+
 def kernel_model_bytes(name, c):
     n, k, B, kind = c["n"], c["k"], c["B"], c["kind"]
     m2 = n + k
@@ -117,6 +135,8 @@ def kernel_model_bytes(name, c):
         "lx_main_bwd": 4 * m2 + B * (4 * n + 4 * k) + 6 * m2 + B * 4 * k + 4 * n + 4 * k + T * 512,
         "lx_main_bwd_phased": 4 * m2 + 16 * m2 + B * (4 * n + 4 * k) + 6 * m2 + B * 4 * k + 8 * n + 8 * k + T * 512,
         "lx_perm_scatter": 12 * ((out_rows * n if is_staged(n) else 0) + (out_cols * k if is_staged(k) else 0)),
+        # row-split backward: per-chunk partial a_bar/b_bar (+ phi_bar/psi_bar) summed in chunk order
+        "lx_chunk_sum": 4 * ch * m2 * (row_split(T, B, phased) + 1),
     }
     v = model.get(name)
     return v if v else None

@@ -905,13 +905,54 @@ void launch_main_mb(const char* name, const lx::ms::MainArgs<R>& a, cudaStream_t
     const size_t smem = sizeof(MainShared<R, NG + NX, TPB / 32, BWD ? (NG == 2 ? 2 : 1) : 0, os_smem ? kTile : 0>);
     smem_attr(kern, smem);
     const int per_sm = occupancy(kern, TPB + 32, smem), sms = num_sms();
-    // persistent: one CTA per resident slot, tiles claimed in order
-    const uint32_t grid = std::max<uint32_t>(1u, std::min<uint32_t>(a.T, (uint32_t)(sms * per_sm)));
+    const uint32_t slots = (uint32_t)(sms * per_sm);
+    lx::ms::MainArgs<R> b = a;
+    // Row split: a batch over fewer tiles than a few rounds of the resident
+    // CTAs leaves slots idle in the last round (C3: 513 tiles of 256 rows on
+    // 296 slots = 2 rounds for 1.73 of work).  Items of (tile, row chunk)
+    // even that out: the chunk count minimising rounds / chunks.
+    uint32_t rc = 1;
+    constexpr bool can_split = NG == 2 || NX == 2;  // lx_main's SPLIT
+    if (can_split && !SEQ && a.rows >= 16 && a.T < 4 * slots) {
+        double best = std::ceil((double)a.T / slots);
+        for (uint32_t c = 2; c <= 8 && (int)c * 4 <= a.rows; ++c) {
+            const double m = std::ceil((double)a.T * c / slots) / c;
+            if (m < best - 1e-9) best = m, rc = c;
+        }
+    }
+    b.rchunk = (a.rows + (int)rc - 1) / (int)rc;
+    b.rsplit = (uint32_t)((a.rows + b.rchunk - 1) / b.rchunk);  // every chunk non-empty
+    DBuf pa, pb;  // per-chunk partial row / column cotangents (backward)
+    if (BWD && b.rsplit > 1) {
+        constexpr int nacc = NG == 2 ? 2 : 1;
+        b.ldpa = a.n;
+        b.ldpb = a.k;
+        pa = DBuf((size_t)nacc * b.rsplit * a.n * sizeof(R), st);
+        pb = DBuf((size_t)nacc * b.rsplit * a.k * sizeof(R), st);
+        b.abar = pa.as<R>();
+        b.phibar = nacc == 2 ? pa.as<R>() + (size_t)b.rsplit * a.n : nullptr;
+        b.bbar = pb.as<R>();
+        b.psibar = nacc == 2 ? pb.as<R>() + (size_t)b.rsplit * a.k : nullptr;
+    }
+    // persistent: one CTA per resident slot, work items claimed in order
+    const uint32_t grid = std::max<uint32_t>(1u, std::min<uint32_t>(a.T * b.rsplit, slots));
     DBuf ctr(4, st);
     ck(cudaMemsetAsync(ctr.p, 0, 4, st), "memset");
-    lx::ms::MainArgs<R> b = a;
     b.tile_ctr = ctr.as<uint32_t>();
     launch(name, st, [&] { kern<<<grid, TPB + 32, smem, st>>>(b); });  // + producer warp
+    if (BWD && b.rsplit > 1) {
+        auto sum = [&](const R* part, size_t m, R* out) {
+            if (!m || !out) return;
+            const unsigned g = (unsigned)std::min<size_t>((m + 255) / 256, (size_t)sms * 8);
+            launch("lx_chunk_sum", st, [&] { lx::ms::lx_chunk_sum<R><<<g, 256, 0, st>>>(part, (int)b.rsplit, m, out); });
+        };
+        sum(b.abar, a.n, a.abar);
+        sum(b.bbar, a.k, a.bbar);
+        if (NG == 2) {
+            sum(b.phibar, a.n, a.phibar);
+            sum(b.psibar, a.k, a.psibar);
+        }
+    }
 }
 
 // The unphased fp32 backward: 2 CTAs/SM (168 registers) for single rows, 3
@@ -923,6 +964,15 @@ void launch_main_mb(const char* name, const lx::ms::MainArgs<R>& a, cudaStream_t
 template <class R, int NG, int NX, bool BWD, bool SEQ = false>
 void launch_main(const char* name, const lx::ms::MainArgs<R>& a, cudaStream_t st) {
     if constexpr (BWD && NG == 1 && NX == 1 && sizeof(R) == 4) {
+        if (a.rows > 1) {
+            launch_main_mb<R, NG, NX, BWD, SEQ, 3>(name, a, st);
+            return;
+        }
+    }
+    // batched unphased forward / transpose: the same 3-CTA budget as the
+    // single-row kernel, instantiated apart so that it prefetches the next
+    // row's tile carries (MB != 0 in lx_main)
+    if constexpr (!BWD && !SEQ && NG + NX == 1 && sizeof(R) == 4 && LX_MAIN_CTAS / MainShape<(NG > 0), false>::TPB == 3) {
         if (a.rows > 1) {
             launch_main_mb<R, NG, NX, BWD, SEQ, 3>(name, a, st);
             return;

@@ -53,6 +53,7 @@ struct MainStage {
     alignas(16) uint32_t oidx[kTile + 16];  // output index ranges: A at [offIA], B at [baseIB + offIB]
     alignas(16) uint16_t gm[kTile];         // store order (lx_group_plan): rows at [0, na), cols at [na, len)
     alignas(16) uint32_t mw[kMergeWords];   // the tile's merge words (lx_group_plan)
+    int r0;  // first batch row of the work item (row split, see MainArgs::rsplit; last: the header layout above is shared)
 };
 
 #ifndef LX_MAIN_STAGES
@@ -111,10 +112,12 @@ struct TileGeom {
 // Producer lane: stage tile t (header, row-0 carries, anchors, output
 // indices, row-0 payloads) and arm the stage's barriers.  t >= T stages the
 // end-of-work sentinel (header only).
-template <class R, int NC, bool SEQ, bool PAY_A, bool PAY_B, bool OUT_A, bool OUT_B, class CH>
-__device__ __forceinline__ void issue_tile(MainStage<R, NC>& S, const MainArgs<R>& p, uint32_t t,
+template <class R, int NC, bool SEQ, bool PAY_A, bool PAY_B, bool OUT_A, bool OUT_B, class CH, bool SPLIT>
+__device__ __forceinline__ void issue_tile(MainStage<R, NC>& S, const MainArgs<R>& p, uint32_t t, int r0,
                                            const TileDesc<R>& dt, const TileDesc<R>& dn, R SL) {
     S.t = t;
+    if constexpr (SPLIT) S.r0 = r0;
+    else r0 = 0;
     if (t >= p.T) {
         mbar_expect_tx(&S.bar, 0u);
         return;
@@ -122,7 +125,7 @@ __device__ __forceinline__ void issue_tile(MainStage<R, NC>& S, const MainArgs<R
     const size_t T = p.T, rows = p.rows;
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
-        const size_t sl0 = (size_t)(2 * c) * rows, sl1 = (size_t)(2 * c + 1) * rows;
+        const size_t sl0 = (size_t)(2 * c) * rows + r0, sl1 = (size_t)(2 * c + 1) * rows + r0;
         S.c0[0][c] = t > 0 ? p.cp[sl0 * T + t - 1] : R(0);
         S.c0[1][c] = (t > 0 && CH::pst(c)) ? p.cp[sl1 * T + t - 1] : R(0);
         S.c0[2][c] = t + 1 < T ? p.cq[sl0 * T + t + 1] : R(0);
@@ -145,11 +148,12 @@ __device__ __forceinline__ void issue_tile(MainStage<R, NC>& S, const MainArgs<R
     if (g.ibytesA) bulk_g2s(S.oidx, p.perm_a + g.a0i, g.ibytesA, &S.bar);
     if (g.ibytesB) bulk_g2s(S.oidx + g.ibytesA / 4, p.perm_b + g.b0i, g.ibytesB, &S.bar);
     if (g.gbytes) bulk_g2s(S.gm, p.gmt + (size_t)t * kTile, g.gbytes, &S.bar);
-    const R* srcA = SEQ ? p.Xs : p.Gs;
+    const R* srcA = (SEQ ? p.Xs : p.Gs) + (size_t)r0 * (SEQ ? p.ldxs : p.ldgs);
     mbar_expect_tx(&S.barp, (PAY_A ? g.bytesA : 0u) + (PAY_B ? g.bytesB : 0u));
     if (PAY_A && g.bytesA) bulk_g2s(S.pay, srcA + g.a0al, g.bytesA, &S.barp);
     if (PAY_B && g.bytesB)
-        bulk_g2s(S.pay + (g.bytesA / sizeof(R)) + MainStage<R, NC>::kPad, p.Xs + g.b0al, g.bytesB, &S.barp);
+        bulk_g2s(S.pay + (g.bytesA / sizeof(R)) + MainStage<R, NC>::kPad, p.Xs + (size_t)r0 * p.ldxs + g.b0al,
+                 g.bytesB, &S.barp);
 }
 
 // Diagnostics only (LX_DIAG_CONTIG): write outputs at the sorted position
@@ -228,6 +232,11 @@ __global__ void __launch_bounds__(TPB + 32, MB ? MB : main_min_blocks<R, BWD, TP
     const R* cpsi = p.cpsi;
     const R* spsi = p.spsi;
 
+    // row split (MainArgs::rsplit) only in the phased kernels (C3's head: a
+    // large batch over few tiles); in the unphased kernels its registers and
+    // producer arithmetic measured slower (C2 +1.3 ms, C5 forward +0.25 ms)
+    constexpr bool SPLIT = PHASED;
+
     // ---- tile schedule: one producer warp, TPB consumer threads ----
     // Tiles are claimed in increasing order from a global counter, so the
     // tiles in flight stay a compact window of the merged sequence (the
@@ -246,8 +255,11 @@ __global__ void __launch_bounds__(TPB + 32, MB ? MB : main_min_blocks<R, BWD, TP
     __syncthreads();
     if (warp == NW) {
         if (lane == 0) {
-            auto claim = [&](uint32_t& tt, TileDesc<R>& d0, TileDesc<R>& d1, R& sl) {
-                tt = atomicAdd(p.tile_ctr, 1u);
+            const uint32_t RS = SPLIT ? p.rsplit : 1u;
+            auto claim = [&](uint32_t& tt, int& r0, TileDesc<R>& d0, TileDesc<R>& d1, R& sl) {
+                const uint32_t item = atomicAdd(p.tile_ctr, 1u);
+                tt = SPLIT ? item / RS : item;
+                r0 = SPLIT ? (int)(item - tt * RS) * p.rchunk : 0;
                 if (tt < T) {
                     d0 = p.desc[tt];
                     d1 = p.desc[tt + 1];
@@ -255,21 +267,23 @@ __global__ void __launch_bounds__(TPB + 32, MB ? MB : main_min_blocks<R, BWD, TP
                 }
             };
             uint32_t tc;
+            int r0;
             TileDesc<R> d0, d1;
             R sl = R(0);
-            claim(tc, d0, d1, sl);
+            claim(tc, r0, d0, d1, sl);
             for (int it = 0;; ++it) {
                 const int s = it % kMainStages;
                 const uint32_t use = (uint32_t)(it / kMainStages);
                 if (it >= kMainStages) mbar_wait_sleep(&sm.st[s].empty, (use - 1u) & 1u);
-                issue_tile<R, NC, SEQ, PAY_A, PAY_B, OUT_A, OUT_B, C>(sm.st[s], p, tc, d0, d1, sl);
+                issue_tile<R, NC, SEQ, PAY_A, PAY_B, OUT_A, OUT_B, C, SPLIT>(sm.st[s], p, tc, r0, d0, d1, sl);
                 if (tc >= T) break;
-                claim(tc, d0, d1, sl);
+                claim(tc, r0, d0, d1, sl);
             }
         }
         return;
     }
 
+    unsigned pph = 0;  // SPLIT: bit s = phase of stage s's payload barrier
     for (int it = 0;; ++it) {
         const int sidx = it % kMainStages;
         auto& S = sm.st[sidx];
@@ -277,6 +291,7 @@ __global__ void __launch_bounds__(TPB + 32, MB ? MB : main_min_blocks<R, BWD, TP
         mbar_wait(&S.bar, use & 1u);
         const uint32_t t = S.t;
         if (t >= T) break;
+        const int r0 = SPLIT ? S.r0 : 0, r1 = SPLIT ? min(rows, r0 + p.rchunk) : rows;  // this item's batch rows
         TileGeom<R> g;
         g.init(S.a0, S.b0, S.na, S.nb, OUT_A, OUT_B);
         const int na = g.na, nb = g.nb, len = na + nb;
@@ -363,16 +378,21 @@ __global__ void __launch_bounds__(TPB + 32, MB ? MB : main_min_blocks<R, BWD, TP
             }
         }
 
-        for (int r = 0; r < rows; ++r) {
-            mbar_wait(&S.barp, (use * (uint32_t)rows + (uint32_t)r) & 1u);
+        for (int r = r0; r < r1; ++r) {
+            if constexpr (SPLIT) {
+                mbar_wait(&S.barp, (pph >> sidx) & 1u);
+                pph ^= 1u << sidx;
+            } else {
+                mbar_wait(&S.barp, (use * (uint32_t)rows + (uint32_t)r) & 1u);
+            }
             // phased kernels: the next batch row's tile carries are copied
             // global -> shared asynchronously now and read after barrier (A)
             // of that row (row 0's come with the producer's staging; C3 bwd
             // 5.43 -> 4.71 ms).  The unphased kernels load them at use: the
             // prefetch's registers cost the single-row C5 kernels more than
             // it saves the batched C2 ones.
-            constexpr bool PF = PHASED;
-            const bool pf = PF && r + 1 < rows && tid < 4 * NC;
+            constexpr bool PF = PHASED || MB != 0;  // MB != 0: the batched unphased backward
+            const bool pf = PF && r + 1 < r1 && tid < 4 * NC;
             if (pf) {
                 const int c = tid % NC, kind = tid / NC;  // kind: prefix, strict prefix, suffix, strict suffix
                 const bool strict = kind & 1;
@@ -497,14 +517,14 @@ __global__ void __launch_bounds__(TPB + 32, MB ? MB : main_min_blocks<R, BWD, TP
                     sm.qw[c][warp] = wq[c];
                 }
             }
-            if (PF && r > 0 && tid < 4 * NC) {  // this row's prefetched carries have landed
+            if (PF && r > r0 && tid < 4 * NC) {  // this row's prefetched carries have landed
                 if (pf)
                     asm volatile("cp.async.wait_group 1;" ::: "memory");
                 else
                     asm volatile("cp.async.wait_group 0;" ::: "memory");
             }
             cbar<TPB>();  // (A) warp totals; every merge of this tile is done; row carries in shared memory
-            if (tid == 0 && r + 1 < rows) {  // next batch row's payloads into this stage
+            if (tid == 0 && r + 1 < r1) {  // next batch row's payloads into this stage
                 const R* srcA = SEQ ? p.Xs : p.Gs;
                 const size_t ldA = SEQ ? p.ldxs : p.ldgs;
                 mbar_expect_tx(&S.barp, (PAY_A ? g.bytesA : 0u) + (PAY_B ? g.bytesB : 0u));
@@ -588,7 +608,7 @@ __global__ void __launch_bounds__(TPB + 32, MB ? MB : main_min_blocks<R, BWD, TP
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
                 const size_t sl0 = ((size_t)(2 * c) * rows + r), sl1 = ((size_t)(2 * c + 1) * rows + r);
-                if (r == 0) {  // staged by the producer
+                if (r == r0) {  // staged by the producer
                     cpv[c] = S.c0[0][c];
                     cps[c] = S.c0[1][c];
                     cqv[c] = S.c0[2][c];
@@ -744,7 +764,7 @@ __global__ void __launch_bounds__(TPB + 32, MB ? MB : main_min_blocks<R, BWD, TP
                     R* acp2 = &sm.acc[NACC > 1 ? 1 : 0][isr ? ia : na + ib];
                     R acc1 = R(0), acc2 = R(0);
                     if constexpr (BWD) {
-                        if (r > 0) {
+                        if (r > r0) {
                             acc1 = *acp1;
                             if constexpr (PHASED) acc2 = *acp2;
                         }
@@ -819,7 +839,7 @@ __global__ void __launch_bounds__(TPB + 32, MB ? MB : main_min_blocks<R, BWD, TP
                     }
                 } else {
                     R* xb = p.xbar + (size_t)r * p.ldxb;
-                    if (r + 1 < rows) {
+                    if (r + 1 < r1) {
                         for (int k = tid; k < nb; k += TPB) {
                             const int li = gmB[k];
                             xb[LXO(iB[li], g.b0 + li)] = stg[li];
@@ -829,8 +849,9 @@ __global__ void __launch_bounds__(TPB + 32, MB ? MB : main_min_blocks<R, BWD, TP
                             const int li = gmB[k];
                             const uint32_t u = LXO(iB[li], g.b0 + li);
                             xb[u] = stg[li];
-                            p.bbar[u] = sm.acc[0][na + li];
-                            if constexpr (PHASED) p.psibar[u] = sm.acc[NACC - 1][na + li];
+                            const size_t cu = SPLIT ? (size_t)(r0 / p.rchunk) * p.ldpb + u : u;  // row chunk's partial
+                            p.bbar[cu] = sm.acc[0][na + li];
+                            if constexpr (PHASED) p.psibar[cu] = sm.acc[NACC - 1][na + li];
                         }
                     }
                 }
@@ -844,12 +865,24 @@ __global__ void __launch_bounds__(TPB + 32, MB ? MB : main_min_blocks<R, BWD, TP
             for (int k = tid; k < na; k += TPB) {
                 const int li = gmA[k];
                 const uint32_t u = LXO(iA[li], g.a0 + li);
-                p.abar[u] = sm.acc[0][li];
-                if constexpr (PHASED) p.phibar[u] = sm.acc[NACC - 1][li];
+                const size_t cu = SPLIT ? (size_t)(r0 / p.rchunk) * p.ldpa + u : u;  // row chunk's partial
+                p.abar[cu] = sm.acc[0][li];
+                if constexpr (PHASED) p.phibar[cu] = sm.acc[NACC - 1][li];
             }
             cbar<TPB>();
         }
         if (tid == 0) mbar_arrive(&S.empty);  // the stage may be refilled
+    }
+}
+
+// Row split: out[i] = sum over the C row chunks of part[c * m + i], chunks in
+// order (deterministic; the unsplit kernel sums the same rows in row order)
+template <class R>
+__global__ void __launch_bounds__(256) lx_chunk_sum(const R* __restrict__ part, int C, size_t m, R* __restrict__ out) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (size_t)gridDim.x * blockDim.x) {
+        R v = part[i];
+        for (int c = 1; c < C; ++c) v = xadd(v, part[(size_t)c * m + i]);
+        out[i] = v;
     }
 }
 

@@ -263,6 +263,14 @@ struct MainArgs {
     R* psibar;
     R* pre;     // SEQ: inclusive prefix / suffix, sorted order
     R* suf;
+    // row split (batches over few tiles): work item i = (tile i / rsplit, rows
+    // [c * rchunk, min(rows, (c + 1) * rchunk)) with c = i % rsplit); the
+    // row-summed cotangents of chunk c go to abar/phibar + c * ldpa and
+    // bbar/psibar + c * ldpb (summed over chunks by lx_chunk_sum).  rsplit = 1:
+    // one item per tile, every row
+    uint32_t rsplit;
+    int rchunk;
+    size_t ldpa, ldpb;
 };
 
 // Channel layout: g channels first (c < NG), then x channels.  Strict prefix

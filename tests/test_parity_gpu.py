@@ -506,3 +506,66 @@ def test_host_api_large_inputs_nonfinite_order():
         L.matvec_vjp(op, xb, gb)  # x reported first
     # and the valid call still works afterwards
     assert O.rel_err_l2(op.matvec(x), O.OracleOp(a, b).matvec(x)) <= 1e-12
+
+
+# ------------------------------------------------ batches over few tiles: row-split work items
+@pytest.mark.parametrize("phased", [False, True])
+def test_row_split_batches_fp64(phased):
+    """A batch whose merge tiles are fewer than the resident CTA slots runs as
+    (tile, row chunk) work items with per-chunk partial cotangents summed in
+    chunk order (lx_main rsplit, lx_chunk_sum).  fp64 against the reference
+    oracle row by row; a_bar/b_bar (and phi_bar/psi_bar) against the oracle's
+    per-row cotangents summed over rows (reference gradients.hpp:122-133)."""
+    import torch
+    rng = np.random.default_rng(47 + phased)
+    n, k, B = 3001, 150_000, 24
+    a = rng.uniform(-50, 50, n)
+    b = rng.uniform(-50, 50, k)
+    b[:500] = a[:500]  # exact ties across the sides
+    phi, psi = (rng.uniform(0, 6.28, n), rng.uniform(0, 6.28, k)) if phased else (None, None)
+    X, G = rng.uniform(-1, 1, (B, k)), rng.uniform(-1, 1, (B, n))
+    dev = torch.device("cuda:0")
+    T = lambda v: None if v is None else torch.tensor(v, device=dev)
+    op = L.DeviceOperator(T(a), T(b), 0.8, T(phi), T(psi))
+    oo = O.OracleOp(a, b, 0.8, phi, psi)
+    Y = op.apply(T(X)).cpu().numpy()
+    cots = [c.cpu().numpy() if c is not None else None for c in op.backward(T(X), T(G))]
+    sums = None
+    for r in range(B):
+        if phased:
+            assert O.rel_err_l2(Y[r], oo.phased_matvec(X[r])) <= 1e-12
+            w = oo.phased_vjp(X[r], G[r])
+        else:
+            assert O.rel_err_l2(Y[r], oo.matvec(X[r])) <= 1e-12
+            w = oo.vjp(X[r], G[r])
+        assert O.rel_err_l2(cots[0][r], w[0]) <= 1e-11
+        sums = list(w[1:]) if sums is None else [s + v for s, v in zip(sums, w[1:])]
+    for got, want in zip(cots[1:], sums):
+        assert O.rel_err_l2(got, want) <= 1e-11
+
+
+def test_row_split_batches_fp32_bitwise_rows():
+    """fp32 unphased batch over few tiles (the 3-CTA batch kernels, carries of the
+    next row prefetched): every row bitwise equal to its single-row call, x_bar
+    bitwise the transpose, row-summed cotangents equal to the sum of single-row
+    ones."""
+    import torch
+    rng = np.random.default_rng(53)
+    n, k, B = 100_000, 90_000, 32
+    dev = torch.device("cuda:0")
+    a = torch.tensor(rng.uniform(-100, 100, n).astype(F32), device=dev)
+    b = torch.tensor(rng.uniform(-100, 100, k).astype(F32), device=dev)
+    X = torch.tensor(rng.uniform(-1, 1, (B, k)).astype(F32), device=dev)
+    G = torch.tensor(rng.uniform(-1, 1, (B, n)).astype(F32), device=dev)
+    op = L.DeviceOperator(a, b, 1.0)
+    Y = op.apply(X)
+    xb, ab, bb, _, _ = op.backward(X, G)
+    parts = [op.backward(X[r:r + 1], G[r:r + 1]) for r in range(B)]
+    for r in range(B):
+        assert torch.equal(Y[r], op.apply(X[r:r + 1])[0])
+        assert torch.equal(xb[r], parts[r][0][0])
+    assert torch.equal(xb, op.apply(G, transpose=True))
+    sa = sum(p[1].double() for p in parts)
+    sb = sum(p[2].double() for p in parts)
+    assert O.rel_err_l2(ab.double().cpu().numpy(), sa.cpu().numpy()) <= 1e-6
+    assert O.rel_err_l2(bb.double().cpu().numpy(), sb.cpu().numpy()) <= 1e-6
