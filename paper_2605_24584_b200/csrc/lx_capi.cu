@@ -902,7 +902,9 @@ void launch_main_mb(const char* name, const lx::ms::MainArgs<R>& a, cudaStream_t
     constexpr int TPB = MainShape<(NG > 0), (NG == 2 || NX == 2)>::TPB, IPT = MainShape<(NG > 0), (NG == 2 || NX == 2)>::IPT;
     auto kern = lx_main<R, NG, NX, BWD, SEQ, TPB, IPT, MB>;
     constexpr bool os_smem = LX_OS_SMEM && BWD && NG != 2 && sizeof(R) == 4;
-    const size_t smem = sizeof(MainShared<R, NG + NX, TPB / 32, BWD ? (NG == 2 ? 2 : 1) : 0, os_smem ? kTile : 0>);
+    constexpr bool mc_smem = LX_PH_MC_SMEM && (NG == 2 || NX == 2) && sizeof(R) == 4;
+    const size_t smem = sizeof(MainShared<R, NG + NX, TPB / 32, BWD ? (NG == 2 ? 2 : 1) : 0, os_smem ? kTile : 0,
+                                          mc_smem ? 2 * kTile : 0>);
     smem_attr(kern, smem);
     const int per_sm = occupancy(kern, TPB + 32, smem), sms = num_sms();
     const uint32_t slots = (uint32_t)(sms * per_sm);

@@ -61,9 +61,14 @@ struct MainStage {
 #endif
 constexpr int kMainStages = LX_MAIN_STAGES;
 
-template <class R, int NC, int NW, int NACC, int NOS>
+template <class R, int NC, int NW, int NACC, int NOS, int NMC = 0>
 struct MainShared {
     MainStage<R, NC> st[kMainStages];
+    // phased fp32: each thread's cos / sin of its elements' phases for the
+    // current tile, [q][thread] (row-invariant values that would otherwise stay
+    // live in registers across the batch-row loop and spill; C3 main kernels
+    // 5.77 -> 5.43 ms.  The in-thread decays there as well measured slower)
+    R mcs[NMC > 0 ? NMC : 1];
     // suffix values recorded between the two re-scans, [k][q][thread] (fp32
     // unphased backward: saves 8 registers where the kernel would spill)
     R os[NOS > 0 ? NOS : 1];
@@ -178,6 +183,9 @@ __device__ __forceinline__ void issue_tile(MainStage<R, NC>& S, const MainArgs<R
 #ifndef LX_OS_SMEM
 #define LX_OS_SMEM 0
 #endif
+#ifndef LX_PH_MC_SMEM
+#define LX_PH_MC_SMEM 1
+#endif
 // phased (256-thread) kernels: resident CTAs per SM the register budget targets
 #ifndef LX_PH_FWD_CTAS
 #define LX_PH_FWD_CTAS 2  // 3 spilled (72 registers): C3 forward 3.37 -> 2.42 ms with 2
@@ -215,7 +223,8 @@ __global__ void __launch_bounds__(TPB + 32, MB ? MB : main_min_blocks<R, BWD, TP
     constexpr int KS = SEQ ? 1 : (!BWD ? (NG > 0 ? NG : NX) : (PHASED ? 4 : 1));
     constexpr int NACC = BWD ? (PHASED ? 2 : 1) : 0;
     constexpr bool OS_SMEM = LX_OS_SMEM && BWD && !PHASED && sizeof(R) == 4;
-    using SM = MainShared<R, NC, NW, NACC, OS_SMEM ? KS * kTile : 0>;
+    constexpr bool MC_SMEM = LX_PH_MC_SMEM && PHASED && sizeof(R) == 4;
+    using SM = MainShared<R, NC, NW, NACC, OS_SMEM ? KS * kTile : 0, MC_SMEM ? 2 * kTile : 0>;
     extern __shared__ __align__(16) unsigned char smem_main[];
     SM& sm = *reinterpret_cast<SM*>(smem_main);
 
@@ -362,7 +371,9 @@ __global__ void __launch_bounds__(TPB + 32, MB ? MB : main_min_blocks<R, BWD, TP
 
         // phased: cos / sin of each element's phase (rows: phi, cols: psi),
         // loaded once per tile instead of once per batch row and use
-        R mc[PHASED ? IPT : 1], ms[PHASED ? IPT : 1];
+        R mcr[PHASED && !MC_SMEM ? IPT : 1], msr[PHASED && !MC_SMEM ? IPT : 1];
+        auto MCw = [&](int q) -> R& { if constexpr (MC_SMEM) return sm.mcs[q * TPB + tid]; else return mcr[q]; };
+        auto MSw = [&](int q) -> R& { if constexpr (MC_SMEM) return sm.mcs[(IPT + q) * TPB + tid]; else return msr[q]; };
         if constexpr (PHASED) {
             int ia = ia0, ib = ib0;
 #pragma unroll
@@ -371,8 +382,8 @@ __global__ void __launch_bounds__(TPB + 32, MB ? MB : main_min_blocks<R, BWD, TP
                 const R* cs = isr ? cphi + g.a0 + ia : cpsi + g.b0 + ib;
                 const R* sn = isr ? sphi + g.a0 + ia : spsi + g.b0 + ib;
                 const bool has = val && (isr ? (NG == 2 || !BWD) : NX == 2);
-                mc[q] = has ? *cs : R(1);
-                ms[q] = has ? *sn : R(0);
+                MCw(q) = has ? *cs : R(1);
+                MSw(q) = has ? *sn : R(0);
                 ia += isr;
                 ib += !isr;
             }
@@ -434,8 +445,8 @@ __global__ void __launch_bounds__(TPB + 32, MB ? MB : main_min_blocks<R, BWD, TP
                         // backward; cols: psi); the forward's rows carry no payload
                         const bool mod = isr ? NG == 2 : NX == 2;
                         raw[q] = v;
-                        pay[0][q] = mod ? xmul(mc[q], v) : v;
-                        pay[1][q] = mod ? xmul(ms[q], v) : R(0);
+                        pay[0][q] = mod ? xmul(MCw(q), v) : v;
+                        pay[1][q] = mod ? xmul(MSw(q), v) : R(0);
                     } else {
                         pay[0][q] = v;
                     }
@@ -778,7 +789,7 @@ __global__ void __launch_bounds__(TPB + 32, MB ? MB : main_min_blocks<R, BWD, TP
                         const int li = ia++;
                         if constexpr (!BWD && NX > 0) {
                             R out = xadd(a[0], OS(0, q));
-                            if constexpr (NX == 2) out = xadd(xmul(mc[q], out), xmul(ms[q], xadd(a[1], OS(1, q))));
+                            if constexpr (NX == 2) out = xadd(xmul(MCw(q), out), xmul(MSw(q), xadd(a[1], OS(1, q))));
                             stg[li] = out;
                         } else if constexpr (BWD) {
                             if constexpr (!PHASED) {
@@ -786,7 +797,7 @@ __global__ void __launch_bounds__(TPB + 32, MB ? MB : main_min_blocks<R, BWD, TP
                                 acc1 = xfma(xmul(gg, p.inv_t), xsub(OS(0, q), a[1]), acc1);
                             } else {
                                 const R gg = raw[q];
-                                const R m0 = mc[q], m1 = ms[q];
+                                const R m0 = MCw(q), m1 = MSw(q);
                                 const R in0 = xsub(OS(2, q), a[NG]);  // sum_{b>a} - sum_{b<a}
                                 const R in1 = xsub(OS(3, q), a[NG + 1]);
                                 acc1 = xfma(xmul(xmul(m0, gg), p.inv_t), in0, acc1);
@@ -807,7 +818,7 @@ __global__ void __launch_bounds__(TPB + 32, MB ? MB : main_min_blocks<R, BWD, TP
                                 acc1 = xfma(xmul(x, p.inv_t), xsub(OS(0, q), b[0]), acc1);
                             } else {
                                 const R x = raw[q];
-                                const R m0 = mc[q], m1 = ms[q];
+                                const R m0 = MCw(q), m1 = MSw(q);
                                 const R xb1 = xadd(a[1], OS(1, q));
                                 stg[li] = xadd(xmul(m0, xb0), xmul(m1, xb1));
                                 acc2 = xfma(x, xadd(xmul(-m1, xb0), xmul(m0, xb1)), acc2);
