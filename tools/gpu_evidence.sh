@@ -1,7 +1,7 @@
 # One gpurun call that regenerates the round's evidence at HEAD (TAG below): bench lines
 # (C5 default + C1..C4), the ncu launch list of the bench command with per-kernel DRAM traffic,
 # and full ncu captures of the dominant kernels (summaries in profiles/).  Usage: bash tools/gpu_evidence.sh TAG
-TAG=${1:-r02e}
+TAG=${1:-r02f}
 timeout 900 python bench.py > gpurun_out/${TAG}_bench_C5.json 2> gpurun_out/${TAG}_bench_C5.err
 for c in C1 C2 C3 C4; do
   timeout 900 python bench.py --config $c > gpurun_out/${TAG}_bench_$c.json 2> gpurun_out/${TAG}_bench_$c.err
