@@ -436,12 +436,15 @@ def make_step(L, torch, c, t):
         o.update(pb=torch.empty(n, device=dev), qb=torch.empty(k, device=dev))
 
     def step():
+        # a training loop's plan: no host synchronisation at creation; the
+        # finiteness errors are checked once per step, after its work is queued
         if kind == "phased":
-            op = L.DeviceOperator(t["a"], t["b"], 1.0, t["phi"], t["psi"])
+            op = L.DeviceOperator(t["a"], t["b"], 1.0, t["phi"], t["psi"], sync=False)
         else:
-            op = L.DeviceOperator(t["a"], t["b"], 1.0)
+            op = L.DeviceOperator(t["a"], t["b"], 1.0, sync=False)
         if kind == "gram":
             op.gram_apply(t["X"], out=o["Y"])
+            op.check()
             return op
         # a training step: the forward saves its sorted x for the backward (LAPLEX_SAVE_X / REUSE_X)
         op.apply(t["X"], out=o["Y"], save_x=kind != "fwd")
@@ -450,6 +453,7 @@ def make_step(L, torch, c, t):
         elif kind == "phased":
             op.backward(t["X"], t["G"], x_bar=o["xb"], a_bar=o["ab"], b_bar=o["bb"], phi_bar=o["pb"],
                         psi_bar=o["qb"], reuse_x=True)
+        op.check()
         return op
     return step, o
 
@@ -555,6 +559,13 @@ def run_ours(args, rank, world, dist):
 
     e2e = None
     if args.e2e and rank == 0:
+        # the host-pointer path runs on its own: the device-path inputs, outputs
+        # and torch's cached blocks (~8 arrays of the config's size) are freed
+        # first, as in a process that only uses the host API
+        del step, outs, t, scrub
+        ab = bb = None  # noqa: F841 (the conservation check's references)
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
         e2e = run_e2e(args, torch, lib, c)
 
     if rank == 0:

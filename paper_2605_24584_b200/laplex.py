@@ -360,7 +360,9 @@ def symmetric_matvec(anchors: SortedAnchors, x) -> np.ndarray:
 class DeviceOperator:
     """Plan built from CUDA tensors; apply/backward on CUDA tensors, stream-ordered."""
 
-    def __init__(self, a, b, temperature: float = 1.0, phi=None, psi=None, stream=None):
+    def __init__(self, a, b, temperature: float = 1.0, phi=None, psi=None, stream=None, sync=True):
+        """sync=False: no host synchronisation at creation (laplex_plan_create_dev_async);
+        non-finite anchors are then reported by check(), e.g. once per training step."""
         import torch
         assert a.is_cuda and b.is_cuda and a.dtype == b.dtype
         self.torch = torch
@@ -369,11 +371,16 @@ class DeviceOperator:
         st = self._stream(stream)
         h = C.c_void_p()
         dt = F64 if a.dtype == torch.float64 else F32
-        _check(lib().laplex_plan_create_dev(dt, a.data_ptr(), self.n, b.data_ptr(), self.k, float(temperature),
-                                            phi.data_ptr() if phi is not None else None,
-                                            psi.data_ptr() if psi is not None else None, st, C.byref(h)))
+        create = lib().laplex_plan_create_dev if sync else lib().laplex_plan_create_dev_async
+        _check(create(dt, a.data_ptr(), self.n, b.data_ptr(), self.k, float(temperature),
+                      phi.data_ptr() if phi is not None else None,
+                      psi.data_ptr() if psi is not None else None, st, C.byref(h)))
         self._h = h
         self.phased = phi is not None
+
+    def check(self):
+        """Raise the creation errors of a sync=False plan (waits for its build)."""
+        _check(lib().laplex_plan_check(self._h))
 
     def _stream(self, stream):
         torch = self.torch

@@ -222,3 +222,26 @@ def test_host_api_saved_x_reuse_is_bitwise(torch, phased, n):
     got2 = LX._vjp(op, X, G, base | LX.REUSE_X)  # not the saved host x: uploaded again
     for f in fields:
         assert np.array_equal(getattr(want, f), getattr(got2, f)), f
+
+
+def test_device_operator_without_creation_sync():
+    """DeviceOperator(sync=False) (laplex_plan_create_dev_async): results bitwise those
+    of a synchronously created plan; non-finite anchors reported by check()."""
+    import torch
+    import paper_2605_24584_b200 as L
+    dev = torch.device("cuda:0")
+    g = torch.Generator(device=dev)
+    g.manual_seed(5)
+    a = torch.empty(70_001, device=dev).uniform_(-50, 50, generator=g)
+    b = torch.empty(50_003, device=dev).uniform_(-50, 50, generator=g)
+    X = torch.empty(3, 50_003, device=dev).uniform_(-1, 1, generator=g)
+    G = torch.empty(3, 70_001, device=dev).uniform_(-1, 1, generator=g)
+    s, q = L.DeviceOperator(a, b, 0.7), L.DeviceOperator(a, b, 0.7, sync=False)
+    assert torch.equal(s.apply(X), q.apply(X))
+    for u, v in zip(s.backward(X, G)[:3], q.backward(X, G)[:3]):
+        assert torch.equal(u, v)
+    q.check()
+    a[123] = float("nan")
+    bad = L.DeviceOperator(a, b, 0.7, sync=False)
+    with pytest.raises(Exception):
+        bad.check()
