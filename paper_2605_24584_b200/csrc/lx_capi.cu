@@ -1081,9 +1081,22 @@ DBuf sorted_payload(const View<R>& v, int rows, const R* user, const Scratch& sc
     }
     launch("lx_gather_agg", st, [&] {
         const uint32_t grid = (v.T + lx::ms::kAggTiles - 1) / lx::ms::kAggTiles;
-        // few tiles and many rows (batched calls): split the rows over CTAs too
-        const int groups = (int)std::max<uint32_t>(1u, std::min<uint32_t>((uint32_t)rows, (4u * 148u + grid - 1) / grid));
-        g.rows_per_cta = std::max(1, (rows + groups - 1) / groups);
+        // few tiles and many rows (batched calls): split the rows over CTAs too,
+        // rows per CTA chosen to minimise waves x (rows per CTA + a per-CTA
+        // overhead of ~2 rows) over the resident slots (4 per SM): C3's 129
+        // CTAs x 256 rows went out as 645 CTAs of 52 rows = 2 waves for 1.09
+        uint32_t rpc = (uint32_t)std::max(rows, 1);
+        if (rows > 1) {
+            const double slots = 4.0 * num_sms();
+            double best = 1e300;
+            for (uint32_t r = 1; r <= (uint32_t)rows; ++r) {
+                const uint32_t gy_r = ((uint32_t)rows + r - 1) / r;
+                if (r > 1 && ((uint32_t)rows + r - 2) / (r - 1) == gy_r) continue;  // same split, fewer rows per CTA
+                const double cost = std::ceil((double)grid * gy_r / slots) * (r + 2.0);
+                if (cost < best - 1e-9) best = cost, rpc = r;
+            }
+        }
+        g.rows_per_cta = (int)rpc;
         const uint32_t gy = (uint32_t)std::max(1, (rows + g.rows_per_cta - 1) / g.rows_per_cta);
         lx::ms::lx_gather_agg<R, NCH, SIDE_A, GFORM, STRICT><<<dim3(grid, gy), lx::ms::kAggThreads, 0, st>>>(g);
     });
