@@ -261,6 +261,21 @@ struct Side {
     uint32_t m = 0;
 };
 
+// Plans up to this many anchors (n + k) build their two sides concurrently
+// (device API; see the core build).  C1 (2^20 + 2^20): 0.338 -> 0.271 ms; at
+// C4's 2 x 3 * 2^20 the forked build measured slower and erratic (3.14 ->
+// 3.29 / 4.40 ms: the side stream cannot reuse pool blocks freed on the other)
+constexpr size_t kForkSidesMax = size_t(1) << 21;
+
+// a second, non-blocking stream of the calling thread on the current device
+cudaStream_t side_stream() {
+    thread_local cudaStream_t ss[64] = {};
+    const int d = current_device();
+    if (d < 0 || d >= 64) fail(LAPLEX_E_CUDA, "device index");
+    if (!ss[d]) ck(cudaStreamCreateWithFlags(&ss[d], cudaStreamNonBlocking), "cudaStreamCreate");
+    return ss[d];
+}
+
 // Sides up to this many elements permute directly (the whole vector is
 // L2-resident, 126 MB); larger ones go through the two-pass plan.
 constexpr uint32_t kDirectMax = 1u << 22;
@@ -827,11 +842,32 @@ laplex_plan create_plan(const R* a, uint32_t n, const R* b, uint32_t k, double t
         ck(cudaEventCreateWithFlags(&fev, cudaEventDisableTiming), "cudaEventCreate");
         ck(cudaEventRecord(fev, st), "cudaEventRecord");
     };
+    // Device API, small plans: the two sides' sorts are short launches that
+    // fill a fraction of the GPU (2^20 keys = 171 tiles for 444 CTA slots), so
+    // side a is built on a second stream, concurrently with side b.  Its
+    // buffers are handed back to `st` (freed there) after the join.
+    const bool fork = !ready && n > 0 && k > 0 && (size_t)n + k <= kForkSidesMax;
+    cudaStream_t st0 = fork ? side_stream() : st;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    if (fork) {
+        ck(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "cudaEventCreate");
+        ck(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "cudaEventCreate");
+        ck(cudaEventRecord(ev_fork, st), "cudaEventRecord");
+        ck(cudaStreamWaitEvent(st0, ev_fork, 0), "cudaStreamWaitEvent");
+    }
     if (ready) ck(cudaStreamWaitEvent(st, ready[0], 0), "cudaStreamWaitEvent");
-    build_side<R>(core->side[0], a, n, R(t), phi, bad.as<int>() + 0, st);
+    build_side<R>(core->side[0], a, n, R(t), phi, bad.as<int>() + 0, st0);
     if (ready) ck(cudaStreamWaitEvent(st, ready[1], 0), "cudaStreamWaitEvent");
     build_side<R>(core->side[1], b, k, R(t), psi, bad.as<int>() + 1, st,
                   early ? std::function<void()>(flags_out) : std::function<void()>());
+    if (fork) {
+        ck(cudaEventRecord(ev_join, st0), "cudaEventRecord");
+        ck(cudaStreamWaitEvent(st, ev_join, 0), "cudaStreamWaitEvent");
+        cudaEventDestroy(ev_fork);
+        cudaEventDestroy(ev_join);
+        Side& s0 = core->side[0];
+        for (DBuf* d : {&s0.vals, &s0.perm, &s0.cph, &s0.sph, &s0.spos, &s0.sdst}) d->st = st;
+    }
     if (!early && phi) {
         launch_finite<R>(phi, n, bad.as<int>() + 2, st);
         launch_finite<R>(psi, k, bad.as<int>() + 2, st);
