@@ -1367,6 +1367,16 @@ void backward_impl(const View<R>& v, const R* X, const R* G, int rows, R* xbar, 
     bwd_end<R, NCH>(*w, nullptr, xbar, abar, bbar, phibar, psibar, st);
 }
 
+// Batched calls: the per-call working set grows with rows x (n + k) (sorted
+// payloads, bucket-staged copies and outputs, ~24 B per row-element), far
+// beyond the plan's per-anchor reservation; without holding it the pool grows
+// on demand inside the step (C2 device step 48 -> 83..195 ms in some runs:
+// host-side mapping stalls between kernels).
+template <class R>
+void reserve_batch(const Core& c, size_t rows, cudaStream_t st) {
+    if (rows > 1) reserve_pool(((size_t)c.side[0].m + c.side[1].m) * rows, sizeof(R), 24, st);
+}
+
 template <class R>
 void do_apply(laplex_plan_s* p, unsigned flags, const R* X, size_t rows, R* Y, cudaStream_t st) {
     Core& c = *p->core;
@@ -1376,6 +1386,7 @@ void do_apply(laplex_plan_s* p, unsigned flags, const R* X, size_t rows, R* Y, c
     if (trn && ph) fail(LAPLEX_E_INVALID_ARGUMENT, "phased transpose is not part of the reference API");
     if (rows == 0) return;
     if (rows > 0x7fffffff) fail(LAPLEX_E_INVALID_SIZE, "too many rows");
+    reserve_batch<R>(c, rows, st);
     View<R> v = view<R>(c, p->swapped, st, rows);
     Core* save = (flags & LAPLEX_SAVE_X) && !trn ? &c : nullptr;
     if (trn)
@@ -1397,6 +1408,7 @@ void do_backward(laplex_plan_s* p, unsigned flags, const R* X, const R* G, size_
     const bool ph = flags & LAPLEX_PHASED;
     if (ph && !c.phased) fail(LAPLEX_E_PHASE_ABSENT, "phased_matvec_vjp: operator has no phases");
     if (!ph && c.phased) fail(LAPLEX_E_PHASE_PRESENT, "matvec_vjp: use phased_matvec_vjp");
+    reserve_batch<R>(c, rows, st);
     View<R> v = view<R>(c, p->swapped, st, rows);
     if (rows == 0) {
         if (before_g) before_g();
